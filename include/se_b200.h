@@ -1,0 +1,213 @@
+/*
+ * se_b200.h -- C ABI of the B200-native Spectral Ewald (SE) hot path.
+ *
+ * Drop-in boundary for the reference package `pmewald` (arXiv 1712.04732,
+ * /root/reference/pkg/src/pmewald).  Every entry point names the reference
+ * interface it replaces (file:line).  Plain pointers and sizes only; no
+ * torch / numpy types.  All compute runs in hand-written sm_100a CUDA
+ * kernels plus cuFFT; there is no CPU fallback for any compute entry point.
+ *
+ * Conventions
+ *  - Positions are (N,3) row-major float64 ("AoS", as ParticleSystem.positions,
+ *    core.py:57-86); charges and potentials are (N,) float64.
+ *  - Grids use the reference's numpy layout: C order [ix][iy][iz] of
+ *    Grid.shape (sekspace.py:64-66): M on periodic axes, Mt = M + P on free
+ *    axes; the first D axes are periodic (core.py:44-46).
+ *  - Functions suffixed _dev take DEVICE pointers (on the plan's device and
+ *    ordered on the plan's stream); functions suffixed _host take HOST
+ *    pointers and include the host<->device copies.
+ *  - Every call returns an int status; SE_OK == 0.  se_last_error() returns
+ *    the thread-local message of the last failure.  Status -> Python
+ *    exception mapping (core.py:23-28):
+ *        SE_EINVAL    -> ValueError
+ *        SE_ECONFIG   -> ConfigurationError(ValueError)
+ *        SE_ESINGULAR -> SingularConfigurationError(ValueError)
+ *        SE_ENUMERIC  -> AssertionError   (numerical guards)
+ *        SE_EDEVICE   -> RuntimeError     (CUDA / cuFFT failure, no device)
+ */
+#ifndef SE_B200_H
+#define SE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SE_OK 0
+#define SE_EINVAL 1
+#define SE_ECONFIG 2
+#define SE_ESINGULAR 3
+#define SE_ENUMERIC 4
+#define SE_EDEVICE 5
+
+/* window kinds: windows.py:24-27 ("gaussian", "kb", "bm") */
+#define SE_WINDOW_GAUSSIAN 0
+#define SE_WINDOW_KB 1
+#define SE_WINDOW_BM 2
+
+/* timings[] slots, the reference's stage keys (sekspace.py:359-388, core.py:211-213) */
+#define SE_T_REALSPACE 0
+#define SE_T_SPREAD 1
+#define SE_T_AFT 2
+#define SE_T_SCALE 3
+#define SE_T_AIFT 4
+#define SE_T_GATHER 5
+#define SE_T_PRECOMPUTE 6
+#define SE_T_COUNT 7
+
+/* SEParams (core.py:89-116), field for field. */
+typedef struct se_params {
+    double xi;      /* Ewald splitting parameter */
+    double rc;      /* real-space cutoff */
+    int32_t M;      /* grid points per periodic axis (even) */
+    int32_t P;      /* window support points */
+    int32_t window; /* SE_WINDOW_* */
+    int32_t nI;     /* low-mode block half width (D in {1,2}) */
+    double shape;   /* m (gaussian) or beta (kb, bm) */
+    double s0;      /* zero-block upsampling */
+    double s;       /* I-block upsampling */
+    double R;       /* truncation radius of the free-space kernel (D < 3) */
+    double eps;     /* accuracy target the set was built for */
+} se_params_t;
+
+/* Grid (sekspace.py:36-70) as built by Grid.build for (L, params, D). */
+typedef struct se_grid {
+    int32_t D, M, P, Mt, g0, gs;
+    int32_t shape[3];
+    double L, h, Lt, R;
+    double offsets[3];
+} se_grid_t;
+
+typedef struct se_plan *se_plan_t;
+
+/* ------------------------------------------------------------------ *
+ * Host-side planning (no device needed).                              *
+ * ------------------------------------------------------------------ */
+
+/* SEParams.validate (core.py:118-138).  SE_EINVAL with the reference's message. */
+int se_params_validate(const se_params_t *p, double L, int D);
+/* Grid.build (sekspace.py:53-62). */
+int se_grid_build(int D, double L, const se_params_t *p, se_grid_t *out);
+/* aft.padded_size (aft.py:76-84) and aft.next_even_smooth (aft.py:68-73). */
+int se_padded_size(double s, int32_t n, int32_t *out);
+int se_next_even_smooth(int32_t n, int32_t *out);
+/* precompute_truncated_greens geometry (sekspace.py:266-279): nconv, fine g0, R. */
+int se_d0_kernel_geometry(double L, int32_t M, int32_t P, double s0, double rc,
+                          int32_t *nconv, int32_t *g0, double *R);
+/* Mode partition counts of ModePartition.build (aft.py:102-117). */
+int se_mode_partition_counts(int32_t M, int D, int32_t nI, int64_t *nI_rows, int64_t *nJ_rows);
+/* Window tables used by the plan (windows.py:242-257): real-space values and
+ * Fourier transforms (BM by long-double Gauss-Legendre quadrature,
+ * windows.py:175-239).  h is the grid spacing, w = P*h/2. */
+int se_window_eval(int window, int32_t P, double h, double shape,
+                   const double *x, int64_t n, double *out);
+int se_window_fourier(int window, int32_t P, double h, double shape,
+                      const double *k, int64_t n, double *out);
+/* greens.zero_mode_values (greens.py:48-85). */
+int se_greens_zero_mode(int D, double R, const double *kappa, int64_t n, double *out);
+
+/* ------------------------------------------------------------------ *
+ * Plan: device resources (tables, cuFFT plans, D=0 kernel, buffers).   *
+ * Mirrors the reference's caches (sekspace.py:97, windows.py:169-172). *
+ * ------------------------------------------------------------------ */
+
+/* Validate (core.py:118-138), build the grid (sekspace.py:53-62) and bind
+ * the plan to `device`.  Tables / FFT plans are created on first use. */
+int se_plan_create(se_plan_t *plan, int D, double L, const se_params_t *p, int device);
+int se_plan_destroy(se_plan_t plan);
+/* Stream for all subsequent calls (cudaStream_t; 0 = the legacy default
+ * stream).  Until it is called the plan uses a stream of its own. */
+int se_plan_set_stream(se_plan_t plan, void *stream);
+int se_plan_grid(se_plan_t plan, se_grid_t *out);
+/* Number of kernel launches issued by this plan since creation (for the bench). */
+int se_plan_launch_count(se_plan_t plan, int64_t *count);
+/* Warning bits raised by the last total-potential call: bit 0 = the system is
+ * not charge neutral in free space (core.py:185-189 warns instead of raising). */
+int se_plan_warnings(se_plan_t plan, int *flags);
+/* Per-kernel device timing of the hot kernels, for roofline reporting:
+ * CUDA events recorded on the plan's stream around each launch when
+ * profiling is on; times accumulate (ms) with launch counts per slot. */
+#define SE_K_REALSPACE 0 /* real-space erfc pair kernel */
+#define SE_K_SPREAD 1    /* spreading kernel */
+#define SE_K_GATHER 2    /* gathering kernel */
+#define SE_K_KSPACE 3    /* k-space stage (cuFFT + multiplier kernels) */
+#define SE_K_SORT 4      /* particle binning (keys, radix sort, records, units) */
+#define SE_K_COUNT 5
+int se_plan_set_profiling(se_plan_t plan, int on);
+int se_plan_kernel_times(se_plan_t plan, double *ms, int64_t *launches);
+/* Number of ordered in-cutoff pairs (r < rc, r >= 1e-14) the real-space sum
+ * evaluates: the unit of the real-space roofline (cell path only). */
+int se_realspace_pair_count_dev(se_plan_t plan, const double *pos, const double *q, int64_t N,
+                                int64_t *pairs);
+/* Truncated-kernel geometry the plan uses for D = 0 (sekspace.py:266-279). */
+int se_plan_d0_geometry(se_plan_t plan, int32_t *nconv, int32_t *g0, double *R);
+
+/* sekspace.spread (sekspace.py:130-156): grid = sum_n q_n w (x) w (x) w.
+ * grid_out holds prod(Grid.shape) float64 and is overwritten. */
+int se_spread_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *grid_out);
+/* aft_forward -> scale -> aft_inverse -> real part (sekspace.py:369-381), or the
+ * D=0 precomputed-kernel path _kspace_freespace_kernel (sekspace.py:301-337)
+ * when D == 0 and use_kernel != 0.  In place on a Grid.shape float64 grid. */
+int se_kspace_apply_dev(se_plan_t plan, double *grid, int use_kernel, double *timings);
+/* sekspace.gather (sekspace.py:159-178), including the h^3 weight.
+ * accumulate != 0 adds into phi instead of overwriting. */
+int se_gather_dev(se_plan_t plan, const double *grid, const double *pos, int64_t N,
+                  double *phi, int accumulate);
+/* sekspace.se_kspace (sekspace.py:340-389): spread, k-space stage, gather. */
+int se_kspace_potential_dev(se_plan_t plan, const double *pos, const double *q, int64_t N,
+                            double *phi, int use_kernel, double *timings);
+/* realspace.real_space_sum (realspace.py:168-180); add_self != 0 also adds
+ * realspace.self_term (realspace.py:183-185).  SE_ESINGULAR on coincident
+ * particles (realspace.py:121-122,157,161). */
+int se_realspace_dev(se_plan_t plan, const double *pos, const double *q, int64_t N,
+                     double *phi, int add_self);
+/* core.total_potential (core.py:194-216): phi = phi_R + phi_F + phi_self. */
+int se_total_potential_dev(se_plan_t plan, const double *pos, const double *q, int64_t N,
+                           double *phi, double *timings);
+
+/* Sharded variants for one-process-per-GPU runs: every rank holds all N
+ * particles; rank r of `world` computes the share of particles it owns
+ * (a contiguous range of the cell-sorted order) and writes only those
+ * entries of phi (others are zeroed), so a sum-all-reduce of phi over
+ * ranks gives core.total_potential.  The spread grid of a shard is partial:
+ * the caller sum-all-reduces it before se_kspace_apply_dev. */
+int se_spread_shard_dev(se_plan_t plan, const double *pos, const double *q, int64_t N,
+                        int rank, int world, double *grid_out);
+int se_gather_shard_dev(se_plan_t plan, const double *grid, const double *pos, int64_t N,
+                        int rank, int world, double *phi, int accumulate);
+int se_realspace_shard_dev(se_plan_t plan, const double *pos, const double *q, int64_t N,
+                           int rank, int world, double *phi, int add_self);
+
+/* realspace.self_term (realspace.py:183-185): out = -2 xi q / sqrt(pi), on the
+ * current CUDA device.  _dev: device pointers on `stream` (cudaStream_t). */
+int se_self_term_dev(const double *q, int64_t N, double xi, double *out, void *stream);
+int se_self_term_host(const double *q, int64_t N, double xi, double *out);
+
+/* core.total_potential through HOST buffers: H2D copies of pos/q, the device
+ * pipeline, and the D2H copy of phi, all on the plan's stream. */
+int se_total_potential_host(se_plan_t plan, const double *pos, const double *q, int64_t N,
+                            double *phi, double *timings);
+/* sekspace.se_kspace / spread / gather / real_space_sum through host buffers. */
+int se_kspace_potential_host(se_plan_t plan, const double *pos, const double *q, int64_t N,
+                             double *phi, int use_kernel, double *timings);
+int se_spread_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *grid_out);
+int se_gather_host(se_plan_t plan, const double *grid, const double *pos, int64_t N, double *phi);
+int se_kspace_apply_host(se_plan_t plan, double *grid, int use_kernel);
+int se_realspace_host(se_plan_t plan, const double *pos, const double *q, int64_t N,
+                      double *phi, int add_self);
+
+/* precompute_truncated_greens (sekspace.py:257-298): the real half-spectrum
+ * table (nconv, nconv, nconv/2+1), computed on the device and copied to host
+ * (`out` must hold nconv*nconv*(nconv/2+1) doubles). */
+int se_d0_kernel_table_host(se_plan_t plan, double *out);
+
+/* Thread-local message of the last failing call. */
+const char *se_last_error(void);
+/* Library version string. */
+const char *se_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SE_B200_H */

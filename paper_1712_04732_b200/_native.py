@@ -1,0 +1,227 @@
+"""ctypes binding of the C ABI in include/se_b200.h (libse_b200.so).
+
+The library is built in-tree (`paper_1712_04732_b200/_lib/libse_b200.so`,
+see csrc/Makefile).  There is no Python or CPU fallback for any compute
+entry point: if the library is missing, every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libse_b200.so")
+
+SE_OK, SE_EINVAL, SE_ECONFIG, SE_ESINGULAR, SE_ENUMERIC, SE_EDEVICE = range(6)
+WINDOWS = {"gaussian": 0, "kb": 1, "bm": 2}
+TIMING_KEYS = ("realspace", "spread", "aft", "scale", "aift", "gather", "precompute")
+KERNEL_SLOTS = ("realspace", "spread", "gather", "kspace", "sort")
+
+c_double_p = ctypes.POINTER(ctypes.c_double)
+c_int32_p = ctypes.POINTER(ctypes.c_int32)
+c_int64_p = ctypes.POINTER(ctypes.c_int64)
+
+
+class se_params_t(ctypes.Structure):
+    _fields_ = [("xi", ctypes.c_double), ("rc", ctypes.c_double), ("M", ctypes.c_int32),
+                ("P", ctypes.c_int32), ("window", ctypes.c_int32), ("nI", ctypes.c_int32),
+                ("shape", ctypes.c_double), ("s0", ctypes.c_double), ("s", ctypes.c_double),
+                ("R", ctypes.c_double), ("eps", ctypes.c_double)]
+
+
+class se_grid_t(ctypes.Structure):
+    _fields_ = [("D", ctypes.c_int32), ("M", ctypes.c_int32), ("P", ctypes.c_int32),
+                ("Mt", ctypes.c_int32), ("g0", ctypes.c_int32), ("gs", ctypes.c_int32),
+                ("shape", ctypes.c_int32 * 3), ("L", ctypes.c_double), ("h", ctypes.c_double),
+                ("Lt", ctypes.c_double), ("R", ctypes.c_double), ("offsets", ctypes.c_double * 3)]
+
+
+_P = ctypes.c_void_p
+# name -> argtypes (restype is always c_int unless listed in _RESTYPES)
+SIGNATURES = {
+    "se_params_validate": [ctypes.POINTER(se_params_t), ctypes.c_double, ctypes.c_int],
+    "se_grid_build": [ctypes.c_int, ctypes.c_double, ctypes.POINTER(se_params_t), ctypes.POINTER(se_grid_t)],
+    "se_padded_size": [ctypes.c_double, ctypes.c_int32, c_int32_p],
+    "se_next_even_smooth": [ctypes.c_int32, c_int32_p],
+    "se_d0_kernel_geometry": [ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                              ctypes.c_double, c_int32_p, c_int32_p, c_double_p],
+    "se_mode_partition_counts": [ctypes.c_int32, ctypes.c_int, ctypes.c_int32, c_int64_p, c_int64_p],
+    "se_window_eval": [ctypes.c_int, ctypes.c_int32, ctypes.c_double, ctypes.c_double, _P,
+                       ctypes.c_int64, _P],
+    "se_window_fourier": [ctypes.c_int, ctypes.c_int32, ctypes.c_double, ctypes.c_double, _P,
+                          ctypes.c_int64, _P],
+    "se_greens_zero_mode": [ctypes.c_int, ctypes.c_double, _P, ctypes.c_int64, _P],
+    "se_plan_create": [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_double, ctypes.POINTER(se_params_t),
+                       ctypes.c_int],
+    "se_plan_destroy": [_P],
+    "se_plan_set_stream": [_P, _P],
+    "se_plan_grid": [_P, ctypes.POINTER(se_grid_t)],
+    "se_plan_launch_count": [_P, c_int64_p],
+    "se_plan_warnings": [_P, ctypes.POINTER(ctypes.c_int)],
+    "se_plan_d0_geometry": [_P, c_int32_p, c_int32_p, c_double_p],
+    "se_plan_set_profiling": [_P, ctypes.c_int],
+    "se_plan_kernel_times": [_P, c_double_p, c_int64_p],
+    "se_realspace_pair_count_dev": [_P, _P, _P, ctypes.c_int64, c_int64_p],
+    "se_spread_dev": [_P, _P, _P, ctypes.c_int64, _P],
+    "se_kspace_apply_dev": [_P, _P, ctypes.c_int, _P],
+    "se_gather_dev": [_P, _P, _P, ctypes.c_int64, _P, ctypes.c_int],
+    "se_kspace_potential_dev": [_P, _P, _P, ctypes.c_int64, _P, ctypes.c_int, _P],
+    "se_realspace_dev": [_P, _P, _P, ctypes.c_int64, _P, ctypes.c_int],
+    "se_total_potential_dev": [_P, _P, _P, ctypes.c_int64, _P, _P],
+    "se_spread_shard_dev": [_P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P],
+    "se_gather_shard_dev": [_P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int],
+    "se_realspace_shard_dev": [_P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int],
+    "se_total_potential_host": [_P, _P, _P, ctypes.c_int64, _P, _P],
+    "se_kspace_potential_host": [_P, _P, _P, ctypes.c_int64, _P, ctypes.c_int, _P],
+    "se_spread_host": [_P, _P, _P, ctypes.c_int64, _P],
+    "se_gather_host": [_P, _P, _P, ctypes.c_int64, _P],
+    "se_kspace_apply_host": [_P, _P, ctypes.c_int],
+    "se_realspace_host": [_P, _P, _P, ctypes.c_int64, _P, ctypes.c_int],
+    "se_self_term_host": [_P, ctypes.c_int64, ctypes.c_double, _P],
+    "se_self_term_dev": [_P, ctypes.c_int64, ctypes.c_double, _P, _P],
+    "se_d0_kernel_table_host": [_P, _P],
+    "se_last_error": [],
+    "se_version": [],
+}
+_RESTYPES = {"se_last_error": ctypes.c_char_p, "se_version": ctypes.c_char_p}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load libse_b200.so (raises OSError if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise OSError(f"SE B200 library not built: {LIB_PATH} (run __graft_entry__.build())")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, args in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = _RESTYPES.get(name, ctypes.c_int)
+            _lib = lib
+    return _lib
+
+
+def _errors():
+    from . import core
+    return {SE_EINVAL: ValueError, SE_ECONFIG: core.ConfigurationError,
+            SE_ESINGULAR: core.SingularConfigurationError, SE_ENUMERIC: AssertionError,
+            SE_EDEVICE: RuntimeError}
+
+
+def call(name, *args):
+    """Call a C-ABI function and map a non-zero status to the reference's exception."""
+    lib = load()
+    st = getattr(lib, name)(*args)
+    if st != SE_OK:
+        msg = lib.se_last_error().decode(errors="replace")
+        raise _errors().get(st, RuntimeError)(msg)
+    return st
+
+
+def params_struct(p) -> se_params_t:
+    """SEParams -> se_params_t (window kinds as in windows.py:24-27)."""
+    if p.window not in WINDOWS:
+        raise ValueError(f"unknown window {p.window!r}")
+    return se_params_t(float(p.xi), float(p.rc), int(p.M), int(p.P), WINDOWS[p.window],
+                       int(p.nI), float(p.shape), float(p.s0), float(p.s), float(p.R), float(p.eps))
+
+
+def ptr(a) -> ctypes.c_void_p:
+    """Data pointer of a C-contiguous numpy array or a CUDA torch tensor."""
+    if isinstance(a, np.ndarray):
+        return ctypes.c_void_p(a.ctypes.data)
+    return ctypes.c_void_p(a.data_ptr())
+
+
+# ----------------------------------------------------------------- plan cache
+class Plan:
+    """Owns one se_plan_t (device tables, cuFFT plans, buffers) for a
+    (D, L, SEParams, device) key -- the analogue of the reference's
+    module-level caches (sekspace.py:97, windows.py:169-172)."""
+
+    def __init__(self, D: int, L: float, params, device: int = 0):
+        self.D, self.L, self.device = int(D), float(L), int(device)
+        self._p = params_struct(params)
+        h = ctypes.c_void_p()
+        call("se_plan_create", ctypes.byref(h), self.D, self.L, ctypes.byref(self._p), self.device)
+        self.handle = h
+
+    def grid(self) -> se_grid_t:
+        g = se_grid_t()
+        call("se_plan_grid", self.handle, ctypes.byref(g))
+        return g
+
+    def set_stream(self, stream_ptr: int):
+        """Order subsequent calls on this cudaStream_t (0 = legacy default stream)."""
+        call("se_plan_set_stream", self.handle, ctypes.c_void_p(int(stream_ptr)))
+
+    def set_profiling(self, on: bool):
+        call("se_plan_set_profiling", self.handle, int(bool(on)))
+
+    def kernel_times(self):
+        """Accumulated (ms, launches) per SE_K_* slot since profiling was enabled."""
+        ms = (ctypes.c_double * 5)()
+        n = (ctypes.c_int64 * 5)()
+        call("se_plan_kernel_times", self.handle, ms, n)
+        return {k: (ms[i], n[i]) for i, k in enumerate(KERNEL_SLOTS)}
+
+    def launches(self) -> int:
+        n = ctypes.c_int64()
+        call("se_plan_launch_count", self.handle, ctypes.byref(n))
+        return int(n.value)
+
+    def warnings(self) -> int:
+        f = ctypes.c_int()
+        call("se_plan_warnings", self.handle, ctypes.byref(f))
+        return int(f.value)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value and _lib is not None:
+            try:
+                _lib.se_plan_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+_PLANS: dict = {}
+
+
+def plan_for(D, L, params, device: int = 0) -> Plan:
+    key = (int(D), float(L), params_key(params), int(device))
+    pl = _PLANS.get(key)
+    if pl is None:
+        pl = Plan(D, L, params, device)
+        _PLANS[key] = pl
+    return pl
+
+
+def params_key(p):
+    return (float(p.xi), float(p.rc), int(p.M), int(p.P), p.window, float(p.shape), float(p.s0),
+            float(p.s), int(p.nI), float(p.R), float(p.eps))
+
+
+def clear_plans():
+    _PLANS.clear()
+
+
+def timings_buffer():
+    return np.zeros(len(TIMING_KEYS))
+
+
+def fill_timings(timings: dict | None, buf, keys=TIMING_KEYS):
+    if timings is None:
+        return
+    for k in keys:
+        timings[k] = float(buf[TIMING_KEYS.index(k)])

@@ -1,0 +1,521 @@
+// extern "C" entry points of the SE B200 library (include/se_b200.h):
+// plan lifetime, stage calls on device pointers, fused pipelines
+// (se_kspace / total_potential), sharded variants and host-buffer variants.
+#include <cstring>
+
+#include "se_common.h"
+
+using namespace se;
+
+#define SE_API_BEGIN try {
+#define SE_API_END                            \
+    return SE_OK;                             \
+    }                                         \
+    catch (const se::Error &e) {              \
+        se::set_last_error(e.what());         \
+        return e.code;                        \
+    }                                         \
+    catch (const std::exception &e) {         \
+        se::set_last_error(e.what());         \
+        return SE_EDEVICE;                    \
+    }
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        SE_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) SE_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+se_plan *checked(se_plan_t p) {
+    if (!p) fail(SE_EINVAL, "null plan");
+    return p;
+}
+
+size_t grid_points(const se_plan *pl) { return (size_t)pl->g.shape[0] * pl->g.shape[1] * pl->g.shape[2]; }
+
+// charge sums and box check in one pass: [sum q, sum |q|, #outside [0,L)]
+__global__ void check_kernel(const double *__restrict__ pos, const double *__restrict__ q, int64_t N, double L,
+                             double *__restrict__ out) {
+    double s = 0.0, a = 0.0, bad = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        double qi = q[i];
+        s += qi;
+        a += fabs(qi);
+        for (int ax = 0; ax < 3; ++ax) {
+            double x = pos[3 * i + ax];
+            if (!(x >= 0.0 && x < L)) bad += 1.0;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, s);
+        atomicAdd(out + 1, a);
+        atomicAdd(out + 2, bad);
+    }
+}
+
+// core.py:65-77 (box) and core.py:180-191 (neutrality): ValueError for D > 0,
+// a warning flag for D = 0.
+void check_system(se_plan *pl, const double *pos, const double *q, int64_t N, bool neutrality) {
+    pl->warnings = 0;
+    if (N <= 0) return;
+    pl->check.ensure(sizeof(double) * 4);
+    SE_CUDA(cudaMemsetAsync(pl->check.ptr, 0, sizeof(double) * 4, pl->stream));
+    int64_t blocks = (N + 255) / 256;
+    if (blocks > 1184) blocks = 1184;
+    check_kernel<<<(unsigned)blocks, 256, 0, pl->stream>>>(pos, q, N, pl->L, pl->check.as<double>());
+    SE_LAUNCH_CHECK();
+    pl->launches += 1;
+    double h[4];
+    SE_CUDA(cudaMemcpyAsync(h, pl->check.ptr, sizeof(double) * 4, cudaMemcpyDeviceToHost, pl->stream));
+    SE_CUDA(cudaStreamSynchronize(pl->stream));
+    if (h[2] > 0) fail(SE_EINVAL, "all coordinates must lie in [0, L)");
+    if (!neutrality) return;
+    double qabs = h[1] > 1.0 ? h[1] : 1.0;
+    if (std::fabs(h[0]) <= 1e-12 * qabs) return;
+    if (pl->D == 0)
+        pl->warnings |= 1;
+    else
+        fail(SE_EINVAL, "periodic Ewald summation requires a charge-neutral system");
+}
+
+void check_flag(se_plan *pl) {
+    int h = 0;
+    SE_CUDA(cudaMemcpyAsync(&h, pl->flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, pl->stream));
+    SE_CUDA(cudaStreamSynchronize(pl->stream));
+    if (h == 1) fail(SE_ESINGULAR, "coincident distinct particles");
+    if (h == 2) fail(SE_ESINGULAR, "particle coincides with an image");
+}
+
+struct Events {
+    bool on;
+    cudaStream_t st;
+    cudaEvent_t e[6];
+    int n = 0;
+    Events(bool enabled, cudaStream_t s) : on(enabled), st(s) {
+        if (on)
+            for (auto &x : e) SE_CUDA(cudaEventCreate(&x));
+    }
+    void mark() {
+        if (on) SE_CUDA(cudaEventRecord(e[n++], st));
+    }
+    double secs(int a, int b) {
+        float ms = 0;
+        SE_CUDA(cudaEventElapsedTime(&ms, e[a], e[b]));
+        return ms * 1e-3;
+    }
+    ~Events() {
+        if (on)
+            for (auto &x : e) cudaEventDestroy(x);
+    }
+};
+
+// spread -> k-space -> gather (sekspace.py:340-389); phi += or = phi_F
+void kspace_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, int use_kernel,
+                     double *timings, int accumulate, int rank, int world) {
+    double *grid = nullptr;
+    pl->grid_dev.ensure(sizeof(double) * grid_points(pl));
+    grid = pl->grid_dev.as<double>();
+    Events ev(timings != nullptr, pl->stream);
+    ev.mark();
+    spread_run(pl, pos, q, N, grid, 0, 1);  // every rank needs the full grid; see the shard API for splitting
+    ev.mark();
+    double kt[SE_T_COUNT] = {0};
+    prof_begin(pl, SE_K_KSPACE);
+    kspace_run(pl, grid, use_kernel, timings ? kt : nullptr);
+    prof_end(pl, SE_K_KSPACE);
+    ev.mark();
+    gather_run(pl, grid, pos, N, phi, accumulate, rank, world, false);
+    ev.mark();
+    prof_collect(pl);
+    if (timings) {
+        SE_CUDA(cudaStreamSynchronize(pl->stream));
+        timings[SE_T_SPREAD] = ev.secs(0, 1);
+        timings[SE_T_AFT] = kt[SE_T_AFT];
+        timings[SE_T_SCALE] = kt[SE_T_SCALE];
+        timings[SE_T_AIFT] = kt[SE_T_AIFT];
+        timings[SE_T_PRECOMPUTE] = kt[SE_T_PRECOMPUTE];
+        timings[SE_T_GATHER] = ev.secs(2, 3);
+    }
+}
+
+void total_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, double *timings) {
+    check_system(pl, pos, q, N, true);
+    Events ev(timings != nullptr, pl->stream);
+    ev.mark();
+    realspace_run(pl, pos, q, N, phi, 1, 0, 1);
+    ev.mark();
+    kspace_pipeline(pl, pos, q, N, phi, 1, timings, 1, 0, 1);
+    check_flag(pl);
+    prof_collect(pl);
+    if (timings) timings[SE_T_REALSPACE] = ev.secs(0, 1);
+}
+
+template <class T>
+T *stage_in(se_plan *pl, DevBuf &b, const T *host, size_t n) {
+    b.ensure(sizeof(T) * (n ? n : 1));
+    if (n) SE_CUDA(cudaMemcpyAsync(b.ptr, host, sizeof(T) * n, cudaMemcpyHostToDevice, pl->stream));
+    return b.as<T>();
+}
+
+void stage_out(se_plan *pl, void *host, const void *dev, size_t bytes) {
+    if (bytes) SE_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, pl->stream));
+    SE_CUDA(cudaStreamSynchronize(pl->stream));
+}
+
+// realspace.py:183-185: -2 xi q / sqrt(pi)
+__global__ void self_kernel(const double *__restrict__ q, int64_t N, double xi, double sqrtpi, double *__restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < N) out[i] = (-2.0 * xi * q[i]) / sqrtpi;
+}
+
+void check_shard(int rank, int world) {
+    if (world < 1 || rank < 0 || rank >= world) fail(SE_EINVAL, "invalid shard (rank, world)");
+}
+
+}  // namespace
+
+namespace se {
+void plan_release_device(se_plan *pl) {
+    for (cufftHandle h : {pl->fft_fwd, pl->fft_inv, pl->fft_rowJ, pl->fft_rowI, pl->fft_row0, pl->fft_c_fwd,
+                          pl->fft_c_inv, pl->fft_f_fwd, pl->fft_f_inv})
+        if (h) cufftDestroy(h);
+    for (Binning *b : {&pl->tbin, &pl->cbin})
+        for (DevBuf *d : {&b->keys, &b->keys_sorted, &b->idx, &b->idx_sorted, &b->counts, &b->starts, &b->units,
+                          &b->nunits, &b->cub_tmp, &b->rec})
+            d->release();
+    for (ModeTable *t : {&pl->tM, &pl->tg0, &pl->tgs, &pl->tMt, &pl->tNc, &pl->tNh}) {
+        t->k.release();
+        t->what.release();
+    }
+    for (DevBuf *d : {&pl->flag, &pl->spec, &pl->spec2, &pl->spec3, &pl->work, &pl->grid_tmp, &pl->rows_I,
+                      &pl->ghat, &pl->grid_dev, &pl->io_pos, &pl->io_q, &pl->io_phi, &pl->io_grid, &pl->check})
+        d->release();
+    if (pl->own_stream) cudaStreamDestroy(pl->own_stream);
+}
+}  // namespace se
+
+extern "C" {
+
+int se_plan_create(se_plan_t *plan, int D, double L, const se_params_t *p, int device) {
+    SE_API_BEGIN
+    if (!plan || !p) fail(SE_EINVAL, "null argument");
+    *plan = nullptr;
+    validate(*p, L, D);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        fail(SE_EDEVICE, "no CUDA device available (the SE B200 library has no CPU fallback)");
+    }
+    if (device < 0 || device >= ndev) fail(SE_EINVAL, "device ordinal out of range");
+    DeviceGuard dg(device);
+    se_plan *pl = new se_plan();
+    pl->D = D;
+    pl->L = L;
+    pl->p = *p;
+    pl->device = device;
+    try {
+        pl->g = build_grid(D, L, *p);
+        SE_CUDA(cudaStreamCreateWithFlags(&pl->own_stream, cudaStreamNonBlocking));
+        pl->stream = pl->own_stream;
+    } catch (...) {
+        delete pl;
+        throw;
+    }
+    *plan = pl;
+    SE_API_END
+}
+
+int se_plan_destroy(se_plan_t plan) {
+    SE_API_BEGIN
+    if (!plan) return SE_OK;
+    {
+        DeviceGuard dg(plan->device);
+        cudaStreamSynchronize(plan->stream);
+        plan_release_device(plan);
+    }
+    delete plan;
+    SE_API_END
+}
+
+int se_plan_set_stream(se_plan_t plan, void *stream) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    pl->stream = (cudaStream_t)stream;  // 0 is the legacy default stream
+    SE_API_END
+}
+
+int se_plan_set_profiling(se_plan_t plan, int on) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    pl->prof = on != 0;
+    for (int i = 0; i < SE_K_COUNT; ++i) {
+        pl->pms[i] = 0.0;
+        pl->pcount[i] = 0;
+        pl->pending[i] = false;
+    }
+    SE_API_END
+}
+
+int se_plan_kernel_times(se_plan_t plan, double *ms, int64_t *launches) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    prof_collect(pl);
+    for (int i = 0; i < SE_K_COUNT; ++i) {
+        if (ms) ms[i] = pl->pms[i];
+        if (launches) launches[i] = pl->pcount[i];
+    }
+    SE_API_END
+}
+
+int se_realspace_pair_count_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, int64_t *pairs) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    long long n = 0;
+    realspace_pair_count(pl, pos, q, N, &n);
+    *pairs = n;
+    SE_API_END
+}
+
+int se_plan_grid(se_plan_t plan, se_grid_t *out) {
+    SE_API_BEGIN
+    *out = checked(plan)->g;
+    SE_API_END
+}
+
+int se_plan_launch_count(se_plan_t plan, int64_t *count) {
+    SE_API_BEGIN
+    *count = checked(plan)->launches;
+    SE_API_END
+}
+
+int se_plan_warnings(se_plan_t plan, int *flags) {
+    SE_API_BEGIN
+    *flags = checked(plan)->warnings;
+    SE_API_END
+}
+
+int se_spread_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *grid_out) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    spread_run(pl, pos, q, N, grid_out, 0, 1);
+    SE_API_END
+}
+
+int se_spread_shard_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, int rank, int world,
+                        double *grid_out) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    check_shard(rank, world);
+    DeviceGuard dg(pl->device);
+    spread_run(pl, pos, q, N, grid_out, rank, world);
+    prof_collect(pl);
+    SE_API_END
+}
+
+int se_kspace_apply_dev(se_plan_t plan, double *grid, int use_kernel, double *timings) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    prof_begin(pl, SE_K_KSPACE);
+    kspace_run(pl, grid, use_kernel, timings);
+    prof_end(pl, SE_K_KSPACE);
+    prof_collect(pl);
+    SE_API_END
+}
+
+int se_gather_dev(se_plan_t plan, const double *grid, const double *pos, int64_t N, double *phi, int accumulate) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    gather_run(pl, grid, pos, N, phi, accumulate, 0, 1, true);
+    SE_API_END
+}
+
+int se_gather_shard_dev(se_plan_t plan, const double *grid, const double *pos, int64_t N, int rank, int world,
+                        double *phi, int accumulate) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    check_shard(rank, world);
+    DeviceGuard dg(pl->device);
+    gather_run(pl, grid, pos, N, phi, accumulate, rank, world, true);
+    prof_collect(pl);
+    SE_API_END
+}
+
+int se_kspace_potential_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *phi, int use_kernel,
+                            double *timings) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    kspace_pipeline(pl, pos, q, N, phi, use_kernel, timings, 0, 0, 1);
+    SE_API_END
+}
+
+int se_realspace_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *phi, int add_self) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    realspace_run(pl, pos, q, N, phi, add_self, 0, 1);
+    check_flag(pl);
+    SE_API_END
+}
+
+int se_realspace_shard_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, int rank, int world,
+                           double *phi, int add_self) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    check_shard(rank, world);
+    DeviceGuard dg(pl->device);
+    realspace_run(pl, pos, q, N, phi, add_self, rank, world);
+    check_flag(pl);
+    prof_collect(pl);
+    SE_API_END
+}
+
+int se_total_potential_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *phi,
+                           double *timings) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    total_pipeline(pl, pos, q, N, phi, timings);
+    SE_API_END
+}
+
+int se_total_potential_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *phi,
+                            double *timings) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    const double *dp = stage_in(pl, pl->io_pos, pos, 3 * (size_t)N);
+    const double *dq = stage_in(pl, pl->io_q, q, (size_t)N);
+    pl->io_phi.ensure(sizeof(double) * (N ? N : 1));
+    total_pipeline(pl, dp, dq, N, pl->io_phi.as<double>(), timings);
+    stage_out(pl, phi, pl->io_phi.ptr, sizeof(double) * N);
+    SE_API_END
+}
+
+int se_kspace_potential_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *phi,
+                             int use_kernel, double *timings) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    const double *dp = stage_in(pl, pl->io_pos, pos, 3 * (size_t)N);
+    const double *dq = stage_in(pl, pl->io_q, q, (size_t)N);
+    pl->io_phi.ensure(sizeof(double) * (N ? N : 1));
+    kspace_pipeline(pl, dp, dq, N, pl->io_phi.as<double>(), use_kernel, timings, 0, 0, 1);
+    stage_out(pl, phi, pl->io_phi.ptr, sizeof(double) * N);
+    SE_API_END
+}
+
+int se_spread_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *grid_out) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    const double *dp = stage_in(pl, pl->io_pos, pos, 3 * (size_t)N);
+    const double *dq = stage_in(pl, pl->io_q, q, (size_t)N);
+    pl->io_grid.ensure(sizeof(double) * grid_points(pl));
+    spread_run(pl, dp, dq, N, pl->io_grid.as<double>(), 0, 1);
+    stage_out(pl, grid_out, pl->io_grid.ptr, sizeof(double) * grid_points(pl));
+    SE_API_END
+}
+
+int se_gather_host(se_plan_t plan, const double *grid, const double *pos, int64_t N, double *phi) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    const double *dg_ = stage_in(pl, pl->io_grid, grid, grid_points(pl));
+    const double *dp = stage_in(pl, pl->io_pos, pos, 3 * (size_t)N);
+    pl->io_phi.ensure(sizeof(double) * (N ? N : 1));
+    gather_run(pl, dg_, dp, N, pl->io_phi.as<double>(), 0, 0, 1, true);
+    stage_out(pl, phi, pl->io_phi.ptr, sizeof(double) * N);
+    SE_API_END
+}
+
+int se_kspace_apply_host(se_plan_t plan, double *grid, int use_kernel) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    double *d = stage_in(pl, pl->io_grid, (const double *)grid, grid_points(pl));
+    kspace_run(pl, d, use_kernel, nullptr);
+    stage_out(pl, grid, d, sizeof(double) * grid_points(pl));
+    SE_API_END
+}
+
+int se_realspace_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *phi, int add_self) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    const double *dp = stage_in(pl, pl->io_pos, pos, 3 * (size_t)N);
+    const double *dq = stage_in(pl, pl->io_q, q, (size_t)N);
+    pl->io_phi.ensure(sizeof(double) * (N ? N : 1));
+    realspace_run(pl, dp, dq, N, pl->io_phi.as<double>(), add_self, 0, 1);
+    check_flag(pl);
+    stage_out(pl, phi, pl->io_phi.ptr, sizeof(double) * N);
+    SE_API_END
+}
+
+int se_d0_kernel_table_host(se_plan_t plan, double *out) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    if (pl->D != 0) fail(SE_EINVAL, "the truncated-kernel table exists for D = 0 only");
+    DeviceGuard dg(pl->device);
+    d0_kernel_prepare(pl, nullptr);
+    size_t n = (size_t)pl->nconv * pl->nconv * (pl->nconv / 2 + 1);
+    stage_out(pl, out, pl->ghat.ptr, sizeof(double) * n);
+    SE_API_END
+}
+
+int se_plan_d0_geometry(se_plan_t plan, int32_t *nconv, int32_t *g0, double *R) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    D0Geom d = d0_geometry(pl->g.L, pl->g.M, pl->g.P, pl->p.s0, pl->p.rc, true);
+    *nconv = d.nconv;
+    *g0 = d.g0;
+    *R = d.R;
+    SE_API_END
+}
+
+int se_self_term_dev(const double *q, int64_t N, double xi, double *out, void *stream) {
+    SE_API_BEGIN
+    if (N > 0) {
+        self_kernel<<<(unsigned)((N + 255) / 256), 256, 0, (cudaStream_t)stream>>>(q, N, xi, std::sqrt(M_PI), out);
+        SE_LAUNCH_CHECK();
+    }
+    SE_API_END
+}
+
+int se_self_term_host(const double *q, int64_t N, double xi, double *out) {
+    SE_API_BEGIN
+    if (N <= 0) return SE_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        fail(SE_EDEVICE, "no CUDA device available (the SE B200 library has no CPU fallback)");
+    }
+    double *d = nullptr;
+    SE_CUDA(cudaMalloc(&d, sizeof(double) * 2 * N));
+    SE_CUDA(cudaMemcpy(d, q, sizeof(double) * N, cudaMemcpyHostToDevice));
+    self_kernel<<<(unsigned)((N + 255) / 256), 256>>>(d, N, xi, std::sqrt(M_PI), d + N);
+    cudaError_t e = cudaMemcpy(out, d + N, sizeof(double) * N, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    SE_CUDA(e);
+    SE_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,238 @@
+// Internal declarations shared by the SE B200 library translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/se_b200.h"
+
+namespace se {
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string &msg) { throw Error(code, msg); }
+
+void set_last_error(const std::string &msg);
+
+#define SE_CUDA(call)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            ::se::fail(SE_EDEVICE, std::string("CUDA error: ") + cudaGetErrorString(e_) \
+                                       + " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+    } while (0)
+
+#define SE_CUFFT(call)                                                                  \
+    do {                                                                                \
+        cufftResult r_ = (call);                                                        \
+        if (r_ != CUFFT_SUCCESS)                                                        \
+            ::se::fail(SE_EDEVICE, std::string("cuFFT error ") + std::to_string((int)r_) \
+                                       + " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+    } while (0)
+
+#define SE_LAUNCH_CHECK() SE_CUDA(cudaGetLastError())
+
+// ------------------------------------------------------------ host planning
+int padded_size(double s, int n);
+int next_even_smooth(int n);
+void validate(const se_params_t &p, double L, int D);
+se_grid_t build_grid(int D, double L, const se_params_t &p);
+struct D0Geom { int nconv, g0; double R; };
+D0Geom d0_geometry(double L, int M, int P, double s0, double rc, bool has_rc);
+std::vector<int> signed_modes(int n);
+std::vector<double> wavenumbers(int n, double h);
+// window Fourier transform at wavenumbers k (windows.py:251-257); BM uses the
+// long-double quadrature of windows.py:175-239.
+std::vector<double> window_fourier(int window, int P, double h, double shape,
+                                   const std::vector<double> &k);
+double window_value(int window, double w, double shape, double x);
+double greens_zero_mode(int D, double R, double kappa);
+double bessel_i0(double x);
+
+// ---------------------------------------------------------- device buffers
+struct DevBuf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t n) {
+        if (n <= bytes) return;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        if (n == 0) return;
+        SE_CUDA(cudaMalloc(&ptr, n));
+        bytes = n;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <class T> T *as() const { return static_cast<T *>(ptr); }
+};
+
+// Per-axis mode table on the device: wavenumbers and window transforms.
+struct ModeTable {
+    int n = 0;
+    DevBuf k, what;
+};
+
+// Particle binning: sort by a key and build (bin, start, count) work units.
+struct Binning {
+    int nbins = 0;
+    int64_t capacity = 0;
+    DevBuf keys, keys_sorted, idx, idx_sorted, counts, starts, units, nunits, cub_tmp;
+    DevBuf rec;  // sorted particle records (x, y, z, q) as double4
+    size_t cub_bytes = 0;
+};
+
+struct TileGeom {
+    int T;        // tile edge in start-index units
+    int Tp;       // padded tile edge T + P - 1
+    int pitch;    // z pitch of the padded smem tile (doubles)
+    int nt[3];    // tiles per axis
+    int lo[3];    // first start index per axis
+    int nwarps;   // warps per CTA (x-plane owners)
+    int batch;    // particles staged per batch
+    size_t smem;  // dynamic shared memory bytes
+};
+
+struct CellGeom {
+    int n;        // cells per axis
+    double edge;  // cell edge
+    int mode[3];  // 0: free (clip), 1: periodic wrap +-2, 2: periodic, all cells + min image
+};
+
+struct se_plan_impl;
+
+}  // namespace se
+
+struct se_plan {
+    int D = 3;
+    double L = 1.0;
+    se_params_t p{};
+    se_grid_t g{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    int64_t launches = 0;
+
+    // spreading / gathering
+    se::TileGeom tile{};
+    se::Binning tbin;  // tile binning for spread / gather
+    // real space
+    se::CellGeom cell{};
+    se::Binning cbin;  // cell binning for the real-space sum
+    se::DevBuf flag;   // device error flags (int)
+
+    // k-space
+    bool kspace_ready = false;
+    double xi_tables = -1.0;
+    se::ModeTable tM, tg0, tgs, tMt, tNc, tNh;
+    se::DevBuf spec, spec2, spec3, work, grid_tmp, rows_I;  // spectra / padded buffers
+    int nI_rows = 0;  // half-plane I rows (D=2: pairs, D=1: planes)
+    cufftHandle fft_fwd = 0, fft_inv = 0;           // main transforms
+    cufftHandle fft_rowJ = 0, fft_rowI = 0, fft_row0 = 0;  // free-axis transforms (D in {1,2})
+    bool fft_made = false;
+    // D=0 kernel path
+    bool d0_ready = false;
+    int nconv = 0, kg0 = 0;
+    double kR = 0.0;
+    se::DevBuf ghat;
+    cufftHandle fft_c_fwd = 0, fft_c_inv = 0;
+    bool d0_fft_made = false;
+    // D=0 full-upsampling path
+    cufftHandle fft_f_fwd = 0, fft_f_inv = 0;
+    bool d0full_fft_made = false;
+    se::DevBuf grid_dev;  // scratch grid for the fused pipelines
+    se::DevBuf io_pos, io_q, io_phi, io_grid;  // staging for _host calls
+    se::DevBuf check;  // neutrality / box reduction scratch
+    int warnings = 0;  // bit 0: non-neutral system in free space (core.py:185-189)
+    // per-kernel CUDA-event timing of the hot kernels (bench roofline)
+    bool prof = false;
+    cudaEvent_t pev[SE_K_COUNT][2] = {};
+    bool pending[SE_K_COUNT] = {};
+    double pms[SE_K_COUNT] = {};
+    int64_t pcount[SE_K_COUNT] = {};
+    se::DevBuf pairs;  // pair counter (count mode of the real-space kernel)
+};
+
+namespace se {
+
+// per-kernel timing (no-ops unless the plan's profiling flag is set)
+inline void prof_begin(se_plan *pl, int id) {
+    if (!pl->prof) return;
+    if (!pl->pev[id][0]) {
+        SE_CUDA(cudaEventCreate(&pl->pev[id][0]));
+        SE_CUDA(cudaEventCreate(&pl->pev[id][1]));
+    }
+    SE_CUDA(cudaEventRecord(pl->pev[id][0], pl->stream));
+}
+inline void prof_end(se_plan *pl, int id) {
+    if (!pl->prof) return;
+    SE_CUDA(cudaEventRecord(pl->pev[id][1], pl->stream));
+    pl->pending[id] = true;
+}
+inline void prof_collect(se_plan *pl) {
+    if (!pl->prof) return;
+    for (int id = 0; id < SE_K_COUNT; ++id) {
+        if (!pl->pending[id]) continue;
+        SE_CUDA(cudaEventSynchronize(pl->pev[id][1]));
+        float ms = 0;
+        SE_CUDA(cudaEventElapsedTime(&ms, pl->pev[id][0], pl->pev[id][1]));
+        pl->pms[id] += ms;
+        pl->pcount[id] += 1;
+        pl->pending[id] = false;
+    }
+}
+
+// launch helpers (defined in the .cu files)
+void realspace_pair_count(se_plan *pl, const double *pos, const double *q, int64_t N, long long *pairs);
+void spread_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *grid,
+                int rank, int world);
+void gather_run(se_plan *pl, const double *grid, const double *pos, int64_t N, double *phi,
+                int accumulate, int rank, int world, bool rebin);
+void kspace_run(se_plan *pl, double *grid, int use_kernel, double *timings);
+void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi,
+                   int add_self, int rank, int world);
+void d0_kernel_prepare(se_plan *pl, double *t_precompute);
+void plan_release_device(se_plan *pl);
+
+// binning (se_sort.cu)
+void binning_reserve(Binning &b, int64_t N, int nbins, int chunk);
+void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, int64_t N,
+                  int nbins, int chunk);
+int64_t binning_max_units(const Binning &b, int64_t N, int nbins, int chunk);
+
+// shared device helpers ---------------------------------------------------
+struct WinParams {
+    int window;
+    int P;
+    double h, w, shape;
+    double peak;   // gaussian: m / (w sqrt(2 pi))
+    double i0b;    // kb: I0(beta)
+};
+
+__host__ __device__ inline WinParams make_win(const se_params_t &p, double h) {
+    WinParams wp;
+    wp.window = p.window;
+    wp.P = p.P;
+    wp.h = h;
+    wp.w = 0.5 * p.P * h;
+    wp.shape = p.shape;
+    wp.peak = p.shape / (wp.w * 2.5066282746310002);  // sqrt(2 pi)
+    wp.i0b = 1.0;
+    return wp;
+}
+
+}  // namespace se

@@ -1,0 +1,637 @@
+// k-space stage of the SE pipeline on cuFFT plus fused multiplier kernels.
+//
+//  D=3  aft_forward/scale/aft_inverse (aft.py:203-206, sekspace.py:198-206,
+//       aft.py:237-238): real-to-complex M^3 FFT, one pass multiplying by
+//       4 pi e^{-k^2/4xi^2} / (k^2 w^2) (0 at k=0), complex-to-real FFT.
+//  D=2,1 adaptive FFT (aft.py:155-265, sekspace.py:217-254): the periodic
+//       transform is real-to-complex, so only the half plane of periodic
+//       modes is carried (the free-axis operator commutes with conjugation);
+//       rows/planes of the zero block (padded to g0), the I block (padded to
+//       gs) and the J block (unpadded Mt) are transformed as three batched
+//       cuFFT calls, scaled by one fused kernel per block, inverted,
+//       restricted to Mt and merged back before the inverse periodic
+//       transform.
+//  D=0  precomputed truncated kernel on the 2x padded grid
+//       (sekspace.py:257-337), including the one-time precompute of the
+//       kernel table on the device (fine g0^3 grid, inverse transform, clip,
+//       forward transform), or the globally upsampled path
+//       (use_kernel = False, sekspace.py:208-215).
+#include <cuda_runtime.h>
+
+#include "se_common.h"
+
+namespace se {
+
+typedef double2 cplx;
+
+// ------------------------------------------------------------- tables
+static void upload(DevBuf &b, const std::vector<double> &v) {
+    b.ensure(sizeof(double) * (v.size() ? v.size() : 1));
+    SE_CUDA(cudaMemcpy(b.ptr, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice));
+}
+
+// sekspace.py:181-185 (_window_table with its underflow guard)
+static void make_table(se_plan *pl, ModeTable &t, int n, bool half) {
+    std::vector<double> k;
+    if (half) {  // 2 pi rfftfreq(n, d=h)
+        int nh = n / 2 + 1;
+        k.resize(nh);
+        double val = 1.0 / (n * pl->g.h);
+        for (int j = 0; j < nh; ++j) k[j] = 2.0 * M_PI * (j * val);
+    } else {
+        k = wavenumbers(n, pl->g.h);
+    }
+    std::vector<double> w = window_fourier(pl->p.window, pl->p.P, pl->g.h, pl->p.shape, k);
+    double mn = 1e300;
+    for (double v : w) mn = std::fmin(mn, std::fabs(v));
+    if (mn < 1e-30) fail(SE_ENUMERIC, "window transform underflow: P/M misconfigured");
+    t.n = (int)k.size();
+    upload(t.k, k);
+    upload(t.what, w);
+}
+
+// ------------------------------------------------------------- helpers
+__device__ __forceinline__ double mollify(double k2, double xi) { return exp(-k2 / (4.0 * xi * xi)); }
+
+// greens.py:48-85 on the device (zero periodic-mode block)
+__device__ double greens_zero_dev(int D, double R, double kappa) {
+    kappa = fabs(kappa);
+    double t = R * kappa;
+    if (t < 1e-2) {
+        double z = t * t;
+        if (D == 0) return R * R * (0.5 - z / 24.0 + z * z / 720.0 - z * z * z / 40320.0 + z * z * z * z / 3628800.0);
+        if (D == 1) {
+            double lr = log(R);
+            return R * R * ((0.25 - 0.5 * lr) - z * (1.0 / 64.0 - lr / 16.0) + z * z * (1.0 / 2304.0 - lr / 384.0) -
+                            z * z * z * (1.0 / 147456.0 - lr / 18432.0) +
+                            z * z * z * z * (1.0 / 14745600.0 - lr / 1474560.0));
+        }
+        return R * R * (-0.5 + z / 8.0 - z * z / 144.0 + z * z * z / 5760.0 - z * z * z * z / 403200.0);
+    }
+    if (D == 0) return R * R * (1.0 - cos(t)) / (t * t);
+    if (D == 1) return (1.0 - j0(t)) / (kappa * kappa) - (R * log(R)) * j1(t) / kappa;
+    return R * R * (1.0 - cos(t) - t * sin(t)) / (t * t);
+}
+
+__global__ void scale_d3_kernel(cplx *__restrict__ F, int M, const double *__restrict__ k, const double *__restrict__ w,
+                                double xi, double norm) {
+    const int nh = M / 2 + 1;
+    int64_t total = (int64_t)M * M * nh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int iz = (int)(i % nh);
+        int64_t r = i / nh;
+        int iy = (int)(r % M), ix = (int)(r / M);
+        double k2 = k[ix] * k[ix] + k[iy] * k[iy] + k[iz] * k[iz];
+        double W = w[ix] * w[iy] * w[iz];
+        double fac = k2 > 0.0 ? 4.0 * M_PI * mollify(k2, xi) * (1.0 / k2) / (W * W) * norm : 0.0;
+        cplx v = F[i];
+        F[i] = make_double2(v.x * fac, v.y * fac);
+    }
+}
+
+__global__ void pad_real_kernel(const double *__restrict__ src, int s0, int s1, int s2, double *__restrict__ dst, int d0,
+                                int d1, int d2) {
+    int64_t total = (int64_t)d0 * d1 * d2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int z = (int)(i % d2);
+        int64_t r = i / d2;
+        int y = (int)(r % d1), x = (int)(r / d1);
+        dst[i] = (x < s0 && y < s1 && z < s2) ? src[((int64_t)x * s1 + y) * s2 + z] : 0.0;
+    }
+}
+
+__global__ void restrict_real_kernel(const double *__restrict__ src, int d1, int d2, double *__restrict__ dst, int s0,
+                                     int s1, int s2, double scale) {
+    int64_t total = (int64_t)s0 * s1 * s2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int z = (int)(i % s2);
+        int64_t r = i / s2;
+        int y = (int)(r % s1), x = (int)(r / s1);
+        dst[i] = src[((int64_t)x * d1 + y) * d2 + z] * scale;
+    }
+}
+
+// D=0 kernel path: F *= ghat * 4 pi * af[x] * af[y] * ah[z] / n^3  (sekspace.py:319-326)
+__global__ void scale_d0k_kernel(cplx *__restrict__ F, int n, const double *__restrict__ ghat,
+                                 const double *__restrict__ af, const double *__restrict__ ah, double norm) {
+    const int nh = n / 2 + 1;
+    int64_t total = (int64_t)n * n * nh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int iz = (int)(i % nh);
+        int64_t r = i / nh;
+        int iy = (int)(r % n), ix = (int)(r / n);
+        double fac = ghat[i] * (4.0 * M_PI * af[ix]) * af[iy] * ah[iz] * norm;
+        cplx v = F[i];
+        F[i] = make_double2(v.x * fac, v.y * fac);
+    }
+}
+
+// D=0 full upsampling: F *= 4 pi e^{-k^2/4xi^2} G0(|k|) / W^2 / g^3  (sekspace.py:208-215)
+__global__ void scale_d0f_kernel(cplx *__restrict__ F, int g, const double *__restrict__ k, const double *__restrict__ w,
+                                 double xi, double R, double norm) {
+    const int gh = g / 2 + 1;
+    int64_t total = (int64_t)g * g * gh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int iz = (int)(i % gh);
+        int64_t r = i / gh;
+        int iy = (int)(r % g), ix = (int)(r / g);
+        double k2 = k[ix] * k[ix] + k[iy] * k[iy] + k[iz] * k[iz];
+        double W = w[ix] * w[iy] * w[iz];
+        double fac = 4.0 * M_PI * mollify(k2, xi) * greens_zero_dev(0, R, sqrt(k2)) / (W * W) * norm;
+        cplx v = F[i];
+        F[i] = make_double2(v.x * fac, v.y * fac);
+    }
+}
+
+// half spectrum of G0 on the fine grid (imaginary part zero)
+__global__ void ghat_fine_kernel(cplx *__restrict__ out, int g, const double *__restrict__ k, double R) {
+    const int gh = g / 2 + 1;
+    int64_t total = (int64_t)g * g * gh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int iz = (int)(i % gh);
+        int64_t r = i / gh;
+        int iy = (int)(r % g), ix = (int)(r / g);
+        double k2 = k[ix] * k[ix] + k[iy] * k[iy] + k[iz] * k[iz];
+        out[i] = make_double2(greens_zero_dev(0, R, sqrt(k2)), 0.0);
+    }
+}
+
+// clip cube [0,half) U [g-half,g) per axis of the fine real kernel (sekspace.py:291-293)
+__global__ void clip_cube_kernel(const double *__restrict__ fine, int g, double *__restrict__ cube, int n, double scale) {
+    const int half = n / 2;
+    int64_t total = (int64_t)n * n * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int z = (int)(i % n);
+        int64_t r = i / n;
+        int y = (int)(r % n), x = (int)(r / n);
+        int sx = x < half ? x : g - n + x, sy = y < half ? y : g - n + y, sz = z < half ? z : g - n + z;
+        cube[i] = fine[((int64_t)sx * g + sy) * g + sz] * scale;
+    }
+}
+
+__global__ void take_real_kernel(const cplx *__restrict__ in, double *__restrict__ out, int64_t total,
+                                 unsigned long long *__restrict__ mx) {
+    double mre = 0.0, mim = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        cplx v = in[i];
+        out[i] = v.x;
+        mre = fmax(mre, fabs(v.x));
+        mim = fmax(mim, fabs(v.y));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+        mim = fmax(mim, __shfl_xor_sync(0xffffffffu, mim, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(mx, (unsigned long long)__double_as_longlong(mre));
+        atomicMax(mx + 1, (unsigned long long)__double_as_longlong(mim));
+    }
+}
+
+// ------------------------------------------------ mixed periodicity (AFT)
+// pack rows/planes of Hk into a zero-padded batch: dst[r][...] (glen^nfree)
+__global__ void pack_kernel(const cplx *__restrict__ Hk, int Mt, int nfree, const int *__restrict__ rows, int nrows,
+                            cplx *__restrict__ dst, int glen) {
+    int64_t per = nfree == 1 ? glen : (int64_t)glen * glen;
+    int64_t src_per = nfree == 1 ? Mt : (int64_t)Mt * Mt;
+    int64_t total = per * nrows;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int r = (int)(i / per);
+        int64_t e = i - (int64_t)r * per;
+        int row = rows ? rows[r] : 0;
+        cplx v = make_double2(0.0, 0.0);
+        if (nfree == 1) {
+            if (e < Mt) v = Hk[(int64_t)row * src_per + e];
+        } else {
+            int y = (int)(e / glen), z = (int)(e - (int64_t)y * glen);
+            if (y < Mt && z < Mt) v = Hk[(int64_t)row * src_per + (int64_t)y * Mt + z];
+        }
+        dst[i] = v;
+    }
+}
+
+__global__ void unpack_kernel(const cplx *__restrict__ src, int glen, int nfree, const int *__restrict__ rows, int nrows,
+                              cplx *__restrict__ Hk, int Mt) {
+    int64_t dper = nfree == 1 ? Mt : (int64_t)Mt * Mt;
+    int64_t sper = nfree == 1 ? glen : (int64_t)glen * glen;
+    int64_t total = dper * nrows;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int r = (int)(i / dper);
+        int64_t e = i - (int64_t)r * dper;
+        int row = rows ? rows[r] : 0;
+        int64_t s;
+        if (nfree == 1) {
+            s = e;
+        } else {
+            int y = (int)(e / Mt), z = (int)(e - (int64_t)y * Mt);
+            s = (int64_t)y * glen + z;
+        }
+        Hk[(int64_t)row * dper + e] = src[(int64_t)r * sper + s];
+    }
+}
+
+struct MixArgs {
+    int D, M, nI, half;  // half = M/2+1 (number of carried modes along the halved periodic axis)
+    double xi, R;
+    const double *kp, *wp;  // periodic mode table (length M)
+};
+
+__device__ __forceinline__ int absmode(int i, int M) { return i < M / 2 ? i : M - i; }
+
+// J-block multiplier applied to every row/plane of Hk whose max-norm mode
+// exceeds nI (sekspace.py:234-254).  Rows of the zero/I blocks are skipped
+// (they are replaced by the unpack of their padded transforms).
+// D=2: Hk layout [ix][iy<half][z] (rows of Mt); D=1: [ix<half][y][z].
+__global__ void scale_mixJ_kernel(cplx *__restrict__ Hk, MixArgs a, int Mt, const double *__restrict__ kf,
+                                  const double *__restrict__ wf, double norm) {
+    const int nfree = 3 - a.D;
+    int64_t per = nfree == 1 ? Mt : (int64_t)Mt * Mt;
+    int64_t rowsN = a.D == 2 ? (int64_t)a.M * a.half : a.half;
+    int64_t total = rowsN * per;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t row = i / per;
+        int64_t e = i - row * per;
+        double kr2, wr;
+        int mu;
+        if (a.D == 2) {
+            int ix = (int)(row / a.half), iy = (int)(row - (int64_t)ix * a.half);
+            mu = max(absmode(ix, a.M), absmode(iy, a.M));
+            kr2 = a.kp[ix] * a.kp[ix] + a.kp[iy] * a.kp[iy];
+            wr = a.wp[ix] * a.wp[iy];
+        } else {
+            int ix = (int)row;
+            mu = absmode(ix, a.M);
+            kr2 = a.kp[ix] * a.kp[ix];
+            wr = a.wp[ix];
+        }
+        if (mu <= a.nI) continue;
+        double k2, W;
+        if (nfree == 1) {
+            k2 = kr2 + kf[e] * kf[e];
+            W = wr * wf[e];
+        } else {
+            int y = (int)(e / Mt), z = (int)(e - (int64_t)y * Mt);
+            k2 = kr2 + kf[y] * kf[y] + kf[z] * kf[z];
+            W = wr * (wf[y] * wf[z]);
+        }
+        double fac = 4.0 * M_PI * mollify(k2, a.xi) / (k2 * (W * W)) * norm;
+        cplx v = Hk[i];
+        Hk[i] = make_double2(v.x * fac, v.y * fac);
+    }
+}
+
+// I-block multiplier on the packed, padded rows (glen = gs).
+__global__ void scale_mixI_kernel(cplx *__restrict__ B, MixArgs a, const int *__restrict__ rows, int nrows, int glen,
+                                  const double *__restrict__ kf, const double *__restrict__ wf, double norm) {
+    const int nfree = 3 - a.D;
+    int64_t per = nfree == 1 ? glen : (int64_t)glen * glen;
+    int64_t total = per * nrows;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int r = (int)(i / per);
+        int64_t e = i - (int64_t)r * per;
+        int row = rows[r];
+        double kr2, wr;
+        if (a.D == 2) {
+            int ix = row / a.half, iy = row - ix * a.half;
+            kr2 = a.kp[ix] * a.kp[ix] + a.kp[iy] * a.kp[iy];
+            wr = a.wp[ix] * a.wp[iy];
+        } else {
+            kr2 = a.kp[row] * a.kp[row];
+            wr = a.wp[row];
+        }
+        double k2, W;
+        if (nfree == 1) {
+            k2 = kr2 + kf[e] * kf[e];
+            W = wr * wf[e];
+        } else {
+            int y = (int)(e / glen), z = (int)(e - (int64_t)y * glen);
+            k2 = kr2 + kf[y] * kf[y] + kf[z] * kf[z];
+            W = wr * (wf[y] * wf[z]);
+        }
+        double fac = 4.0 * M_PI * mollify(k2, a.xi) / (k2 * (W * W)) * norm;
+        cplx v = B[i];
+        B[i] = make_double2(v.x * fac, v.y * fac);
+    }
+}
+
+// zero block multiplier (sekspace.py:221-232), glen = g0
+__global__ void scale_mix0_kernel(cplx *__restrict__ Z, MixArgs a, int glen, const double *__restrict__ kf,
+                                  const double *__restrict__ wf, double norm) {
+    const int nfree = 3 - a.D;
+    int64_t total = nfree == 1 ? glen : (int64_t)glen * glen;
+    double wp0 = a.D == 2 ? a.wp[0] * a.wp[0] : a.wp[0];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        double kap2, wfree;
+        if (nfree == 1) {
+            kap2 = kf[i] * kf[i];
+            wfree = wf[i];
+        } else {
+            int y = (int)(i / glen), z = (int)(i - (int64_t)y * glen);
+            kap2 = kf[y] * kf[y] + kf[z] * kf[z];
+            wfree = wf[y] * wf[z];
+        }
+        double W = wp0 * wfree;
+        double fac = 4.0 * M_PI * mollify(kap2, a.xi) * greens_zero_dev(a.D, a.R, sqrt(kap2)) / (W * W) * norm;
+        cplx v = Z[i];
+        Z[i] = make_double2(v.x * fac, v.y * fac);
+    }
+}
+
+// ------------------------------------------------------------- launch utils
+static unsigned grid_for(int64_t total) {
+    int64_t b = (total + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+
+#define LAUNCH(kern, total, ...)                                                   \
+    do {                                                                           \
+        kern<<<grid_for(total), 256, 0, pl->stream>>>(__VA_ARGS__);                \
+        SE_LAUNCH_CHECK();                                                         \
+        pl->launches += 1;                                                         \
+    } while (0)
+
+struct StageTimer {
+    se_plan *pl;
+    bool on;
+    cudaEvent_t ev[8];
+    int n = 0;
+    StageTimer(se_plan *p, bool enabled) : pl(p), on(enabled) {
+        if (on)
+            for (auto &e : ev) SE_CUDA(cudaEventCreate(&e));
+    }
+    void mark() {
+        if (on) SE_CUDA(cudaEventRecord(ev[n++], pl->stream));
+    }
+    double secs(int a, int b) {
+        float ms = 0;
+        SE_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+        return ms * 1e-3;
+    }
+    ~StageTimer() {
+        if (on)
+            for (auto &e : ev) cudaEventDestroy(e);
+    }
+};
+
+// ------------------------------------------------------------- plans
+static void ensure_tables(se_plan *pl) {
+    if (pl->kspace_ready) return;
+    const int D = pl->D;
+    const se_grid_t &g = pl->g;
+    if (D == 3) {
+        make_table(pl, pl->tM, g.M, false);
+    } else if (D == 0) {
+        make_table(pl, pl->tg0, g.g0, false);
+    } else {
+        make_table(pl, pl->tM, g.M, false);
+        make_table(pl, pl->tg0, g.g0, false);
+        make_table(pl, pl->tMt, g.Mt, false);
+        if (pl->nI_rows >= 0) make_table(pl, pl->tgs, g.gs, false);
+        // I rows of the half plane
+        std::vector<int> rows;
+        const int M = g.M, half = M / 2 + 1;
+        std::vector<int> m = signed_modes(M);
+        if (D == 2) {
+            for (int ix = 0; ix < M; ++ix)
+                for (int iy = 0; iy < half; ++iy) {
+                    int mu = std::max(std::abs(m[ix]), std::abs(m[iy]));
+                    if (mu >= 1 && mu <= pl->p.nI) rows.push_back(ix * half + iy);
+                }
+        } else {
+            for (int ix = 0; ix < half; ++ix) {
+                int mu = std::abs(m[ix]);
+                if (mu >= 1 && mu <= pl->p.nI) rows.push_back(ix);
+            }
+        }
+        pl->nI_rows = (int)rows.size();
+        pl->rows_I.ensure(sizeof(int) * (rows.size() + 1));
+        if (!rows.empty())
+            SE_CUDA(cudaMemcpy(pl->rows_I.ptr, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
+    }
+    pl->kspace_ready = true;
+}
+
+static void make_ffts(se_plan *pl) {
+    if (pl->fft_made) return;
+    const se_grid_t &g = pl->g;
+    const int D = pl->D, M = g.M, Mt = g.Mt;
+    if (D == 3) {
+        SE_CUFFT(cufftPlan3d(&pl->fft_fwd, M, M, M, CUFFT_D2Z));
+        SE_CUFFT(cufftPlan3d(&pl->fft_inv, M, M, M, CUFFT_Z2D));
+        pl->spec.ensure(sizeof(cplx) * (size_t)M * M * (M / 2 + 1));
+    } else if (D == 2) {
+        const int half = M / 2 + 1;
+        int n[2] = {M, M}, rin[2] = {M, M}, cout[2] = {M, half};
+        SE_CUFFT(cufftPlanMany(&pl->fft_fwd, 2, n, rin, Mt, 1, cout, Mt, 1, CUFFT_D2Z, Mt));
+        SE_CUFFT(cufftPlanMany(&pl->fft_inv, 2, n, cout, Mt, 1, rin, Mt, 1, CUFFT_Z2D, Mt));
+        int nJ[1] = {Mt}, nI1[1] = {g.gs}, n0[1] = {g.g0};
+        SE_CUFFT(cufftPlanMany(&pl->fft_rowJ, 1, nJ, nullptr, 1, Mt, nullptr, 1, Mt, CUFFT_Z2Z, M * half));
+        if (pl->nI_rows > 0)
+            SE_CUFFT(cufftPlanMany(&pl->fft_rowI, 1, nI1, nullptr, 1, g.gs, nullptr, 1, g.gs, CUFFT_Z2Z, pl->nI_rows));
+        SE_CUFFT(cufftPlanMany(&pl->fft_row0, 1, n0, nullptr, 1, g.g0, nullptr, 1, g.g0, CUFFT_Z2Z, 1));
+        pl->spec.ensure(sizeof(cplx) * (size_t)M * half * Mt);
+        pl->spec2.ensure(sizeof(cplx) * (size_t)g.g0);
+        pl->spec3.ensure(sizeof(cplx) * (size_t)(pl->nI_rows ? pl->nI_rows : 1) * g.gs);
+    } else if (D == 1) {
+        const int half = M / 2 + 1;
+        int n[1] = {M}, rin[1] = {M}, cout[1] = {half};
+        SE_CUFFT(cufftPlanMany(&pl->fft_fwd, 1, n, rin, Mt * Mt, 1, cout, Mt * Mt, 1, CUFFT_D2Z, Mt * Mt));
+        SE_CUFFT(cufftPlanMany(&pl->fft_inv, 1, n, cout, Mt * Mt, 1, rin, Mt * Mt, 1, CUFFT_Z2D, Mt * Mt));
+        int nJ[2] = {Mt, Mt}, nI2[2] = {g.gs, g.gs}, n0[2] = {g.g0, g.g0};
+        SE_CUFFT(cufftPlanMany(&pl->fft_rowJ, 2, nJ, nullptr, 1, Mt * Mt, nullptr, 1, Mt * Mt, CUFFT_Z2Z, half));
+        if (pl->nI_rows > 0)
+            SE_CUFFT(cufftPlanMany(&pl->fft_rowI, 2, nI2, nullptr, 1, g.gs * g.gs, nullptr, 1, g.gs * g.gs, CUFFT_Z2Z,
+                                   pl->nI_rows));
+        SE_CUFFT(cufftPlanMany(&pl->fft_row0, 2, n0, nullptr, 1, g.g0 * g.g0, nullptr, 1, g.g0 * g.g0, CUFFT_Z2Z, 1));
+        pl->spec.ensure(sizeof(cplx) * (size_t)half * Mt * Mt);
+        pl->spec2.ensure(sizeof(cplx) * (size_t)g.g0 * g.g0);
+        pl->spec3.ensure(sizeof(cplx) * (size_t)(pl->nI_rows ? pl->nI_rows : 1) * g.gs * g.gs);
+    }
+    pl->fft_made = true;
+}
+
+static void set_streams(se_plan *pl, std::initializer_list<cufftHandle> hs) {
+    for (cufftHandle h : hs)
+        if (h) SE_CUFFT(cufftSetStream(h, pl->stream));
+}
+
+// ------------------------------------------------------------- D = 0 kernel
+void d0_kernel_prepare(se_plan *pl, double *t_pre) {
+    if (pl->d0_ready) {
+        if (t_pre) *t_pre = 0.0;
+        return;
+    }
+    StageTimer tm(pl, t_pre != nullptr);
+    tm.mark();
+    const se_grid_t &g = pl->g;
+    D0Geom d = d0_geometry(g.L, g.M, g.P, pl->p.s0, pl->p.rc, true);
+    pl->nconv = d.nconv;
+    pl->kg0 = d.g0;
+    pl->kR = d.R;
+    const int gf = d.g0, n = d.nconv, nh = n / 2 + 1;
+    // fine grid wavenumbers (window-independent)
+    std::vector<double> kf = wavenumbers(gf, g.h);
+    DevBuf dk;
+    upload(dk, kf);
+    DevBuf half, fine;
+    half.ensure(sizeof(cplx) * (size_t)gf * gf * (gf / 2 + 1));
+    fine.ensure(sizeof(double) * (size_t)gf * gf * gf);
+    LAUNCH(ghat_fine_kernel, (int64_t)gf * gf * (gf / 2 + 1), half.as<cplx>(), gf, dk.as<double>(), d.R);
+    cufftHandle hinv = 0, hfwd = 0;
+    SE_CUFFT(cufftPlan3d(&hinv, gf, gf, gf, CUFFT_Z2D));
+    SE_CUFFT(cufftSetStream(hinv, pl->stream));
+    SE_CUFFT(cufftExecZ2D(hinv, half.as<cplx>(), fine.as<double>()));
+    cufftDestroy(hinv);
+    half.release();
+    DevBuf cube, cspec;
+    cube.ensure(sizeof(double) * (size_t)n * n * n);
+    // numpy ifftn normalisation 1/g^3; the reference's /h^3 and h^3 cancel
+    double scale = 1.0 / ((double)gf * gf * gf);
+    LAUNCH(clip_cube_kernel, (int64_t)n * n * n, fine.as<double>(), gf, cube.as<double>(), n, scale);
+    fine.release();
+    cspec.ensure(sizeof(cplx) * (size_t)n * n * nh);
+    SE_CUFFT(cufftPlan3d(&hfwd, n, n, n, CUFFT_D2Z));
+    SE_CUFFT(cufftSetStream(hfwd, pl->stream));
+    SE_CUFFT(cufftExecD2Z(hfwd, cube.as<double>(), cspec.as<cplx>()));
+    cufftDestroy(hfwd);
+    cube.release();
+    pl->ghat.ensure(sizeof(double) * (size_t)n * n * nh);
+    DevBuf mx;
+    mx.ensure(2 * sizeof(unsigned long long));
+    SE_CUDA(cudaMemsetAsync(mx.ptr, 0, 2 * sizeof(unsigned long long), pl->stream));
+    LAUNCH(take_real_kernel, (int64_t)n * n * nh, cspec.as<cplx>(), pl->ghat.as<double>(), (int64_t)n * n * nh,
+           mx.as<unsigned long long>());
+    unsigned long long hm[2];
+    SE_CUDA(cudaMemcpyAsync(hm, mx.ptr, sizeof(hm), cudaMemcpyDeviceToHost, pl->stream));
+    SE_CUDA(cudaStreamSynchronize(pl->stream));
+    cspec.release();
+    double mre, mim;
+    memcpy(&mre, &hm[0], 8);
+    memcpy(&mim, &hm[1], 8);
+    if (!(mim < 1e-13 * mre)) fail(SE_ENUMERIC, "truncated kernel transform must be real");
+    // per-axis factors a = e^{-k^2/4xi^2} / w^2 on the full and half mode sets
+    make_table(pl, pl->tNc, n, false);
+    make_table(pl, pl->tNh, n, true);
+    auto afac = [&](ModeTable &t) {
+        std::vector<double> k(t.n), w(t.n), a(t.n);
+        SE_CUDA(cudaMemcpy(k.data(), t.k.ptr, sizeof(double) * t.n, cudaMemcpyDeviceToHost));
+        SE_CUDA(cudaMemcpy(w.data(), t.what.ptr, sizeof(double) * t.n, cudaMemcpyDeviceToHost));
+        const double xi = pl->p.xi;
+        for (int i = 0; i < t.n; ++i) a[i] = std::exp(-(k[i] * k[i]) / (4.0 * xi * xi)) / (w[i] * w[i]);
+        upload(t.what, a);  // reuse the slot: holds a(k) from here on
+    };
+    afac(pl->tNc);
+    afac(pl->tNh);
+    SE_CUFFT(cufftPlan3d(&pl->fft_c_fwd, n, n, n, CUFFT_D2Z));
+    SE_CUFFT(cufftPlan3d(&pl->fft_c_inv, n, n, n, CUFFT_Z2D));
+    pl->d0_fft_made = true;
+    pl->d0_ready = true;
+    tm.mark();
+    if (t_pre) {
+        SE_CUDA(cudaStreamSynchronize(pl->stream));
+        *t_pre = tm.secs(0, 1);
+    }
+}
+
+// ------------------------------------------------------------- driver
+void kspace_run(se_plan *pl, double *grid, int use_kernel, double *timings) {
+    const int D = pl->D;
+    const se_grid_t &g = pl->g;
+    if (timings) timings[SE_T_PRECOMPUTE] = 0.0;
+    ensure_tables(pl);
+    StageTimer tm(pl, timings != nullptr);
+    if (D == 0 && use_kernel) {
+        d0_kernel_prepare(pl, timings ? &timings[SE_T_PRECOMPUTE] : nullptr);
+        const int n = pl->nconv, nh = n / 2 + 1, Mt = g.Mt;
+        pl->grid_tmp.ensure(sizeof(double) * (size_t)n * n * n);
+        pl->spec.ensure(sizeof(cplx) * (size_t)n * n * nh);
+        set_streams(pl, {pl->fft_c_fwd, pl->fft_c_inv});
+        tm.mark();
+        LAUNCH(pad_real_kernel, (int64_t)n * n * n, grid, Mt, Mt, Mt, pl->grid_tmp.as<double>(), n, n, n);
+        SE_CUFFT(cufftExecD2Z(pl->fft_c_fwd, pl->grid_tmp.as<double>(), pl->spec.as<cplx>()));
+        tm.mark();
+        LAUNCH(scale_d0k_kernel, (int64_t)n * n * nh, pl->spec.as<cplx>(), n, pl->ghat.as<double>(),
+               pl->tNc.what.as<double>(), pl->tNh.what.as<double>(), 1.0 / ((double)n * n * n));
+        tm.mark();
+        SE_CUFFT(cufftExecZ2D(pl->fft_c_inv, pl->spec.as<cplx>(), pl->grid_tmp.as<double>()));
+        LAUNCH(restrict_real_kernel, (int64_t)Mt * Mt * Mt, pl->grid_tmp.as<double>(), n, n, grid, Mt, Mt, Mt, 1.0);
+        tm.mark();
+    } else if (D == 0) {
+        const int gf = g.g0, gh = gf / 2 + 1, Mt = g.Mt;
+        if (!pl->d0full_fft_made) {
+            SE_CUFFT(cufftPlan3d(&pl->fft_f_fwd, gf, gf, gf, CUFFT_D2Z));
+            SE_CUFFT(cufftPlan3d(&pl->fft_f_inv, gf, gf, gf, CUFFT_Z2D));
+            pl->d0full_fft_made = true;
+        }
+        pl->grid_tmp.ensure(sizeof(double) * (size_t)gf * gf * gf);
+        pl->spec.ensure(sizeof(cplx) * (size_t)gf * gf * gh);
+        set_streams(pl, {pl->fft_f_fwd, pl->fft_f_inv});
+        tm.mark();
+        LAUNCH(pad_real_kernel, (int64_t)gf * gf * gf, grid, Mt, Mt, Mt, pl->grid_tmp.as<double>(), gf, gf, gf);
+        SE_CUFFT(cufftExecD2Z(pl->fft_f_fwd, pl->grid_tmp.as<double>(), pl->spec.as<cplx>()));
+        tm.mark();
+        LAUNCH(scale_d0f_kernel, (int64_t)gf * gf * gh, pl->spec.as<cplx>(), gf, pl->tg0.k.as<double>(),
+               pl->tg0.what.as<double>(), pl->p.xi, g.R, 1.0 / ((double)gf * gf * gf));
+        tm.mark();
+        SE_CUFFT(cufftExecZ2D(pl->fft_f_inv, pl->spec.as<cplx>(), pl->grid_tmp.as<double>()));
+        LAUNCH(restrict_real_kernel, (int64_t)Mt * Mt * Mt, pl->grid_tmp.as<double>(), gf, gf, grid, Mt, Mt, Mt, 1.0);
+        tm.mark();
+    } else if (D == 3) {
+        make_ffts(pl);
+        set_streams(pl, {pl->fft_fwd, pl->fft_inv});
+        const int M = g.M;
+        tm.mark();
+        SE_CUFFT(cufftExecD2Z(pl->fft_fwd, grid, pl->spec.as<cplx>()));
+        tm.mark();
+        LAUNCH(scale_d3_kernel, (int64_t)M * M * (M / 2 + 1), pl->spec.as<cplx>(), M, pl->tM.k.as<double>(),
+               pl->tM.what.as<double>(), pl->p.xi, 1.0 / ((double)M * M * M));
+        tm.mark();
+        SE_CUFFT(cufftExecZ2D(pl->fft_inv, pl->spec.as<cplx>(), grid));
+        tm.mark();
+    } else {
+        if (g.Mt % 2) fail(SE_EINVAL, "free-axis grid size must be even");
+        make_ffts(pl);
+        set_streams(pl, {pl->fft_fwd, pl->fft_inv, pl->fft_rowJ, pl->fft_rowI, pl->fft_row0});
+        const int M = g.M, Mt = g.Mt, half = M / 2 + 1, nfree = 3 - D;
+        const int nI = pl->nI_rows;
+        cplx *Hk = pl->spec.as<cplx>(), *Z = pl->spec2.as<cplx>(), *B = pl->spec3.as<cplx>();
+        const int *rows = pl->rows_I.as<int>();
+        MixArgs ma{D, M, pl->p.nI, half, pl->p.xi, g.R, pl->tM.k.as<double>(), pl->tM.what.as<double>()};
+        const double perN = D == 2 ? (double)M * M : (double)M;
+        auto pw = [&](int n) { return nfree == 1 ? (double)n : (double)n * n; };
+        tm.mark();
+        SE_CUFFT(cufftExecD2Z(pl->fft_fwd, grid, Hk));
+        LAUNCH(pack_kernel, (int64_t)pw(g.g0), Hk, Mt, nfree, nullptr, 1, Z, g.g0);
+        if (nI) LAUNCH(pack_kernel, (int64_t)pw(g.gs) * nI, Hk, Mt, nfree, rows, nI, B, g.gs);
+        SE_CUFFT(cufftExecZ2Z(pl->fft_rowJ, Hk, Hk, CUFFT_FORWARD));
+        if (nI) SE_CUFFT(cufftExecZ2Z(pl->fft_rowI, B, B, CUFFT_FORWARD));
+        SE_CUFFT(cufftExecZ2Z(pl->fft_row0, Z, Z, CUFFT_FORWARD));
+        tm.mark();
+        int64_t rowsN = D == 2 ? (int64_t)M * half : half;
+        LAUNCH(scale_mixJ_kernel, rowsN * (int64_t)pw(Mt), Hk, ma, Mt, pl->tMt.k.as<double>(),
+               pl->tMt.what.as<double>(), 1.0 / (pw(Mt) * perN));
+        if (nI)
+            LAUNCH(scale_mixI_kernel, (int64_t)pw(g.gs) * nI, B, ma, rows, nI, g.gs, pl->tgs.k.as<double>(),
+                   pl->tgs.what.as<double>(), 1.0 / (pw(g.gs) * perN));
+        LAUNCH(scale_mix0_kernel, (int64_t)pw(g.g0), Z, ma, g.g0, pl->tg0.k.as<double>(), pl->tg0.what.as<double>(),
+               1.0 / (pw(g.g0) * perN));
+        tm.mark();
+        SE_CUFFT(cufftExecZ2Z(pl->fft_rowJ, Hk, Hk, CUFFT_INVERSE));
+        if (nI) SE_CUFFT(cufftExecZ2Z(pl->fft_rowI, B, B, CUFFT_INVERSE));
+        SE_CUFFT(cufftExecZ2Z(pl->fft_row0, Z, Z, CUFFT_INVERSE));
+        if (nI) LAUNCH(unpack_kernel, (int64_t)pw(Mt) * nI, B, g.gs, nfree, rows, nI, Hk, Mt);
+        LAUNCH(unpack_kernel, (int64_t)pw(Mt), Z, g.g0, nfree, nullptr, 1, Hk, Mt);
+        SE_CUFFT(cufftExecZ2D(pl->fft_inv, Hk, grid));
+        tm.mark();
+    }
+    if (timings) {
+        SE_CUDA(cudaStreamSynchronize(pl->stream));
+        timings[SE_T_AFT] = tm.secs(0, 1);
+        timings[SE_T_SCALE] = tm.secs(1, 2);
+        timings[SE_T_AIFT] = tm.secs(2, 3);
+    }
+}
+
+}  // namespace se

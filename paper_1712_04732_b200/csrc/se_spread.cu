@@ -1,0 +1,500 @@
+// Spreading (particle -> grid) and gathering (grid -> particle) for the SE
+// Fourier pipeline: sekspace.spread / sekspace.gather (sekspace.py:105-178).
+//
+// Design (B200, fp64):
+//  * Particles are binned by the TILE of their stencil start index
+//    first = floor(u/h - P/2) + 1 (sekspace.py:114), stable-sorted, and split
+//    into work units of <= UNIT particles (clustered inputs stay balanced).
+//  * One CTA per unit accumulates into a zero-initialised padded tile of
+//    (T+P-1)^3 doubles in shared memory.  fp64 shared-memory atomics are
+//    CAS loops on sm_100a (ATOMS.CAST.SPIN.64), so the tile is updated with
+//    plain LDS/DFMA/STS and made race free by ownership: warp w owns the
+//    padded-tile x-planes lx == w (mod nwarps).  Every particle touches P
+//    consecutive x-planes, so with nwarps | P each warp updates exactly
+//    P/nwarps planes of every particle and no two warps ever touch the same
+//    address.  Lanes cover the P*P (y,z) footprint; the (y,z) weight product
+//    is formed once per particle and reused across the warp's planes.
+//  * The window factors (3P per particle, fused Gaussian / ES / KB
+//    evaluation) are computed once per particle into shared memory.
+//  * The tile is flushed with native fp64 global reductions
+//    (REDG.E.ADD.F64) into the L2-resident grid, wrapping periodic axes.
+//  * Gather mirrors this: the padded tile of the grid is staged in shared
+//    memory and a warp reduces each particle's P^3 stencil.
+// Windows whose padded tile cannot fit in shared memory (P > ~24) use a
+// direct kernel (one warp per particle, global fp64 reductions / loads).
+#include "se_common.h"
+
+namespace se {
+
+struct SpreadArgs {
+    int P, M, Mt, D;
+    int shape[3];
+    double h, halfP;
+    double off[3];
+    int T, Tp, pitch, nwarps, batch;
+    int nt[3];
+    int lo[3];
+    // window
+    int window;
+    double w, shapep, peak, mm, ww2, i0b;
+    int64_t rlo, rhi;  // sorted-particle range of this shard
+};
+
+// ---------------------------------------------------------------- windows
+template <int WIN>
+__device__ __forceinline__ double window_eval(double x, const SpreadArgs &a) {
+    if (!(fabs(x) <= a.w)) return 0.0;
+    if (WIN == SE_WINDOW_GAUSSIAN) {
+        // windows.py:81-83: peak * exp(-(m*m)*(x*x)/(2*w*w))
+        return a.peak * exp(__ddiv_rn(__dmul_rn(-a.mm, __dmul_rn(x, x)), a.ww2));
+    }
+    double r = __ddiv_rn(x, a.w);
+    double t = __dsub_rn(1.0, __dmul_rn(r, r));
+    t = t < 0.0 ? 0.0 : t;
+    if (WIN == SE_WINDOW_BM) return exp(__dmul_rn(a.shapep, __dsub_rn(sqrt(t), 1.0)));  // windows.py:151-153
+    return __ddiv_rn(cyl_bessel_i0(__dmul_rn(a.shapep, sqrt(t))), a.i0b);                 // windows.py:110-111
+}
+
+// first stencil index along one axis (sekspace.py:113-114), IEEE division.
+__device__ __forceinline__ long long stencil_first(double u, const SpreadArgs &a) {
+    return (long long)floor(__dsub_rn(__ddiv_rn(u, a.h), a.halfP)) + 1;
+}
+
+__device__ __forceinline__ int start_index(long long first, int axis, const SpreadArgs &a) {
+    if (axis < a.D) {
+        long long m = first % a.M;
+        return (int)(m < 0 ? m + a.M : m);
+    }
+    return (int)first;
+}
+
+__device__ __forceinline__ int tile_coord(int s, int axis, const SpreadArgs &a) {
+    int t = (s - a.lo[axis]) / a.T;
+    t = t < 0 ? 0 : t;
+    return t >= a.nt[axis] ? a.nt[axis] - 1 : t;
+}
+
+__global__ void tile_keys_kernel(const double *__restrict__ pos, int64_t N, SpreadArgs a,
+                                 unsigned *__restrict__ keys, int *__restrict__ counts) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    int tc[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        double u = __dadd_rn(pos[3 * i + ax], a.off[ax]);
+        tc[ax] = tile_coord(start_index(stencil_first(u, a), ax, a), ax, a);
+    }
+    unsigned key = (unsigned)((tc[0] * a.nt[1] + tc[1]) * a.nt[2] + tc[2]);
+    keys[i] = key;
+    atomicAdd(&counts[key], 1);
+}
+
+// Stage the 3P window factors of a batch of particles.  wts layout:
+// [p][axis][t]; loc: [p][4] = local start (x,y,z) within the padded tile and
+// the sorted index.  FOLDQ multiplies the x factors by the charge.
+template <int WIN, bool FOLDQ>
+__device__ __forceinline__ void stage_batch(const double4 *__restrict__ rec, int s0, int nb, const int org[3],
+                                            const SpreadArgs &a, double *wts, int *loc) {
+    const int P = a.P;
+    for (int task = threadIdx.x; task < nb * 3; task += blockDim.x) {
+        int p = task / 3, ax = task - 3 * p;
+        double4 r = rec[s0 + p];
+        double x = ax == 0 ? r.x : (ax == 1 ? r.y : r.z);
+        double u = __dadd_rn(x, a.off[ax]);
+        long long f = stencil_first(u, a);
+        double *wo = wts + (p * 3 + ax) * P;
+        for (int t = 0; t < P; ++t) {
+            double d = __dsub_rn(__dmul_rn((double)(f + t), a.h), u);  // sekspace.py:116
+            double v = window_eval<WIN>(d, a);
+            if (FOLDQ && ax == 0) v = __dmul_rn(r.w, v);
+            wo[t] = v;
+        }
+        loc[p * 4 + ax] = start_index(f, ax, a) - org[ax];
+        if (ax == 0) loc[p * 4 + 3] = s0 + p;
+    }
+}
+
+__device__ __forceinline__ void unit_origin(int bin, const SpreadArgs &a, int org[3]) {
+    int tz = bin % a.nt[2];
+    int ty = (bin / a.nt[2]) % a.nt[1];
+    int tx = bin / (a.nt[2] * a.nt[1]);
+    org[0] = a.lo[0] + tx * a.T;
+    org[1] = a.lo[1] + ty * a.T;
+    org[2] = a.lo[2] + tz * a.T;
+}
+
+// global linear index of padded-tile cell (lx,ly,lz); -1 if off the grid
+__device__ __forceinline__ long long tile_to_global(int lx, int ly, int lz, const int org[3], const SpreadArgs &a) {
+    int gidx[3] = {org[0] + lx, org[1] + ly, org[2] + lz};
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        if (ax < a.D) {
+            gidx[ax] %= a.M;
+        } else if (gidx[ax] < 0 || gidx[ax] >= a.Mt) {
+            return -1;
+        }
+    }
+    return ((long long)gidx[0] * a.shape[1] + gidx[1]) * a.shape[2] + gidx[2];
+}
+
+template <int WIN>
+__global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restrict__ rec, const int4 *__restrict__ units,
+                                                          const int *__restrict__ nunits, SpreadArgs a,
+                                                          double *__restrict__ grid) {
+    if ((int)blockIdx.x >= *nunits) return;
+    int4 un = units[blockIdx.x];
+    int ubeg = (int)max((int64_t)un.y, a.rlo), uend = (int)min((int64_t)un.y + un.z, a.rhi);
+    if (ubeg >= uend) return;
+    extern __shared__ double smem[];
+    const int P = a.P, Tp = a.Tp, pitch = a.pitch, plane = Tp * pitch;
+    const int ncell = Tp * plane;
+    double *tile = smem;
+    double *wts = tile + ncell;
+    int *loc = reinterpret_cast<int *>(wts + a.batch * 3 * P);
+    int org[3];
+    unit_origin(un.x, a, org);
+    for (int i = threadIdx.x; i < ncell; i += blockDim.x) tile[i] = 0.0;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = a.nwarps;
+    const int npair = P * P;
+    for (int b0 = ubeg; b0 < uend; b0 += a.batch) {
+        int nb = min(a.batch, uend - b0);
+        __syncthreads();  // tile zeroed / previous batch consumed
+        stage_batch<WIN, true>(rec, b0, nb, org, a, wts, loc);
+        __syncthreads();
+        for (int p = 0; p < nb; ++p) {
+            const int lx0 = loc[p * 4], ly0 = loc[p * 4 + 1], lz0 = loc[p * 4 + 2];
+            const double *wx = wts + p * 3 * P, *wy = wx + P, *wz = wy + P;
+            int t0 = (warp - lx0) % nw;
+            t0 = t0 < 0 ? t0 + nw : t0;
+            for (int pi = lane; pi < npair; pi += 32) {
+                int ty = pi / P, tz = pi - ty * P;
+                double cyz = __dmul_rn(wy[ty], wz[tz]);
+                int off = (ly0 + ty) * pitch + lz0 + tz;
+                for (int t = t0; t < P; t += nw) {
+                    double *c = tile + (lx0 + t) * plane + off;
+                    *c = fma(wx[t], cyz, *c);
+                }
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ncell; i += blockDim.x) {
+        double v = tile[i];
+        if (v == 0.0) continue;
+        int lx = i / plane, rem = i - lx * plane, ly = rem / pitch, lz = rem - ly * pitch;
+        if (lz >= Tp) continue;
+        long long gi = tile_to_global(lx, ly, lz, org, a);
+        if (gi >= 0) atomicAdd(grid + gi, v);
+    }
+}
+
+template <int WIN>
+__global__ void __launch_bounds__(512) gather_tile_kernel(const double4 *__restrict__ rec, const int *__restrict__ sidx,
+                                                          const int4 *__restrict__ units, const int *__restrict__ nunits,
+                                                          SpreadArgs a, const double *__restrict__ grid,
+                                                          double *__restrict__ phi, double h3, int accumulate) {
+    if ((int)blockIdx.x >= *nunits) return;
+    int4 un = units[blockIdx.x];
+    int ubeg = (int)max((int64_t)un.y, a.rlo), uend = (int)min((int64_t)un.y + un.z, a.rhi);
+    if (ubeg >= uend) return;
+    extern __shared__ double smem[];
+    const int P = a.P, Tp = a.Tp, pitch = a.pitch, plane = Tp * pitch;
+    const int ncell = Tp * plane;
+    double *tile = smem;
+    double *wts = tile + ncell;
+    int *loc = reinterpret_cast<int *>(wts + a.batch * 3 * P);
+    int org[3];
+    unit_origin(un.x, a, org);
+    for (int i = threadIdx.x; i < ncell; i += blockDim.x) {
+        int lx = i / plane, rem = i - lx * plane, ly = rem / pitch, lz = rem - ly * pitch;
+        double v = 0.0;
+        if (lz < Tp) {
+            long long gi = tile_to_global(lx, ly, lz, org, a);
+            if (gi >= 0) v = grid[gi];
+        }
+        tile[i] = v;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = a.nwarps;
+    const int npair = P * P;
+    for (int b0 = ubeg; b0 < uend; b0 += a.batch) {
+        int nb = min(a.batch, uend - b0);
+        __syncthreads();
+        stage_batch<WIN, false>(rec, b0, nb, org, a, wts, loc);
+        __syncthreads();
+        for (int p = warp; p < nb; p += nw) {
+            const int lx0 = loc[p * 4], ly0 = loc[p * 4 + 1], lz0 = loc[p * 4 + 2];
+            const double *wx = wts + p * 3 * P, *wy = wx + P, *wz = wy + P;
+            double acc = 0.0;
+            for (int pi = lane; pi < npair; pi += 32) {
+                int ty = pi / P, tz = pi - ty * P;
+                const double *c = tile + lx0 * plane + (ly0 + ty) * pitch + lz0 + tz;
+                double s = 0.0;
+                for (int t = 0; t < P; ++t) s = fma(wx[t], c[t * plane], s);
+                acc = fma(__dmul_rn(wy[ty], wz[tz]), s, acc);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) {
+                int orig = sidx[loc[p * 4 + 3]];
+                double v = acc * h3;
+                phi[orig] = accumulate ? phi[orig] + v : v;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------- large-P direct path
+template <int WIN, bool SPREAD>
+__global__ void direct_kernel(const double4 *__restrict__ rec, const int *__restrict__ sidx, int64_t rlo, int64_t rhi,
+                              SpreadArgs a, double *__restrict__ grid, const double *__restrict__ gin,
+                              double *__restrict__ phi, double h3, int accumulate) {
+    extern __shared__ double smem[];
+    const int P = a.P;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *w = smem + warp * 3 * P;
+    int64_t i = rlo + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (i >= rhi) return;
+    double4 r = rec[i];
+    long long f[3];
+    int s[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        double x = ax == 0 ? r.x : (ax == 1 ? r.y : r.z);
+        double u = __dadd_rn(x, a.off[ax]);
+        f[ax] = stencil_first(u, a);
+        s[ax] = start_index(f[ax], ax, a);
+        for (int t = lane; t < P; t += 32) {
+            double d = __dsub_rn(__dmul_rn((double)(f[ax] + t), a.h), u);
+            double v = window_eval<WIN>(d, a);
+            if (SPREAD && ax == 0) v = __dmul_rn(r.w, v);
+            w[ax * P + t] = v;
+        }
+    }
+    __syncwarp();
+    double acc = 0.0;
+    for (int pi = lane; pi < P * P; pi += 32) {
+        int ty = pi / P, tz = pi - ty * P;
+        int gy = s[1] + ty, gz = s[2] + tz;
+        if (1 < a.D) gy %= a.M;
+        if (2 < a.D) gz %= a.M;
+        if (gy >= a.shape[1] || gz >= a.shape[2]) continue;
+        double cyz = __dmul_rn(w[P + ty], w[2 * P + tz]);
+        double sacc = 0.0;
+        for (int t = 0; t < P; ++t) {
+            int gx = s[0] + t;
+            if (0 < a.D) gx %= a.M;
+            if (gx >= a.shape[0]) continue;
+            long long gi = ((long long)gx * a.shape[1] + gy) * a.shape[2] + gz;
+            if (SPREAD)
+                atomicAdd(grid + gi, w[t] * cyz);
+            else
+                sacc = fma(w[t], gin[gi], sacc);
+        }
+        if (!SPREAD) acc = fma(cyz, sacc, acc);
+    }
+    if (!SPREAD) {
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            int orig = sidx[i];
+            double v = acc * h3;
+            phi[orig] = accumulate ? phi[orig] + v : v;
+        }
+    }
+}
+
+// --------------------------------------------------------------- host side
+static SpreadArgs make_args(se_plan *pl) {
+    const se_grid_t &g = pl->g;
+    const se_params_t &p = pl->p;
+    SpreadArgs a{};
+    a.P = p.P;
+    a.M = g.M;
+    a.Mt = g.Mt;
+    a.D = g.D;
+    for (int i = 0; i < 3; ++i) {
+        a.shape[i] = g.shape[i];
+        a.off[i] = g.offsets[i];
+    }
+    a.h = g.h;
+    a.halfP = 0.5 * p.P;
+    a.window = p.window;
+    a.w = 0.5 * p.P * g.h;
+    a.shapep = p.shape;
+    a.peak = p.shape / (a.w * std::sqrt(2.0 * M_PI));
+    a.mm = p.shape * p.shape;
+    a.ww2 = 2.0 * a.w * a.w;
+    a.i0b = 1.0;
+    if (p.window == SE_WINDOW_KB) a.i0b = bessel_i0(p.shape);
+    const TileGeom &t = pl->tile;
+    a.T = t.T;
+    a.Tp = t.Tp;
+    a.pitch = t.pitch;
+    a.nwarps = t.nwarps;
+    a.batch = t.batch;
+    for (int i = 0; i < 3; ++i) {
+        a.nt[i] = t.nt[i];
+        a.lo[i] = t.lo[i];
+    }
+    return a;
+}
+
+static const int kUnit = 1024;     // particles per spreading work unit
+static const size_t kSmemCap = 200 * 1024;
+
+void tile_setup(se_plan *pl) {
+    TileGeom &t = pl->tile;
+    if (t.T) return;
+    const int P = pl->p.P;
+    int nw = P <= 16 ? P : 16;
+    while (nw > 1 && P % nw) --nw;
+    if (nw < 4 && P > 4) nw = P < 16 ? P : 16;  // keep enough warps even if nw does not divide P
+    t.nwarps = nw;
+    t.batch = 64;
+    const int cand[] = {16, 14, 12, 10, 8, 6, 4, 2, 1};
+    t.T = 0;
+    for (size_t pass = 0; pass < 2 && !t.T; ++pass) {
+        size_t cap = pass == 0 ? 110 * 1024 : kSmemCap;
+        for (int T : cand) {
+            int Tp = T + P - 1;
+            int pitch = Tp;
+            if (P % 16 == 8) pitch = Tp + ((8 - Tp % 16) + 16) % 16;
+            size_t bytes = sizeof(double) * ((size_t)Tp * Tp * pitch + (size_t)t.batch * 3 * P) + sizeof(int) * 4 * t.batch;
+            if (bytes <= cap) {
+                t.T = T;
+                t.Tp = Tp;
+                t.pitch = pitch;
+                t.smem = bytes;
+                break;
+            }
+        }
+    }
+    if (!t.T) {  // direct path
+        t.T = -1;
+        t.Tp = 0;
+        t.pitch = 0;
+        t.smem = 0;
+        for (int i = 0; i < 3; ++i) {
+            t.nt[i] = 1;
+            t.lo[i] = 0;
+        }
+        return;
+    }
+    for (int ax = 0; ax < 3; ++ax) {
+        int extent = ax < pl->g.D ? pl->g.M : pl->g.M + 2;
+        t.lo[ax] = 0;
+        t.nt[ax] = (extent + t.T - 1) / t.T;
+    }
+}
+
+static void bin_tiles(se_plan *pl, const double *pos, const double *q, int64_t N) {
+    tile_setup(pl);
+    TileGeom &t = pl->tile;
+    int nbins = t.nt[0] * t.nt[1] * t.nt[2];
+    binning_reserve(pl->tbin, N, nbins, kUnit);
+    prof_begin(pl, SE_K_SORT);
+    SE_CUDA(cudaMemsetAsync(pl->tbin.counts.ptr, 0, sizeof(int) * (nbins + 1), pl->stream));
+    SpreadArgs a = make_args(pl);
+    if (N > 0) {
+        tile_keys_kernel<<<(unsigned)((N + 255) / 256), 256, 0, pl->stream>>>(pos, N, a, pl->tbin.keys.as<unsigned>(),
+                                                                               pl->tbin.counts.as<int>());
+        SE_LAUNCH_CHECK();
+        pl->launches += 1;
+    }
+    binning_sort(pl, pl->tbin, pos, q, N, nbins, kUnit);
+    prof_end(pl, SE_K_SORT);
+}
+
+template <class F>
+static void dispatch_window(int window, F f) {
+    if (window == SE_WINDOW_GAUSSIAN)
+        f(std::integral_constant<int, SE_WINDOW_GAUSSIAN>());
+    else if (window == SE_WINDOW_KB)
+        f(std::integral_constant<int, SE_WINDOW_KB>());
+    else
+        f(std::integral_constant<int, SE_WINDOW_BM>());
+}
+
+static void shard_range(int64_t N, int rank, int world, int64_t &lo, int64_t &hi) {
+    lo = N * rank / world;
+    hi = N * (rank + 1) / world;
+}
+
+void spread_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *grid, int rank, int world) {
+    if (pl->p.P > pl->g.M) fail(SE_EINVAL, "window support P must not exceed M");
+    const se_grid_t &g = pl->g;
+    size_t gsize = (size_t)g.shape[0] * g.shape[1] * g.shape[2];
+    SE_CUDA(cudaMemsetAsync(grid, 0, sizeof(double) * gsize, pl->stream));
+    if (N <= 0) return;
+    bin_tiles(pl, pos, q, N);
+    SpreadArgs a = make_args(pl);
+    shard_range(N, rank, world, a.rlo, a.rhi);
+    const TileGeom &t = pl->tile;
+    const double4 *rec = pl->tbin.rec.as<double4>();
+    prof_begin(pl, SE_K_SPREAD);
+    if (t.T > 0) {
+        int64_t maxu = binning_max_units(pl->tbin, N, t.nt[0] * t.nt[1] * t.nt[2], kUnit);
+        dispatch_window(pl->p.window, [&](auto W) {
+            auto kern = spread_tile_kernel<decltype(W)::value>;
+            SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
+            kern<<<(unsigned)maxu, 32 * t.nwarps, t.smem, pl->stream>>>(rec, pl->tbin.units.as<int4>(),
+                                                                         pl->tbin.nunits.as<int>(), a, grid);
+        });
+    } else {
+        int64_t n = a.rhi - a.rlo;
+        int wpb = 4;
+        size_t sm = sizeof(double) * 3 * pl->p.P * wpb;
+        dispatch_window(pl->p.window, [&](auto W) {
+            auto kern = direct_kernel<decltype(W)::value, true>;
+            SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            kern<<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, sm, pl->stream>>>(
+                rec, pl->tbin.idx_sorted.as<int>(), a.rlo, a.rhi, a, grid, nullptr, nullptr, 0.0, 0);
+        });
+    }
+    SE_LAUNCH_CHECK();
+    prof_end(pl, SE_K_SPREAD);
+    pl->launches += 1;
+}
+
+void gather_run(se_plan *pl, const double *grid, const double *pos, int64_t N, double *phi, int accumulate,
+                int rank, int world, bool rebin) {
+    if (N <= 0) return;
+    // the fused pipelines reuse the spreading bins (same positions); a
+    // stand-alone gather bins its own positions (charges are not read)
+    if (rebin) bin_tiles(pl, pos, nullptr, N);
+    SpreadArgs a = make_args(pl);
+    int64_t lo, hi;
+    shard_range(N, rank, world, lo, hi);
+    a.rlo = lo;
+    a.rhi = hi;
+    if (!accumulate && world > 1) SE_CUDA(cudaMemsetAsync(phi, 0, sizeof(double) * N, pl->stream));
+    const TileGeom &t = pl->tile;
+    const double h3 = pl->g.h * pl->g.h * pl->g.h;
+    const double4 *rec = pl->tbin.rec.as<double4>();
+    prof_begin(pl, SE_K_GATHER);
+    if (t.T > 0) {
+        int64_t maxu = binning_max_units(pl->tbin, N, t.nt[0] * t.nt[1] * t.nt[2], kUnit);
+        dispatch_window(pl->p.window, [&](auto W) {
+            auto kern = gather_tile_kernel<decltype(W)::value>;
+            SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
+            kern<<<(unsigned)maxu, 32 * t.nwarps, t.smem, pl->stream>>>(
+                rec, pl->tbin.idx_sorted.as<int>(), pl->tbin.units.as<int4>(), pl->tbin.nunits.as<int>(), a, grid,
+                phi, h3, accumulate);
+        });
+    } else {
+        int64_t n = a.rhi - a.rlo;
+        int wpb = 4;
+        size_t sm = sizeof(double) * 3 * pl->p.P * wpb;
+        dispatch_window(pl->p.window, [&](auto W) {
+            auto kern = direct_kernel<decltype(W)::value, false>;
+            SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            kern<<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, sm, pl->stream>>>(
+                rec, pl->tbin.idx_sorted.as<int>(), a.rlo, a.rhi, a, nullptr, grid, phi, h3, accumulate);
+        });
+    }
+    SE_LAUNCH_CHECK();
+    prof_end(pl, SE_K_GATHER);
+    pl->launches += 1;
+}
+
+}  // namespace se

@@ -1,0 +1,191 @@
+"""Fourier-space pipeline (mirror of pmewald.sekspace) on the SE B200 library.
+
+Stage calls map onto the C ABI (include/se_b200.h):
+
+    spread                      -> se_spread_host      (tile-binned smem spreading kernel)
+    gather                      -> se_gather_host      (tile-staged gather kernel)
+    apply_kspace                -> se_kspace_apply_host (cuFFT + fused multiplier)
+    se_kspace                   -> se_kspace_potential_host (spread, k-space, gather)
+    precompute_truncated_greens -> se_d0_kernel_table_host (device precompute)
+
+Grid geometry and the D=0 kernel geometry come from the library's planning
+routines (sekspace.py:53-70, 266-279 of the reference).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native, windows
+from .core import ParticleSystem, Periodicity, SEParams
+
+
+@dataclass(frozen=True)
+class Grid:
+    """Grid geometry (sekspace.py:36-70): M per periodic axis, Mt = M + P per
+    free axis, spacing h = L/M, free-axis offsets P h / 2."""
+
+    L: float
+    M: int
+    P: int
+    D: int
+    h: float
+    Lt: float
+    Mt: int
+    R: float
+    g0: int
+    gs: int
+
+    @classmethod
+    def build(cls, L: float, params: SEParams, periodicity: Periodicity) -> "Grid":
+        g = _native.se_grid_t()
+        _native.call("se_grid_build", int(periodicity.D), float(L),
+                     _native.params_struct(params), ctypes.byref(g))
+        return cls(g.L, g.M, g.P, g.D, g.h, g.Lt, g.Mt, g.R, g.g0, g.gs)
+
+    @property
+    def shape(self) -> tuple[int, int, int]:
+        return tuple(self.M if a < self.D else self.Mt for a in range(3))
+
+    @property
+    def offsets(self) -> np.ndarray:
+        return np.array([0.0 if a < self.D else 0.5 * self.P * self.h for a in range(3)])
+
+
+@dataclass(frozen=True)
+class GridField:
+    values: np.ndarray
+    grid: Grid
+
+
+@dataclass(frozen=True)
+class PrecomputedKernel:
+    """Truncated free-space kernel on the convolution grid (sekspace.py:73-94)."""
+
+    Mt: int
+    g0: int
+    nconv: int
+    R: float
+    h: float
+    ghat: np.ndarray
+
+
+_KERNEL_CACHE: dict = {}
+
+
+def mode_values(n: int, h: float) -> np.ndarray:
+    """2 pi fftfreq(n, d=h) (sekspace.py:100-102)."""
+    return 2.0 * np.pi * np.fft.fftfreq(n, d=h)
+
+
+def _stage_params(grid: Grid, wspec: windows.WindowSpec) -> SEParams:
+    """Parameters that pin a library plan to (grid, window) for the stage calls;
+    xi / rc / upsampling do not enter spreading or gathering."""
+    s0 = max(1.0, grid.g0 / grid.Mt) if grid.D < 3 else 1.0
+    return SEParams(xi=1.0, rc=1.0, M=grid.M, P=grid.P, window=wspec.kind, shape=wspec.shape,
+                    s0=s0, s=1.0, nI=0, R=grid.R if grid.R > 0 else 1.0, eps=1e-12)
+
+
+def _stage_plan(grid: Grid, wspec: windows.WindowSpec):
+    if grid.P > grid.M:
+        raise ValueError("window support P must not exceed M")
+    return _native.plan_for(grid.D, grid.L, _stage_params(grid, wspec))
+
+
+def spread(system: ParticleSystem, wspec: windows.WindowSpec, grid: Grid,
+           periodicity: Periodicity, threads: int = 1) -> GridField:
+    """H = sum_n q_n w (x) w (x) w on the grid (sekspace.py:130-156)."""
+    plan = _stage_plan(grid, wspec)
+    out = np.empty(grid.shape)
+    _native.call("se_spread_host", plan.handle, _native.ptr(system.positions),
+                 _native.ptr(system.charges), system.N, _native.ptr(out))
+    return GridField(out, grid)
+
+
+def gather(field: GridField, system: ParticleSystem, wspec: windows.WindowSpec,
+           periodicity: Periodicity, threads: int = 1) -> np.ndarray:
+    """phi_m = h^3 sum H~ w (x) w (x) w, the adjoint of spread (sekspace.py:159-178)."""
+    grid = field.grid
+    plan = _stage_plan(grid, wspec)
+    H = np.ascontiguousarray(field.values, dtype=np.float64)
+    if H.shape != grid.shape:
+        raise ValueError("grid values do not match the grid shape")
+    phi = np.empty(system.N)
+    _native.call("se_gather_host", plan.handle, _native.ptr(H), _native.ptr(system.positions),
+                 system.N, _native.ptr(phi))
+    return phi
+
+
+def apply_kspace(field: GridField, params: SEParams, periodicity: Periodicity,
+                 use_kernel: bool | None = None) -> GridField:
+    """H -> H~: aft_forward, scale, aft_inverse, real part (sekspace.py:366-381),
+    or the D=0 precomputed-kernel path (sekspace.py:301-337)."""
+    plan = _native.plan_for(periodicity.D, field.grid.L, params)
+    H = np.array(field.values, dtype=np.float64, order="C", copy=True)
+    uk = 1 if (periodicity.D == 0 and (use_kernel or use_kernel is None)) else 0
+    _native.call("se_kspace_apply_host", plan.handle, _native.ptr(H), uk)
+    return GridField(H, field.grid)
+
+
+def precompute_truncated_greens(L: float, M: int, P: int, s0: float,
+                                rc: float | None = None) -> PrecomputedKernel:
+    """Tabulate the truncated free-space kernel on the device (sekspace.py:257-298)."""
+    if s0 < 1.0 + math.sqrt(3.0) - 1e-12:
+        raise ValueError("free-space precompute requires s0 >= 1 + sqrt(3)")
+    rcv = 1e-300 if rc is None else float(rc)  # margin = max(P h, min(rc, L))
+    nconv, g0, R = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
+    _native.call("se_d0_kernel_geometry", float(L), int(M), int(P), float(s0), rcv,
+                 ctypes.byref(nconv), ctypes.byref(g0), ctypes.byref(R))
+    h = L / M
+    key = (M + P, g0.value, nconv.value, round(R.value, 12), round(h, 12))
+    hit = _KERNEL_CACHE.get(key)
+    if hit is not None:
+        return hit
+    prm = SEParams(xi=1.0, rc=rcv, M=M, P=P, window="bm", shape=2.5 * P, s0=s0, R=1.0)
+    plan = _native.Plan(0, L, prm)
+    n = nconv.value
+    tab = np.empty((n, n, n // 2 + 1))
+    _native.call("se_d0_kernel_table_host", plan.handle, _native.ptr(tab))
+    kern = PrecomputedKernel(M + P, g0.value, n, R.value, h, tab)
+    _KERNEL_CACHE[key] = kern
+    return kern
+
+
+def se_kspace(system: ParticleSystem, params: SEParams, periodicity: Periodicity,
+              threads: int = 1, timings: dict | None = None,
+              use_kernel: bool | None = None) -> np.ndarray:
+    """Fourier-space potential at every source (sekspace.py:340-389)."""
+    params.validate(system.L, periodicity)
+    plan = _native.plan_for(periodicity.D, system.L, params)
+    uk = 1 if (periodicity.D == 0 and (use_kernel or use_kernel is None)) else 0
+    phi = np.empty(system.N)
+    tb = _native.timings_buffer() if timings is not None else None
+    _native.call("se_kspace_potential_host", plan.handle, _native.ptr(system.positions),
+                 _native.ptr(system.charges), system.N, _native.ptr(phi), uk,
+                 _native.ptr(tb) if tb is not None else None)
+    if timings is not None:
+        _native.fill_timings(timings, tb, ("spread", "aft", "scale", "aift", "gather"))
+        timings.setdefault("precompute", float(tb[_native.TIMING_KEYS.index("precompute")]))
+    return phi
+
+
+def global_upsampled_kspace(system: ParticleSystem, params: SEParams,
+                            periodicity: Periodicity) -> np.ndarray:
+    """Validation path with every free axis padded at s0 (sekspace.py:392-435).
+
+    With nI = M/2 and s = s0 the adaptive transform degenerates to exactly this
+    single padded transform (the reference's own acceptance criterion,
+    test_acceptance.py:134-147); D=0 is the use_kernel=False path.
+    """
+    D = periodicity.D
+    params.validate(system.L, periodicity)
+    if D == 3:
+        return se_kspace(system, params, periodicity)
+    if D == 0:
+        return se_kspace(system, params, periodicity, use_kernel=False)
+    degenerate = SEParams(**{**params.__dict__, "nI": params.M // 2, "s": params.s0})
+    return se_kspace(system, degenerate, periodicity)

@@ -1,0 +1,350 @@
+"""GPU parity: the sm_100a pipeline through the public API (C ABI) against
+the reference's golden vectors and the CPU oracle (oracle/se_oracle.py).
+
+Tolerances: every comparison is fp64; the north-star bar is relative RMS
+<= 1e-10 against the reference CPU implementation.  Stage comparisons use
+tighter bounds (1e-12 .. 1e-13) because the only differences are rounding
+(fp64 atomics in spreading, cuFFT vs pocketfft, CUDA vs cephes erfc).
+"""
+
+import math
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, PIPELINE_CASES, load_case
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import se_oracle as orc  # noqa: E402
+
+import paper_1712_04732_b200 as se  # noqa: E402
+from paper_1712_04732_b200 import device as sedev  # noqa: E402
+from paper_1712_04732_b200 import sekspace, windows  # noqa: E402
+
+FIELDS = ("xi", "rc", "M", "P", "window", "shape", "s0", "s", "nI", "R", "eps")
+PARITY = 1e-10  # north_star bar (relative RMS vs the reference CPU path)
+
+
+def params_of(c):
+    return se.SEParams(**{k: c["prm"][k] for k in FIELDS})
+
+
+def system_of(c):
+    return se.ParticleSystem(c["pos"], c["q"], c["L"])
+
+
+def rand_system(N, L, seed):
+    rng = np.random.default_rng(seed)
+    pos = rng.random((N, 3)) * L
+    q = rng.uniform(-1, 1, N)
+    q -= q.mean()
+    return se.ParticleSystem(pos, q, L)
+
+
+# ------------------------------------------------------------ golden vectors
+
+@pytest.mark.parametrize("name", PIPELINE_CASES)
+def test_golden_stages(name):
+    c = load_case(name)
+    s, p, peri = system_of(c), params_of(c), se.Periodicity(c["D"])
+    grid = sekspace.Grid.build(s.L, p, peri)
+    wspec = windows.WindowSpec(p.window, p.P, grid.h, p.shape)
+    H = sekspace.spread(s, wspec, grid, peri).values
+    assert np.max(np.abs(H - c["H"])) <= 1e-13 * np.max(np.abs(c["H"]))
+    uk = None if c["use_kernel"] < 0 else bool(c["use_kernel"])
+    phik = se.se_kspace(s, p, peri, use_kernel=uk)
+    assert se.relative_rms_error(phik, c["phi_k"]) < 1e-12
+    if "phi_r" in c:
+        phir = se.real_space_sum(s, p.xi, p.rc, peri)
+        assert np.allclose(phir, c["phi_r"], rtol=1e-12, atol=1e-13)
+        assert np.allclose(se.self_term(s.charges, p.xi), c["phi_s"], rtol=1e-15, atol=0)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            phi = se.total_potential(s, p, peri) if uk is None else phir + phik + se.self_term(s.charges, p.xi)
+        assert se.relative_rms_error(phi, c["phi"]) < PARITY
+        assert se.relative_rms_error(phi, c["phi"]) < 1e-12
+
+
+def test_golden_realspace_paths():
+    z = np.load(os.path.join(GOLDEN, "realspace.npz"))
+    s = se.ParticleSystem(z["img_pos"], z["img_q"], 1.0)
+    for D, rc in ((3, 1.2), (2, 0.8), (1, 0.7)):
+        assert np.allclose(se.real_space_sum(s, 4.0, rc, se.Periodicity(D)), z[f"img_d{D}"], rtol=1e-12, atol=1e-13)
+    s = se.ParticleSystem(z["cell_pos"], z["cell_q"], 1.0)
+    for D in (0, 1, 2, 3):
+        assert np.allclose(se.real_space_sum(s, 7.0, 0.23, se.Periodicity(D)), z[f"cell_d{D}"], rtol=1e-12, atol=1e-13)
+        assert np.allclose(se.real_space_sum(s, 5.0, 0.45, se.Periodicity(D)), z[f"cell2_d{D}"], rtol=1e-12, atol=1e-13)
+
+
+def test_golden_d0_kernel_table():
+    z = np.load(os.path.join(GOLDEN, "d0_kernel.npz"))
+    k = sekspace.precompute_truncated_greens(1.0, 16, 8, 1 + math.sqrt(3.0), rc=0.5)
+    assert k.nconv == int(z["nconv"]) and k.g0 == int(z["g0"])
+    assert np.max(np.abs(k.ghat - z["ghat"])) <= 1e-12 * np.max(np.abs(z["ghat"]))
+    assert sekspace.precompute_truncated_greens(1.0, 16, 8, 1 + math.sqrt(3.0), rc=0.5) is k
+
+
+# ------------------------------------------------------- oracle, larger sizes
+
+CFG_SMALL = {
+    # cfg1 exactly (N=2000, Gaussian P=16, M=32, rc=0.3, xi=12.94)
+    "cfg1": (3, 2000, 1.0, dict(xi=12.94, rc=0.3, M=32, P=16, window="gaussian",
+                                shape=math.sqrt(16 * math.pi), eps=1e-8)),
+    # cfg2 shape at 1/100 of the particles (same density: L = 10 * 0.1^(2/3))
+    "cfg2_small": (3, 10000, 10.0 * 0.01 ** (1 / 3), dict(xi=4.2919, rc=1.0, M=28, P=8, window="bm",
+                                                          shape=20.0, eps=1e-8)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CFG_SMALL))
+def test_oracle_parity_configs(name):
+    D, N, L, prm = CFG_SMALL[name]
+    s = rand_system(N, L, 11)
+    p = se.SEParams(**prm)
+    phi = se.total_potential(s, p, se.Periodicity(D))
+    ref = orc.total_potential(s.positions, s.charges, L, D, dict(p.__dict__))
+    assert se.relative_rms_error(phi, ref) < PARITY
+
+
+@pytest.mark.parametrize("D", [0, 1, 2])
+def test_oracle_parity_mixed(D):
+    # cfg3/4/5 shapes at reduced N and grids
+    s = rand_system(3000, 2.0, 20 + D)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        p, _ = se.auto_params(s, se.Periodicity(D), 4.0, 1e-8,
+                              window="gaussian" if D == 1 else "bm")
+    phi = se.total_potential(s, p, se.Periodicity(D))
+    ref = orc.total_potential(s.positions, s.charges, s.L, D, dict(p.__dict__))
+    assert se.relative_rms_error(phi, ref) < PARITY
+
+
+def test_d0_full_path_matches_oracle_and_kernel():
+    s = rand_system(200, 1.0, 5)
+    p = se.SEParams(xi=8.0, rc=0.43, M=24, P=16, window="bm", shape=40.0, s0=3.0, R=2.9, eps=1e-12)
+    full = se.se_kspace(s, p, se.Periodicity(0), use_kernel=False)
+    kern = se.se_kspace(s, p, se.Periodicity(0), use_kernel=True)
+    ref = orc.se_kspace(s.positions, s.charges, 1.0, 0, dict(p.__dict__), use_kernel=False)
+    assert se.relative_rms_error(full, ref) < 1e-12
+    assert se.relative_rms_error(kern, full) < 1e-10
+
+
+@pytest.mark.parametrize("D", [1, 2])
+def test_degenerate_aft_equals_global_padding(D):
+    s = rand_system(60, 1.0, 6 + D)
+    M, P = 16, 8
+    rc = 0.5
+    s0 = max(1 + math.sqrt(3 - D), ((1 + math.sqrt(3 - D)) + 2 * rc) / 1.5)
+    from paper_1712_04732_b200 import aft
+    R = 0.5 * (aft.padded_size(s0, M + P) / M - 1 + math.sqrt(3 - D))
+    p = se.SEParams(xi=5.0, rc=rc, M=M, P=P, window="bm", shape=20.0, s0=s0, s=s0, nI=M // 2, R=R, eps=1e-8)
+    a = se.se_kspace(s, p, se.Periodicity(D))
+    b = sekspace.global_upsampled_kspace(s, p, se.Periodicity(D))
+    ref = orc.se_kspace(s.positions, s.charges, 1.0, D, dict(p.__dict__))
+    assert se.relative_rms_error(a, b) < 1e-13
+    assert se.relative_rms_error(a, ref) < 1e-12
+
+
+def test_large_support_direct_path():
+    # P=34 > shared-memory tile capacity: direct global-atomic spreading path
+    s = rand_system(80, 1.0, 9)
+    p = se.SEParams(xi=12.0, rc=0.4, M=64, P=34, window="bm", shape=85.0, eps=1e-12)
+    phi = se.se_kspace(s, p, se.Periodicity(3))
+    ref = orc.se_kspace(s.positions, s.charges, 1.0, 3, dict(p.__dict__))
+    assert se.relative_rms_error(phi, ref) < 1e-12
+
+
+# ----------------------------------------------------------- reference tests
+
+def test_spread_gather_adjoint_all_periodicities():
+    rng = np.random.default_rng(15)
+    for D in (0, 1, 2, 3):
+        for window in ("bm", "gaussian", "kb"):
+            p = se.SEParams(xi=5.0, rc=0.4, M=14, P=6, window=window,
+                            shape=windows.default_shape(window, 6), s0=3.0, R=2.0)
+            grid = sekspace.Grid.build(1.0, p, se.Periodicity(D))
+            wspec = windows.WindowSpec(window, 6, grid.h, p.shape)
+            s = se.generate_random_system(9, 1.0, seed=D)
+            H = sekspace.spread(s, wspec, grid, se.Periodicity(D))
+            G = rng.normal(size=grid.shape)
+            lhs = grid.h ** 3 * float(np.sum(H.values * G))
+            rhs = float(s.charges @ sekspace.gather(sekspace.GridField(G, grid), s, wspec, se.Periodicity(D)))
+            assert lhs == pytest.approx(rhs, rel=1e-13)
+
+
+def test_spread_on_node_tensor_window_and_count():
+    M, P = 16, 6
+    p = se.SEParams(xi=5.0, rc=0.4, M=M, P=P, window="bm", shape=15.0, s0=3.0, R=2.0)
+    grid = sekspace.Grid.build(1.0, p, se.Periodicity(0))
+    wspec = windows.WindowSpec("bm", P, grid.h, 15.0)
+    x = 5 * grid.h
+    H = sekspace.spread(se.ParticleSystem(np.array([[x, x, x]]), np.array([1.0]), 1.0), wspec, grid,
+                        se.Periodicity(0)).values
+    ref = orc.spread(np.array([[x, x, x]]), np.array([1.0]), orc.geometry(1.0, 0, M, P, 3.0, 1.0, 2.0), "bm", 15.0)
+    assert np.array_equal(H != 0, ref != 0)
+    assert np.allclose(H, ref, rtol=1e-14, atol=1e-300)
+    p3 = se.SEParams(xi=5.0, rc=0.4, M=20, P=6, window="bm", shape=15.0)
+    g3 = sekspace.Grid.build(1.0, p3, se.Periodicity(3))
+    H3 = sekspace.spread(se.ParticleSystem(np.array([[0.311, 0.77, 0.132]]), np.array([1.0]), 1.0),
+                         windows.WindowSpec("bm", 6, g3.h, 15.0), g3, se.Periodicity(3)).values
+    assert np.count_nonzero(H3) == 6 ** 3
+
+
+def test_empty_and_zero_charge_systems():
+    p = se.SEParams(xi=6.0, rc=0.4, M=16, P=8, window="bm", shape=20.0, eps=1e-8)
+    grid = sekspace.Grid.build(1.0, p, se.Periodicity(3))
+    wspec = windows.WindowSpec("bm", 8, grid.h, 20.0)
+    empty = se.ParticleSystem(np.empty((0, 3)), np.empty(0), 1.0)
+    assert not np.any(sekspace.spread(empty, wspec, grid, se.Periodicity(3)).values)
+    assert se.se_kspace(empty, p, se.Periodicity(3)).shape == (0,)
+    s = se.generate_random_system(6, 1.0, seed=4)
+    s0 = se.ParticleSystem(s.positions, np.zeros(6), 1.0)
+    assert np.all(se.total_potential(s0, p, se.Periodicity(3)) == 0.0)
+
+
+def test_error_conventions():
+    p = se.SEParams(xi=5.0, rc=0.4, M=16, P=8, window="bm", shape=20.0, eps=1e-8)
+    pos = np.array([[0.5, 0.5, 0.5], [0.5, 0.5, 0.5]])
+    s = se.ParticleSystem(pos, np.array([1.0, -1.0]), 1.0)
+    with pytest.raises(se.SingularConfigurationError):
+        se.real_space_sum(s, 5.0, 0.4, se.Periodicity(0))
+    with pytest.raises(se.SingularConfigurationError):
+        se.total_potential(s, p, se.Periodicity(3))
+    charged = se.ParticleSystem(np.array([[0.1, 0.2, 0.3], [0.6, 0.5, 0.4]]), np.array([1.0, 0.5]), 1.0)
+    with pytest.raises(ValueError, match="charge-neutral"):
+        se.total_potential(charged, p, se.Periodicity(3))
+    pd0 = se.SEParams(xi=5.0, rc=0.4, M=16, P=8, window="bm", shape=20.0, s0=3.0, R=2.0, eps=1e-8)
+    with pytest.warns(UserWarning):
+        se.total_potential(charged, pd0, se.Periodicity(0))
+    with pytest.raises(ValueError):
+        se.real_space_sum(s, -1.0, 0.4, se.Periodicity(3))
+
+
+def test_two_particle_single_term_and_cutoff():
+    from scipy.special import erfc
+    r = 0.2
+    s = se.ParticleSystem(np.array([[0.3, 0.5, 0.5], [0.5, 0.5, 0.5]]), np.array([2.0, -1.0]), 1.0)
+    phi = se.real_space_sum(s, 5.0, 0.45, se.Periodicity(0))
+    assert phi[0] == pytest.approx(-1.0 * erfc(5.0 * r) / r, rel=1e-15)
+    assert phi[1] == pytest.approx(2.0 * erfc(5.0 * r) / r, rel=1e-15)
+    rc = 0.25
+    far = se.ParticleSystem(np.array([[0.1, 0.5, 0.5], [0.1 + rc + 1 / 28, 0.5, 0.5]]), np.array([1.0, -1.0]), 1.0)
+    assert np.all(se.real_space_sum(far, 5.0, rc, se.Periodicity(0)) == 0.0)
+
+
+def test_threads_argument_and_determinism():
+    s = rand_system(4000, 1.0, 8)
+    p = se.SEParams(xi=8.0, rc=0.4, M=32, P=8, window="bm", shape=20.0, eps=1e-8)
+    a = se.total_potential(s, p, se.Periodicity(3), threads=1)
+    b = se.total_potential(s, p, se.Periodicity(3), threads=8)
+    # fp64 atomics flush the spreading tiles in nondeterministic order: the
+    # only run-to-run difference is final-bit rounding
+    assert se.relative_rms_error(a, b) < 1e-14
+    ra = se.real_space_sum(s, 8.0, 0.4, se.Periodicity(3), threads=1)
+    rb = se.real_space_sum(s, 8.0, 0.4, se.Periodicity(3), threads=4)
+    assert np.array_equal(ra, rb)
+
+
+def test_xi_invariance_all_periodicities():
+    s = rand_system(60, 1.0, 11)
+    worst = 0.0
+    for D in (0, 1, 2, 3):
+        phis = []
+        for xi in (4.0, 6.3, 8.0):
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                p, _ = se.auto_params(s, se.Periodicity(D), xi, 1e-10)
+            phis.append(se.total_potential(s, p, se.Periodicity(D)))
+        for i in range(3):
+            for j in range(i + 1, 3):
+                worst = max(worst, se.relative_rms_error(phis[i], phis[j]))
+    assert worst <= 1e-9
+
+
+def test_timings_keys():
+    s = rand_system(500, 1.0, 3)
+    p = se.SEParams(xi=8.0, rc=0.4, M=24, P=8, window="bm", shape=20.0, eps=1e-8)
+    t = {}
+    se.total_potential(s, p, se.Periodicity(3), timings=t)
+    for k in ("realspace", "spread", "aft", "scale", "aift", "gather", "precompute"):
+        assert k in t and t[k] >= 0.0
+
+
+# ----------------------------------------------------------- device API
+
+def test_device_api_matches_host_api():
+    s = rand_system(5000, 2.0, 31)
+    p = se.SEParams(xi=5.0, rc=0.6, M=32, P=8, window="bm", shape=20.0, eps=1e-8)
+    host = se.total_potential(s, p, se.Periodicity(3))
+    pos = torch.from_numpy(s.positions).cuda()
+    q = torch.from_numpy(s.charges).cuda()
+    dev = sedev.total_potential(pos, q, s.L, p, se.Periodicity(3)).cpu().numpy()
+    assert se.relative_rms_error(dev, host) < 1e-14
+
+
+def test_sharded_pipeline_single_process_world_splits():
+    # the shard entry points, summed over ranks, reproduce the full potential
+    from paper_1712_04732_b200 import _native
+    s = rand_system(3000, 1.0, 41)
+    p = se.SEParams(xi=8.0, rc=0.4, M=24, P=8, window="bm", shape=20.0, eps=1e-8)
+    full = se.total_potential(s, p, se.Periodicity(3))
+    pos = torch.from_numpy(s.positions).cuda()
+    q = torch.from_numpy(s.charges).cuda()
+    from paper_1712_04732_b200.distributed import NativeBackend
+    be = NativeBackend(s.L, p, se.Periodicity(3), pos.device)
+    world = 3
+    grid = torch.zeros(be.shape, dtype=torch.float64, device=pos.device)
+    for r in range(world):
+        g = be.empty_grid()
+        be.spread_shard(pos, q, r, world, g)
+        grid += g
+    be.kspace_apply(grid)
+    phi = torch.zeros(3000, dtype=torch.float64, device=pos.device)
+    for r in range(world):
+        ph = be.empty_phi(3000)
+        be.realspace_shard(pos, q, r, world, ph)
+        be.gather_shard(grid, pos, r, world, ph)
+        phi += ph
+    assert se.relative_rms_error(phi.cpu().numpy(), full) < 1e-13
+
+
+# --------------------------------------------- full-size (cfg2) properties
+
+@pytest.fixture(scope="module")
+def cfg2_full():
+    rng = np.random.default_rng(2)
+    N, L = 1_000_000, 10.0
+    pos = rng.random((N, 3)) * L
+    q = rng.uniform(-1, 1, N)
+    q -= q.mean()
+    p = se.SEParams(xi=4.2919, rc=1.0, M=128, P=8, window="bm", shape=20.0, eps=1e-8)
+    return pos, q, L, p
+
+
+def test_cfg2_full_size_realspace_sample_vs_oracle(cfg2_full):
+    pos, q, L, p = cfg2_full
+    s = se.ParticleSystem(pos, q, L)
+    phir = se.real_space_sum(s, p.xi, p.rc, se.Periodicity(3))
+    sel = np.random.default_rng(0).choice(len(q), 200, replace=False)
+    ref = orc.realspace(pos, q, L, 3, p.xi, p.rc, targets=sel)
+    assert se.relative_rms_error(phir[sel], ref) < 1e-13
+
+
+def test_cfg2_full_size_linearity_and_translation(cfg2_full):
+    pos, q, L, p = cfg2_full
+    phi = se.total_potential(se.ParticleSystem(pos, q, L), p, se.Periodicity(3))
+    phi2 = se.total_potential(se.ParticleSystem(pos, -2.0 * q, L), p, se.Periodicity(3))
+    assert se.relative_rms_error(phi2, -2.0 * phi) < 1e-13
+    # a shift by exactly 3 grid spacings (h = L/M) is a symmetry of the grid
+    h = L / p.M
+    sh = np.mod(pos + 3 * h, L)
+    sh[sh >= L] = 0.0
+    phi3 = se.total_potential(se.ParticleSystem(sh, q, L), p, se.Periodicity(3))
+    assert se.relative_rms_error(phi3, phi) < 1e-11
