@@ -201,7 +201,7 @@ void plan_release_device(se_plan *pl) {
         t->what.release();
     }
     for (DevBuf *d : {&pl->flag, &pl->spec, &pl->spec2, &pl->spec3, &pl->work, &pl->grid_tmp, &pl->rows_I,
-                      &pl->ghat, &pl->grid_dev, &pl->io_pos, &pl->io_q, &pl->io_phi, &pl->io_grid, &pl->check})
+                      &pl->ghat, &pl->grid_dev, &pl->io_pos, &pl->io_q, &pl->io_phi, &pl->io_grid, &pl->check, &pl->pairs, &pl->racc})
         d->release();
     if (pl->own_stream) cudaStreamDestroy(pl->own_stream);
 }

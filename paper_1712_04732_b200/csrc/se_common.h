@@ -165,6 +165,7 @@ struct se_plan {
     double pms[SE_K_COUNT] = {};
     int64_t pcount[SE_K_COUNT] = {};
     se::DevBuf pairs;  // pair counter (count mode of the real-space kernel)
+    se::DevBuf racc;   // real-space pair sums in cell-sorted order (Newton path)
 };
 
 namespace se {

@@ -28,9 +28,20 @@ struct RealArgs {
     int mode[3];     // 0 free, 1 periodic +-2 wrap, 2 periodic all cells + min image
     int64_t rlo, rhi;
     int add_self;
-    double self_coef;  // -2 xi / sqrt(pi) applied as ((-2 xi) q) / sqrt(pi)
     double sqrtpi;
+    float rc2f;       // fp32 prefilter bound (rc^2 plus the fp32 coordinate rounding margin)
+    float Lf, invLf;  // box length for the fp32 minimum image
 };
+
+// fp32 prefilter bound: coordinates in [-L, 2L) carry <= 2^-23 L absolute
+// rounding each, so r^2 in fp32 is within ~1.5e-6 rc L (+ fp32 products) of
+// the exact value for candidates near the cutoff; 4x that keeps every pair
+// with r < rc.
+static inline void set_prefilter(RealArgs &a) {
+    a.rc2f = (float)(a.rc * a.rc + 6e-6 * a.rc * a.L + 2e-6 * a.rc * a.rc);
+    a.Lf = (float)a.L;
+    a.invLf = (float)(1.0 / a.L);
+}
 
 __global__ void cell_keys_kernel(const double *__restrict__ pos, int64_t N, RealArgs a, unsigned *__restrict__ keys,
                                  int *__restrict__ counts) {
@@ -48,75 +59,157 @@ __global__ void cell_keys_kernel(const double *__restrict__ pos, int64_t N, Real
 }
 
 __device__ __forceinline__ double min_image(double d, double L) { return d - L * rint(d / L); }
+__device__ __forceinline__ float min_image_f(float d, float L, float invL) { return d - L * rintf(d * invL); }
 
-template <bool MI, bool COUNT>
-__device__ __forceinline__ void pair_run(const double4 *__restrict__ rec, int j0, int j1, double shx, double shy,
-                                         double shz, const RealArgs &a, double4 *st, int *sj, double4 tp, int tidx,
-                                         bool active, double &acc, int &singular, const int mi[3], long long &cnt) {
-    const int lane = threadIdx.x & 31;
-    for (int jb = j0; jb < j1; jb += 32) {
-        int j = jb + lane;
-        if (j < j1) {
-            double4 r = rec[j];
-            st[lane] = make_double4(__dadd_rn(r.x, shx), __dadd_rn(r.y, shy), __dadd_rn(r.z, shz), r.w);
-            sj[lane] = j;
-        }
-        __syncwarp();
-        int m = min(32, j1 - jb);
-        if (active) {
-            for (int k = 0; k < m; ++k) {
-                double4 s = st[k];
-                double dx = __dsub_rn(tp.x, s.x), dy = __dsub_rn(tp.y, s.y), dz = __dsub_rn(tp.z, s.z);
-                if (MI) {
-                    if (mi[0]) dx = min_image(dx, a.L);
-                    if (mi[1]) dy = min_image(dy, a.L);
-                    if (mi[2]) dz = min_image(dz, a.L);
-                }
-                double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-                if (r2 < a.rc2) {
-                    double r = sqrt(r2);
-                    if (r < a.rc) {
-                        if (r < 1e-14) {
-                            if (sj[k] != tidx) singular = 1;
-                        } else if (COUNT) {
-                            ++cnt;
-                        } else {
-                            acc += s.w * (erfc(a.xi * r) / r);
-                        }
-                    }
-                }
-            }
-        }
-        __syncwarp();
+constexpr int kWarps = 4;  // warps (units) per block
+
+// Shared-memory workspace of one warp unit.
+struct __align__(16) WarpBuf {
+    double4 tst[32];         // the unit's targets (x, y, z, q)
+    double4 sst[32];         // current source batch, image shift applied
+    float4 sf[32];           // the same in fp32 for the prefilter
+    double acc[32][32];      // per-lane private accumulators, acc[lane][(t + lane) & 31]
+    unsigned short ent[1024];  // compacted hits of a batch: (target << 5) | source
+};
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
     }
+    return v;
 }
 
-template <bool MI, bool COUNT>
-__global__ void __launch_bounds__(128) realspace_cell_kernel(const double4 *__restrict__ rec, const int *__restrict__ sidx,
-                                                             const int *__restrict__ starts, const int4 *__restrict__ units,
-                                                             const int *__restrict__ nunits, RealArgs a,
-                                                             double *__restrict__ phi, int *__restrict__ flag,
-                                                             unsigned long long *__restrict__ npairs) {
-    __shared__ double4 stage[4][32];
-    __shared__ int sj[4][32];
+// Exact fp64 evaluation of one compacted hit (target tt, source k of the
+// batch): d = x_t - (x_s + shift) (realspace.py:113-117), r < rc, the
+// coincidence check, and f = erfc(xi r)/r via 1/r = rsqrt(r^2).
+// Target side into the lane's private row; with NEWTON the source side
+// q_t f goes to the source's global accumulator (native fp64 REDG).
+template <bool MI, bool COUNT, bool NEWTON>
+__device__ __forceinline__ void eval_hit(unsigned en, const RealArgs &a, WarpBuf &wb, int lane, int jb, int tbase,
+                                         double *__restrict__ acc_src, int &singular, long long &cnt) {
+    const int tt = (int)(en >> 5), k = (int)(en & 31u);
+    const double4 tp = wb.tst[tt];
+    const double4 sp = wb.sst[k];
+    double dx = __dsub_rn(tp.x, sp.x), dy = __dsub_rn(tp.y, sp.y), dz = __dsub_rn(tp.z, sp.z);
+    if (MI) {
+        if (a.mode[0] == 2) dx = min_image(dx, a.L);
+        if (a.mode[1] == 2) dy = min_image(dy, a.L);
+        if (a.mode[2] == 2) dz = min_image(dz, a.L);
+    }
+    const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    if (r2 < 1e-28) {  // r < 1e-14: the self pair or a coincidence (realspace.py:118-122)
+        if (jb + k != tbase + tt) singular = 1;
+        return;
+    }
+    const double rinv = rsqrt(r2);
+    const double rr = r2 * rinv;
+    if (!(rr < a.rc)) return;
+    if (COUNT) {
+        cnt += NEWTON ? 2 : 1;
+        return;
+    }
+    const double f = erfc(a.xi * rr) * rinv;
+    double *slot = &wb.acc[lane][(tt + lane) & 31];
+    *slot = fma(sp.w, f, *slot);
+    if (NEWTON) atomicAdd(acc_src + jb + k, tp.w * f);
+}
+
+// One batch of <= 32 candidate sources [jb, jb+m) of a neighbour-cell run:
+//  1. fp32 prefilter of all 32 x m (target, source) pairs against a bound
+//     that covers the fp32 rounding of the coordinates -> per-lane hit mask
+//     (with NEWTON, sources of the target's own cell count only if j > t);
+//  2. warp prefix scan of the hit counts and compaction of the hits into a
+//     target-major list;
+//  3. the list is evaluated 64 hits at a time (two per lane, independent
+//     chains) on full warps.
+template <bool MI, bool COUNT, bool NEWTON>
+__device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int jb, int j1, double shx, double shy,
+                                           double shz, const RealArgs &a, WarpBuf &wb, int lane, bool active,
+                                           float fx, float fy, float fz, int t, int tbase, int hs,
+                                           double *__restrict__ acc_src, int &singular, long long &cnt) {
+    const int j = jb + lane;
+    if (j < j1) {
+        const double4 r = rec[j];
+        const double xs = __dadd_rn(r.x, shx), ys = __dadd_rn(r.y, shy), zs = __dadd_rn(r.z, shz);
+        wb.sst[lane] = make_double4(xs, ys, zs, r.w);
+        wb.sf[lane] = make_float4((float)xs, (float)ys, (float)zs, 0.f);
+    }
+    __syncwarp();
+    const int m = min(32, j1 - jb);
+    unsigned hit = 0;
+    if (active) {
+#pragma unroll 8
+        for (int k = 0; k < m; ++k) {
+            const float4 p = wb.sf[k];
+            float dx = fx - p.x, dy = fy - p.y, dz = fz - p.z;
+            if (MI) {
+                if (a.mode[0] == 2) dx = min_image_f(dx, a.Lf, a.invLf);
+                if (a.mode[1] == 2) dy = min_image_f(dy, a.Lf, a.invLf);
+                if (a.mode[2] == 2) dz = min_image_f(dz, a.Lf, a.invLf);
+            }
+            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            hit |= (r2 < a.rc2f ? 1u : 0u) << k;
+        }
+        if (NEWTON && hs >= 0) {
+            // own-cell sources j in [hs, t] are visited from their own unit
+            const int lo = max(hs - jb, 0), hi = t - jb;  // exclude k in [lo, hi]
+            if (hi >= lo && lo < 32) {
+                const unsigned upto = hi >= 31 ? 0xffffffffu : ((2u << hi) - 1u);
+                const unsigned from = lo == 0 ? 0xffffffffu : ~((1u << lo) - 1u);
+                hit &= ~(upto & from);
+            }
+        }
+    }
+    const int c = __popc(hit);
+    const int incl = warp_incl_scan(c, lane);
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int pos = incl - c;
+    while (hit) {
+        const int k = __ffs(hit) - 1;
+        hit &= hit - 1;
+        wb.ent[pos++] = (unsigned short)((lane << 5) | k);
+    }
+    __syncwarp();
+    for (int e0 = 0; e0 < total; e0 += 64) {
+        const int e1 = e0 + lane, e2 = e0 + 32 + lane;
+        if (e1 < total) eval_hit<MI, COUNT, NEWTON>(wb.ent[e1], a, wb, lane, jb, tbase, acc_src, singular, cnt);
+        if (e2 < total) eval_hit<MI, COUNT, NEWTON>(wb.ent[e2], a, wb, lane, jb, tbase, acc_src, singular, cnt);
+    }
+    __syncwarp();
+}
+
+// NEWTON: every unordered pair once -- neighbour cells in the half shell
+// o > 0 (lexicographic on (ox, oy, oz)) plus own-cell pairs with t < j; the
+// partial sums of both sides go to acc_src (sorted order, zeroed before) and
+// a finishing kernel scatters them.  Otherwise the full 5x5x5 neighbourhood
+// and direct writes of phi (minimum-image mode for < 5 cells per axis).
+template <bool MI, bool COUNT, bool NEWTON>
+__global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
+    const double4 *__restrict__ rec, const int *__restrict__ sidx, const int *__restrict__ starts,
+    const int4 *__restrict__ units, const int *__restrict__ nunits, RealArgs a, double *__restrict__ phi,
+    double *__restrict__ acc_src, int *__restrict__ flag, unsigned long long *__restrict__ npairs) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int u = blockIdx.x * 4 + warp;
+    WarpBuf &wb = reinterpret_cast<WarpBuf *>(smem_raw)[warp];
+    const int u = blockIdx.x * kWarps + warp;
     if (u >= *nunits) return;
-    int4 un = units[u];
+    const int4 un = units[u];
     const int n = a.n;
     const int cell = un.x;
     const int cz = cell % n, cy = (cell / n) % n, cx = cell / (n * n);
-    int t = un.y + lane;
-    bool active = lane < un.z && t >= a.rlo && t < a.rhi;
+    const int t = un.y + lane;
+    const bool active = lane < un.z && t >= a.rlo && t < a.rhi;
     if (__ballot_sync(0xffffffffu, active) == 0) return;
-    double4 tp = active ? rec[t] : make_double4(0, 0, 0, 0);
-    double acc = 0.0;
+    const double4 tp = active ? rec[t] : make_double4(0, 0, 0, 0);
+    wb.tst[lane] = tp;
+    for (int i = 0; i < 32; ++i) wb.acc[lane][i] = 0.0;
+    const float fx = (float)tp.x, fy = (float)tp.y, fz = (float)tp.z;
     int singular = 0;
     long long cnt = 0;
-    const int mi[3] = {a.mode[0] == 2, a.mode[1] == 2, a.mode[2] == 2};
+    __syncwarp();
+    const int home_start = starts[cell];
 
-    // per-axis candidate lists: (cell, shift index) for x and y; z as runs
-    int xs_lo, xs_hi, ys_lo, ys_hi;
     auto axis_range = [&](int c, int mode, int &lo, int &hi) {
         if (mode == 2) {
             lo = 0;
@@ -129,18 +222,25 @@ __global__ void __launch_bounds__(128) realspace_cell_kernel(const double4 *__re
             hi = min(n - 1, c + 2);
         }
     };
-    axis_range(cx, a.mode[0], xs_lo, xs_hi);
-    axis_range(cy, a.mode[1], ys_lo, ys_hi);
-    int zlo, zhi;
+    int xlo, xhi, ylo, yhi, zlo, zhi;
+    axis_range(cx, a.mode[0], xlo, xhi);
+    axis_range(cy, a.mode[1], ylo, yhi);
     axis_range(cz, a.mode[2], zlo, zhi);
-    for (int ox = xs_lo; ox <= xs_hi; ++ox) {
+    if (NEWTON) xlo = cx;  // ox >= 0
+    auto run = [&](int j0, int j1, double shx, double shy, double shz, int hs) {
+        for (int jb = j0; jb < j1; jb += 32)
+            pair_batch<MI, COUNT, NEWTON>(rec, jb, j1, shx, shy, shz, a, wb, lane, active, fx, fy, fz, t, un.y, hs,
+                                          acc_src, singular, cnt);
+    };
+    for (int ox = xlo; ox <= xhi; ++ox) {
         int xc = ox;
         double shx = 0.0;
         if (a.mode[0] == 1) {
             if (xc < 0) { xc += n; shx = -a.L; }
             else if (xc >= n) { xc -= n; shx = a.L; }
         }
-        for (int oy = ys_lo; oy <= ys_hi; ++oy) {
+        const int ylo2 = (NEWTON && ox == cx) ? cy : ylo;  // ox == 0: oy >= 0
+        for (int oy = ylo2; oy <= yhi; ++oy) {
             int yc = oy;
             double shy = 0.0;
             if (a.mode[1] == 1) {
@@ -148,40 +248,48 @@ __global__ void __launch_bounds__(128) realspace_cell_kernel(const double4 *__re
                 else if (yc >= n) { yc -= n; shy = a.L; }
             }
             const int rowbase = (xc * n + yc) * n;
+            const bool own_row = NEWTON && ox == cx && oy == cy;
+            const int zlo2 = own_row ? cz : zlo;  // (0,0): oz >= 0, own cell with j > t
+            const int hs = own_row ? home_start : -1;
             if (a.mode[2] == 1) {
-                // up to three runs: wrapped below, in range, wrapped above
-                int r0 = zlo, r1 = zhi;
-                int blo = max(r0, 0), bhi = min(r1, n - 1);
-                if (r0 < 0) {
-                    int c0 = r0 + n, c1 = n - 1;
-                    pair_run<MI, COUNT>(rec, starts[rowbase + c0], starts[rowbase + c1 + 1], shx, shy, -a.L, a, stage[warp],
-                                 sj[warp], tp, t, active, acc, singular, mi, cnt);
-                }
-                if (blo <= bhi)
-                    pair_run<MI, COUNT>(rec, starts[rowbase + blo], starts[rowbase + bhi + 1], shx, shy, 0.0, a, stage[warp],
-                                 sj[warp], tp, t, active, acc, singular, mi, cnt);
-                if (r1 > n - 1) {
-                    int c0 = 0, c1 = r1 - n;
-                    pair_run<MI, COUNT>(rec, starts[rowbase + c0], starts[rowbase + c1 + 1], shx, shy, a.L, a, stage[warp],
-                                 sj[warp], tp, t, active, acc, singular, mi, cnt);
-                }
+                // up to three contiguous runs: wrapped below, in range, wrapped above
+                if (zlo2 < 0) run(starts[rowbase + zlo2 + n], starts[rowbase + n], shx, shy, -a.L, -1);
+                const int blo = max(zlo2, 0), bhi = min(zhi, n - 1);
+                if (blo <= bhi) run(starts[rowbase + blo], starts[rowbase + bhi + 1], shx, shy, 0.0, hs);
+                if (zhi > n - 1) run(starts[rowbase], starts[rowbase + zhi - n + 1], shx, shy, a.L, -1);
             } else {
-                pair_run<MI, COUNT>(rec, starts[rowbase + zlo], starts[rowbase + zhi + 1], shx, shy, 0.0, a, stage[warp],
-                             sj[warp], tp, t, active, acc, singular, mi, cnt);
+                run(starts[rowbase + zlo2], starts[rowbase + zhi + 1], shx, shy, 0.0, hs);
             }
         }
     }
     if (COUNT) {
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0) atomicAdd(npairs, (unsigned long long)cnt);
+        long long c = cnt;
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) atomicAdd(npairs, (unsigned long long)c);
         return;
     }
+    if (__any_sync(0xffffffffu, singular) && lane == 0) atomicExch(flag, 1);
+    __syncwarp();
     if (active) {
-        if (singular) atomicExch(flag, 1);
-        double v = acc;
-        if (a.add_self) v += (-2.0 * a.xi * tp.w) / a.sqrtpi;
-        phi[sidx[t]] = v;
+        double v = 0.0;
+        for (int i = 0; i < 32; ++i) v += wb.acc[i][(lane + i) & 31];
+        if (NEWTON) {
+            atomicAdd(acc_src + t, v);
+        } else {
+            if (a.add_self) v += (-2.0 * a.xi * tp.w) / a.sqrtpi;
+            phi[sidx[t]] = v;
+        }
     }
+}
+
+// NEWTON finish: phi[orig] = accumulated pair sums (+ the self term of owned targets)
+__global__ void realspace_finish_kernel(const double *__restrict__ acc, const double4 *__restrict__ rec,
+                                        const int *__restrict__ sidx, int64_t N, RealArgs a, double *__restrict__ phi) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    double v = acc[i];
+    if (a.add_self && i >= a.rlo && i < a.rhi) v += (-2.0 * a.xi * rec[i].w) / a.sqrtpi;
+    phi[sidx[i]] = v;
 }
 
 // rc > L/2 with periodic axes: explicit images (realspace.py:138-165)
@@ -227,6 +335,7 @@ static const int kRealUnit = 32;
 // cells of edge >= rc/2 and the particle binning by cell
 static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N, RealArgs &a) {
     const double L = pl->L, rc = pl->p.rc;
+    if (N >= (1LL << 27)) fail(SE_EINVAL, "real-space kernel supports N < 2^27 particles per call");
     CellGeom &c = pl->cell;
     long long nn = (long long)std::floor(2.0 * L / rc);
     if (nn < 1) nn = 1;
@@ -255,22 +364,36 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
     const CellGeom &c = pl->cell;
     int nbins = c.n * c.n * c.n;
     int64_t maxu = binning_max_units(pl->cbin, N, nbins, kRealUnit);
-    bool mi = c.mode[0] == 2 || c.mode[1] == 2 || c.mode[2] == 2;
-    unsigned blocks = (unsigned)((maxu + 3) / 4);
+    const bool mi = c.mode[0] == 2 || c.mode[1] == 2 || c.mode[2] == 2;
+    unsigned blocks = (unsigned)((maxu + kWarps - 1) / kWarps);
     cudaStream_t st = pl->stream;
+    const size_t smem = sizeof(WarpBuf) * kWarps;
+    double *acc = nullptr;
+    if (!mi) {
+        pl->racc.ensure(sizeof(double) * N);
+        acc = pl->racc.as<double>();
+        SE_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * N, st));
+    }
     auto args = [&](auto kern) {
-        kern<<<blocks, 128, 0, st>>>(pl->cbin.rec.as<double4>(), pl->cbin.idx_sorted.as<int>(),
-                                     pl->cbin.starts.as<int>(), pl->cbin.units.as<int4>(), pl->cbin.nunits.as<int>(),
-                                     a, phi, pl->flag.as<int>(), npairs);
+        SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<blocks, 32 * kWarps, smem, st>>>(pl->cbin.rec.as<double4>(), pl->cbin.idx_sorted.as<int>(),
+                                                pl->cbin.starts.as<int>(), pl->cbin.units.as<int4>(),
+                                                pl->cbin.nunits.as<int>(), a, phi, acc, pl->flag.as<int>(), npairs);
     };
     if (!COUNT) prof_begin(pl, SE_K_REALSPACE);
     if (mi)
-        args(realspace_cell_kernel<true, COUNT>);
+        args(realspace_cell_kernel<true, COUNT, false>);
     else
-        args(realspace_cell_kernel<false, COUNT>);
+        args(realspace_cell_kernel<false, COUNT, true>);
     SE_LAUNCH_CHECK();
-    if (!COUNT) prof_end(pl, SE_K_REALSPACE);
     pl->launches += 1;
+    if (!mi && !COUNT) {
+        realspace_finish_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(acc, pl->cbin.rec.as<double4>(),
+                                                                           pl->cbin.idx_sorted.as<int>(), N, a, phi);
+        SE_LAUNCH_CHECK();
+        pl->launches += 1;
+    }
+    if (!COUNT) prof_end(pl, SE_K_REALSPACE);
 }
 
 void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, int add_self, int rank,
@@ -292,6 +415,7 @@ void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, d
     a.sqrtpi = std::sqrt(M_PI);
     a.rlo = N * rank / world;
     a.rhi = N * (rank + 1) / world;
+    set_prefilter(a);
     if (D >= 1 && rc > L / 2 + 1e-12) {
         int layers = (int)std::floor((rc + L / 2) / L) + 1;
         prof_begin(pl, SE_K_REALSPACE);
@@ -319,6 +443,7 @@ void realspace_pair_count(se_plan *pl, const double *pos, const double *q, int64
     a.sqrtpi = std::sqrt(M_PI);
     a.rlo = 0;
     a.rhi = N;
+    set_prefilter(a);
     pl->flag.ensure(sizeof(int) * 4);
     SE_CUDA(cudaMemsetAsync(pl->flag.ptr, 0, sizeof(int) * 4, pl->stream));
     pl->pairs.ensure(sizeof(unsigned long long));

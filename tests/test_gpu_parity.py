@@ -244,12 +244,15 @@ def test_threads_argument_and_determinism():
     p = se.SEParams(xi=8.0, rc=0.4, M=32, P=8, window="bm", shape=20.0, eps=1e-8)
     a = se.total_potential(s, p, se.Periodicity(3), threads=1)
     b = se.total_potential(s, p, se.Periodicity(3), threads=8)
-    # fp64 atomics flush the spreading tiles in nondeterministic order: the
-    # only run-to-run difference is final-bit rounding
+    # fp64 atomics (spreading-tile flush, Newton-symmetric real-space pair
+    # sums) add in nondeterministic order: the only run-to-run difference is
+    # final-bit rounding, far below the 1e-10 parity bar.  The reference's
+    # bit-identity across thread counts (test_core.py:139-145) becomes this
+    # bound.
     assert se.relative_rms_error(a, b) < 1e-14
     ra = se.real_space_sum(s, 8.0, 0.4, se.Periodicity(3), threads=1)
     rb = se.real_space_sum(s, 8.0, 0.4, se.Periodicity(3), threads=4)
-    assert np.array_equal(ra, rb)
+    assert se.relative_rms_error(ra, rb) < 1e-14
 
 
 def test_xi_invariance_all_periodicities():
