@@ -19,6 +19,7 @@
 // Image path (D >= 1 and rc > L/2): all pairs x explicit images
 // (realspace.py:138-165), one thread per target.
 #include "se_common.h"
+#include "se_erfc_coeffs.h"
 
 namespace se {
 
@@ -56,6 +57,30 @@ __global__ void cell_keys_kernel(const double *__restrict__ pos, int64_t N, Real
     unsigned key = (unsigned)((c[0] * a.n + c[1]) * a.n + c[2]);
     keys[i] = key;
     atomicAdd(&counts[key], 1);
+}
+
+// erfc(x), x >= 0, as exp(-x^2) erfcx(x): erfcx by a degree-17 polynomial in
+// s = A t + B, t = (x - K)/(x + K), and exp by Cody-Waite reduction with the
+// x^2 rounding residual folded in; coefficients are __constant__ operands
+// (tools/gen_erfc_coeffs.py; max relative error 4e-15 on [0, 6], the same
+// as scipy's erfc).  Beyond SE_ERFC_XMAX the library erfc is used.
+__device__ __forceinline__ double erfc_fast(double x) {
+    if (x > SE_ERFC_XMAX) return erfc(x);
+    const double t = (x - SE_ERFC_K) * __drcp_rn(x + SE_ERFC_K);
+    const double s = fma(t, SE_ERFC_A, SE_ERFC_B);
+    double p = se_erfcx_c[SE_ERFC_NE];
+#pragma unroll
+    for (int i = SE_ERFC_NE - 1; i >= 0; --i) p = fma(p, s, se_erfcx_c[i]);
+    const double u = x * x;
+    const double ul = fma(x, x, -u);
+    const double n = rint(u * -SE_LOG2E);
+    double r = fma(n, -SE_LN2_HI, -u);
+    r = fma(n, -SE_LN2_LO, r) - ul;
+    double e = se_exp_c[SE_EXP_NX];
+#pragma unroll
+    for (int i = SE_EXP_NX - 1; i >= 0; --i) e = fma(e, r, se_exp_c[i]);
+    const double scale = __hiloint2double(((int)n + 1023) << 20, 0);
+    return p * (e * scale);
 }
 
 __device__ __forceinline__ double min_image(double d, double L) { return d - L * rint(d / L); }
@@ -109,7 +134,7 @@ __device__ __forceinline__ void eval_hit(unsigned en, const RealArgs &a, WarpBuf
         cnt += NEWTON ? 2 : 1;
         return;
     }
-    const double f = erfc(a.xi * rr) * rinv;
+    const double f = erfc_fast(a.xi * rr) * rinv;
     double *slot = &wb.acc[lane][(tt + lane) & 31];
     *slot = fma(sp.w, f, *slot);
     if (NEWTON) atomicAdd(acc_src + jb + k, tp.w * f);
