@@ -87,14 +87,15 @@ __device__ __forceinline__ double min_image(double d, double L) { return d - L *
 __device__ __forceinline__ float min_image_f(float d, float L, float invL) { return d - L * rintf(d * invL); }
 
 constexpr int kWarps = 4;  // warps (units) per block
+constexpr int kT = 16;     // targets per warp unit: lane l tests target l % 16 against half of a 32-source batch
 
-// Shared-memory workspace of one warp unit.
+// Shared-memory workspace of one warp unit (7 KB: 8 blocks x 4 warps per SM).
 struct __align__(16) WarpBuf {
-    double4 tst[32];         // the unit's targets (x, y, z, q)
-    double4 sst[32];         // current source batch, image shift applied
-    float4 sf[32];           // the same in fp32 for the prefilter
-    double acc[32][32];      // per-lane private accumulators, acc[lane][(t + lane) & 31]
-    unsigned short ent[1024];  // compacted hits of a batch: (target << 5) | source
+    double4 tst[kT];             // the unit's targets (x, y, z, q)
+    double4 sst[32];             // current source batch, image shift applied
+    float4 sf[32];               // the same in fp32 for the prefilter
+    double acc[32][kT];          // per-lane private accumulators, acc[lane][(t + lane) % kT]
+    unsigned short ent[kT * 32];  // compacted hits of a batch: (target << 5) | source
 };
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -135,7 +136,7 @@ __device__ __forceinline__ void eval_hit(unsigned en, const RealArgs &a, WarpBuf
         return;
     }
     const double f = erfc_fast(a.xi * rr) * rinv;
-    double *slot = &wb.acc[lane][(tt + lane) & 31];
+    double *slot = &wb.acc[lane][(tt + lane) & (kT - 1)];
     *slot = fma(sp.w, f, *slot);
     if (NEWTON) atomicAdd(acc_src + jb + k, tp.w * f);
 }
@@ -163,9 +164,12 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     __syncwarp();
     const int m = min(32, j1 - jb);
     unsigned hit = 0;
+    const int k0 = (lane / kT) * kT;  // this lane's half of the batch
     if (active) {
 #pragma unroll 8
-        for (int k = 0; k < m; ++k) {
+        for (int kk = 0; kk < kT; ++kk) {
+            const int k = k0 + kk;
+            if (k >= m) break;
             const float4 p = wb.sf[k];
             float dx = fx - p.x, dy = fy - p.y, dz = fz - p.z;
             if (MI) {
@@ -193,7 +197,7 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     while (hit) {
         const int k = __ffs(hit) - 1;
         hit &= hit - 1;
-        wb.ent[pos++] = (unsigned short)((lane << 5) | k);
+        wb.ent[pos++] = (unsigned short)(((lane & (kT - 1)) << 5) | k);
     }
     __syncwarp();
     for (int e0 = 0; e0 < total; e0 += 64) {
@@ -223,12 +227,13 @@ __global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
     const int n = a.n;
     const int cell = un.x;
     const int cz = cell % n, cy = (cell / n) % n, cx = cell / (n * n);
-    const int t = un.y + lane;
-    const bool active = lane < un.z && t >= a.rlo && t < a.rhi;
+    const int tl = lane & (kT - 1);
+    const int t = un.y + tl;
+    const bool active = tl < un.z && t >= a.rlo && t < a.rhi;
     if (__ballot_sync(0xffffffffu, active) == 0) return;
     const double4 tp = active ? rec[t] : make_double4(0, 0, 0, 0);
-    wb.tst[lane] = tp;
-    for (int i = 0; i < 32; ++i) wb.acc[lane][i] = 0.0;
+    if (lane < kT) wb.tst[lane] = tp;
+    for (int i = 0; i < kT; ++i) wb.acc[lane][i] = 0.0;
     const float fx = (float)tp.x, fy = (float)tp.y, fz = (float)tp.z;
     int singular = 0;
     long long cnt = 0;
@@ -295,9 +300,9 @@ __global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
     }
     if (__any_sync(0xffffffffu, singular) && lane == 0) atomicExch(flag, 1);
     __syncwarp();
-    if (active) {
+    if (active && lane < kT) {
         double v = 0.0;
-        for (int i = 0; i < 32; ++i) v += wb.acc[i][(lane + i) & 31];
+        for (int i = 0; i < 32; ++i) v += wb.acc[i][(tl + i) & (kT - 1)];
         if (NEWTON) {
             atomicAdd(acc_src + t, v);
         } else {
@@ -355,7 +360,7 @@ __global__ void realspace_image_kernel(const double *__restrict__ pos, const dou
     phi[t] = v;
 }
 
-static const int kRealUnit = 32;
+static const int kRealUnit = kT;
 
 // cells of edge >= rc/2 and the particle binning by cell
 static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N, RealArgs &a) {
