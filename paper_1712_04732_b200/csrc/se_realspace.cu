@@ -64,9 +64,30 @@ __global__ void cell_keys_kernel(const double *__restrict__ pos, int64_t N, Real
 // x^2 rounding residual folded in; coefficients are __constant__ operands
 // (tools/gen_erfc_coeffs.py; max relative error 4e-15 on [0, 6], the same
 // as scipy's erfc).  Beyond SE_ERFC_XMAX the library erfc is used.
+// 1/d and 1/sqrt(d) from the MUFU approximations plus two Newton steps,
+// branch-free (d is a positive normal number here; error ~1 ulp).
+__device__ __forceinline__ double rcp_nr(double d) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double e = fma(-d, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-d, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double d) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double hy = 0.5 * y;
+    double e = fma(-d * y, y, 1.0);
+    y = fma(hy, e, y);
+    hy = 0.5 * y;
+    e = fma(-d * y, y, 1.0);
+    return fma(hy, e, y);
+}
+
 __device__ __forceinline__ double erfc_fast(double x) {
     if (x > SE_ERFC_XMAX) return erfc(x);
-    const double t = (x - SE_ERFC_K) * __drcp_rn(x + SE_ERFC_K);
+    const double t = (x - SE_ERFC_K) * rcp_nr(x + SE_ERFC_K);
     const double s = fma(t, SE_ERFC_A, SE_ERFC_B);
     double p = se_erfcx_c[SE_ERFC_NE];
 #pragma unroll
@@ -128,7 +149,7 @@ __device__ __forceinline__ void eval_hit(unsigned en, const RealArgs &a, WarpBuf
         if (jb + k != tbase + tt) singular = 1;
         return;
     }
-    const double rinv = rsqrt(r2);
+    const double rinv = rsqrt_nr(r2);
     const double rr = r2 * rinv;
     if (!(rr < a.rc)) return;
     if (COUNT) {
@@ -166,11 +187,8 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     unsigned hit = 0;
     const int k0 = (lane / kT) * kT;  // this lane's half of the batch
     if (active) {
-#pragma unroll 8
-        for (int kk = 0; kk < kT; ++kk) {
-            const int k = k0 + kk;
-            if (k >= m) break;
-            const float4 p = wb.sf[k];
+        auto test = [&](int kk) -> unsigned {
+            const float4 p = wb.sf[k0 + kk];
             float dx = fx - p.x, dy = fy - p.y, dz = fz - p.z;
             if (MI) {
                 if (a.mode[0] == 2) dx = min_image_f(dx, a.Lf, a.invLf);
@@ -178,8 +196,18 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
                 if (a.mode[2] == 2) dz = min_image_f(dz, a.Lf, a.invLf);
             }
             const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            hit |= (r2 < a.rc2f ? 1u : 0u) << k;
+            return r2 < a.rc2f ? 1u : 0u;
+        };
+        if (m == 32) {  // full batch: compile-time bit positions, no bounds test
+#pragma unroll
+            for (int kk = 0; kk < kT; ++kk)
+                if (test(kk)) hit |= 1u << kk;
+        } else {
+            const int mm = m - k0;
+            for (int kk = 0; kk < mm && kk < kT; ++kk)
+                if (test(kk)) hit |= 1u << kk;
         }
+        hit <<= k0;
         if (NEWTON && hs >= 0) {
             // own-cell sources j in [hs, t] are visited from their own unit
             const int lo = max(hs - jb, 0), hi = t - jb;  // exclude k in [lo, hi]
