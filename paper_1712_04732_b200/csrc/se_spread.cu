@@ -91,11 +91,12 @@ __global__ void tile_keys_kernel(const double *__restrict__ pos, int64_t N, Spre
 
 // Stage the 3P window factors of a batch of particles.  wts layout:
 // [p][axis][t]; loc: [p][4] = local start (x,y,z) within the padded tile and
-// the sorted index.  FOLDQ multiplies the x factors by the charge.
-template <int WIN, bool FOLDQ>
+// the sorted index.  FOLDQ multiplies the x factors by the charge.  PC > 0
+// is the window support P as a compile-time constant (0: runtime a.P).
+template <int WIN, bool FOLDQ, int PC>
 __device__ __forceinline__ void stage_batch(const double4 *__restrict__ rec, int s0, int nb, const int org[3],
                                             const SpreadArgs &a, double *wts, int *loc) {
-    const int P = a.P;
+    const int P = PC > 0 ? PC : a.P;
     for (int task = threadIdx.x; task < nb * 3; task += blockDim.x) {
         int p = task / 3, ax = task - 3 * p;
         double4 r = rec[s0 + p];
@@ -103,7 +104,9 @@ __device__ __forceinline__ void stage_batch(const double4 *__restrict__ rec, int
         double u = __dadd_rn(x, a.off[ax]);
         long long f = stencil_first(u, a);
         double *wo = wts + (p * 3 + ax) * P;
-        for (int t = 0; t < P; ++t) {
+#pragma unroll
+        for (int t = 0; t < (PC > 0 ? PC : 64); ++t) {
+            if (PC == 0 && t >= P) break;
             double d = __dsub_rn(__dmul_rn((double)(f + t), a.h), u);  // sekspace.py:116
             double v = window_eval<WIN>(d, a);
             if (FOLDQ && ax == 0) v = __dmul_rn(r.w, v);
@@ -137,7 +140,25 @@ __device__ __forceinline__ long long tile_to_global(int lx, int ly, int lz, cons
     return ((long long)gidx[0] * a.shape[1] + gidx[1]) * a.shape[2] + gidx[2];
 }
 
-template <int WIN>
+// Per-lane share of the P x P (y, z) footprint: lane handles pairs
+// pi = lane + 32 it; with compile-time P the pair coordinates are computed
+// once per CTA instead of per particle.
+template <int PC>
+struct LanePairs {
+    static constexpr int NPI = PC > 0 ? (PC * PC + 31) / 32 : 1;
+    int ty[NPI], tz[NPI];
+    __device__ __forceinline__ void init(int lane) {
+#pragma unroll
+        for (int it = 0; it < NPI; ++it) {
+            const int pi = lane + 32 * it;
+            ty[it] = pi / (PC > 0 ? PC : 1);
+            tz[it] = pi - ty[it] * (PC > 0 ? PC : 1);
+        }
+    }
+    __device__ __forceinline__ bool valid(int lane, int it) const { return lane + 32 * it < PC * PC; }
+};
+
+template <int WIN, int PC>
 __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restrict__ rec, const int4 *__restrict__ units,
                                                           const int *__restrict__ nunits, SpreadArgs a,
                                                           double *__restrict__ grid) {
@@ -146,7 +167,7 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
     int ubeg = (int)max((int64_t)un.y, a.rlo), uend = (int)min((int64_t)un.y + un.z, a.rhi);
     if (ubeg >= uend) return;
     extern __shared__ double smem[];
-    const int P = a.P, Tp = a.Tp, pitch = a.pitch, plane = Tp * pitch;
+    const int P = PC > 0 ? PC : a.P, Tp = a.Tp, pitch = a.pitch, plane = Tp * pitch;
     const int ncell = Tp * plane;
     double *tile = smem;
     double *wts = tile + ncell;
@@ -157,23 +178,40 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = a.nwarps;
     const int npair = P * P;
+    LanePairs<PC> lp;
+    lp.init(lane);
     for (int b0 = ubeg; b0 < uend; b0 += a.batch) {
         int nb = min(a.batch, uend - b0);
         __syncthreads();  // tile zeroed / previous batch consumed
-        stage_batch<WIN, true>(rec, b0, nb, org, a, wts, loc);
+        stage_batch<WIN, true, PC>(rec, b0, nb, org, a, wts, loc);
         __syncthreads();
         for (int p = 0; p < nb; ++p) {
             const int lx0 = loc[p * 4], ly0 = loc[p * 4 + 1], lz0 = loc[p * 4 + 2];
             const double *wx = wts + p * 3 * P, *wy = wx + P, *wz = wy + P;
-            int t0 = (warp - lx0) % nw;
-            t0 = t0 < 0 ? t0 + nw : t0;
-            for (int pi = lane; pi < npair; pi += 32) {
-                int ty = pi / P, tz = pi - ty * P;
-                double cyz = __dmul_rn(wy[ty], wz[tz]);
-                int off = (ly0 + ty) * pitch + lz0 + tz;
-                for (int t = t0; t < P; t += nw) {
-                    double *c = tile + (lx0 + t) * plane + off;
-                    *c = fma(wx[t], cyz, *c);
+            if (PC > 0) {
+                // nwarps == P: this warp owns exactly one x-plane of the particle
+                int t0 = (warp - lx0) % PC;
+                t0 = t0 < 0 ? t0 + PC : t0;
+                const double wxt = wx[t0];
+                double *base = tile + (lx0 + t0) * plane + ly0 * pitch + lz0;
+#pragma unroll
+                for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
+                    if (lp.valid(lane, it)) {
+                        double *c = base + lp.ty[it] * pitch + lp.tz[it];
+                        *c = fma(wxt, __dmul_rn(wy[lp.ty[it]], wz[lp.tz[it]]), *c);
+                    }
+                }
+            } else {
+                int t0 = (warp - lx0) % nw;
+                t0 = t0 < 0 ? t0 + nw : t0;
+                for (int pi = lane; pi < npair; pi += 32) {
+                    int ty = pi / P, tz = pi - ty * P;
+                    double cyz = __dmul_rn(wy[ty], wz[tz]);
+                    int off = (ly0 + ty) * pitch + lz0 + tz;
+                    for (int t = t0; t < P; t += nw) {
+                        double *c = tile + (lx0 + t) * plane + off;
+                        *c = fma(wx[t], cyz, *c);
+                    }
                 }
             }
             __syncwarp();
@@ -190,7 +228,7 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
     }
 }
 
-template <int WIN>
+template <int WIN, int PC>
 __global__ void __launch_bounds__(512) gather_tile_kernel(const double4 *__restrict__ rec, const int *__restrict__ sidx,
                                                           const int4 *__restrict__ units, const int *__restrict__ nunits,
                                                           SpreadArgs a, const double *__restrict__ grid,
@@ -200,7 +238,7 @@ __global__ void __launch_bounds__(512) gather_tile_kernel(const double4 *__restr
     int ubeg = (int)max((int64_t)un.y, a.rlo), uend = (int)min((int64_t)un.y + un.z, a.rhi);
     if (ubeg >= uend) return;
     extern __shared__ double smem[];
-    const int P = a.P, Tp = a.Tp, pitch = a.pitch, plane = Tp * pitch;
+    const int P = PC > 0 ? PC : a.P, Tp = a.Tp, pitch = a.pitch, plane = Tp * pitch;
     const int ncell = Tp * plane;
     double *tile = smem;
     double *wts = tile + ncell;
@@ -218,21 +256,37 @@ __global__ void __launch_bounds__(512) gather_tile_kernel(const double4 *__restr
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = a.nwarps;
     const int npair = P * P;
+    LanePairs<PC> lp;
+    lp.init(lane);
     for (int b0 = ubeg; b0 < uend; b0 += a.batch) {
         int nb = min(a.batch, uend - b0);
         __syncthreads();
-        stage_batch<WIN, false>(rec, b0, nb, org, a, wts, loc);
+        stage_batch<WIN, false, PC>(rec, b0, nb, org, a, wts, loc);
         __syncthreads();
         for (int p = warp; p < nb; p += nw) {
             const int lx0 = loc[p * 4], ly0 = loc[p * 4 + 1], lz0 = loc[p * 4 + 2];
             const double *wx = wts + p * 3 * P, *wy = wx + P, *wz = wy + P;
             double acc = 0.0;
-            for (int pi = lane; pi < npair; pi += 32) {
-                int ty = pi / P, tz = pi - ty * P;
-                const double *c = tile + lx0 * plane + (ly0 + ty) * pitch + lz0 + tz;
-                double s = 0.0;
-                for (int t = 0; t < P; ++t) s = fma(wx[t], c[t * plane], s);
-                acc = fma(__dmul_rn(wy[ty], wz[tz]), s, acc);
+            if (PC > 0) {
+                const double *base = tile + lx0 * plane + ly0 * pitch + lz0;
+#pragma unroll
+                for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
+                    if (lp.valid(lane, it)) {
+                        const double *c = base + lp.ty[it] * pitch + lp.tz[it];
+                        double s = 0.0;
+#pragma unroll
+                        for (int t = 0; t < PC; ++t) s = fma(wx[t], c[t * plane], s);
+                        acc = fma(__dmul_rn(wy[lp.ty[it]], wz[lp.tz[it]]), s, acc);
+                    }
+                }
+            } else {
+                for (int pi = lane; pi < npair; pi += 32) {
+                    int ty = pi / P, tz = pi - ty * P;
+                    const double *c = tile + lx0 * plane + (ly0 + ty) * pitch + lz0 + tz;
+                    double s = 0.0;
+                    for (int t = 0; t < P; ++t) s = fma(wx[t], c[t * plane], s);
+                    acc = fma(__dmul_rn(wy[ty], wz[tz]), s, acc);
+                }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -405,6 +459,21 @@ static void bin_tiles(se_plan *pl, const double *pos, const double *q, int64_t N
     prof_end(pl, SE_K_SORT);
 }
 
+// compile-time window support for the common even P (others: runtime P)
+template <class F>
+static void dispatch_p(int P, F f) {
+    switch (P) {
+        case 4: f(std::integral_constant<int, 4>()); break;
+        case 6: f(std::integral_constant<int, 6>()); break;
+        case 8: f(std::integral_constant<int, 8>()); break;
+        case 10: f(std::integral_constant<int, 10>()); break;
+        case 12: f(std::integral_constant<int, 12>()); break;
+        case 14: f(std::integral_constant<int, 14>()); break;
+        case 16: f(std::integral_constant<int, 16>()); break;
+        default: f(std::integral_constant<int, 0>()); break;
+    }
+}
+
 template <class F>
 static void dispatch_window(int window, F f) {
     if (window == SE_WINDOW_GAUSSIAN)
@@ -434,11 +503,14 @@ void spread_run(se_plan *pl, const double *pos, const double *q, int64_t N, doub
     prof_begin(pl, SE_K_SPREAD);
     if (t.T > 0) {
         int64_t maxu = binning_max_units(pl->tbin, N, t.nt[0] * t.nt[1] * t.nt[2], kUnit);
+        const int PC = t.nwarps == pl->p.P ? pl->p.P : 0;
         dispatch_window(pl->p.window, [&](auto W) {
-            auto kern = spread_tile_kernel<decltype(W)::value>;
-            SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
-            kern<<<(unsigned)maxu, 32 * t.nwarps, t.smem, pl->stream>>>(rec, pl->tbin.units.as<int4>(),
-                                                                         pl->tbin.nunits.as<int>(), a, grid);
+            dispatch_p(PC, [&](auto PCv) {
+                auto kern = spread_tile_kernel<decltype(W)::value, decltype(PCv)::value>;
+                SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
+                kern<<<(unsigned)maxu, 32 * t.nwarps, t.smem, pl->stream>>>(rec, pl->tbin.units.as<int4>(),
+                                                                             pl->tbin.nunits.as<int>(), a, grid);
+            });
         });
     } else {
         int64_t n = a.rhi - a.rlo;
@@ -474,12 +546,15 @@ void gather_run(se_plan *pl, const double *grid, const double *pos, int64_t N, d
     prof_begin(pl, SE_K_GATHER);
     if (t.T > 0) {
         int64_t maxu = binning_max_units(pl->tbin, N, t.nt[0] * t.nt[1] * t.nt[2], kUnit);
+        const int PC = t.nwarps == pl->p.P ? pl->p.P : 0;
         dispatch_window(pl->p.window, [&](auto W) {
-            auto kern = gather_tile_kernel<decltype(W)::value>;
-            SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
-            kern<<<(unsigned)maxu, 32 * t.nwarps, t.smem, pl->stream>>>(
-                rec, pl->tbin.idx_sorted.as<int>(), pl->tbin.units.as<int4>(), pl->tbin.nunits.as<int>(), a, grid,
-                phi, h3, accumulate);
+            dispatch_p(PC, [&](auto PCv) {
+                auto kern = gather_tile_kernel<decltype(W)::value, decltype(PCv)::value>;
+                SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
+                kern<<<(unsigned)maxu, 32 * t.nwarps, t.smem, pl->stream>>>(
+                    rec, pl->tbin.idx_sorted.as<int>(), pl->tbin.units.as<int4>(), pl->tbin.nunits.as<int>(), a, grid,
+                    phi, h3, accumulate);
+            });
         });
     } else {
         int64_t n = a.rhi - a.rlo;
