@@ -31,6 +31,7 @@ struct RealArgs {
     int add_self;
     double sqrtpi;
     float rc2f;       // fp32 prefilter bound (rc^2 plus the fp32 coordinate rounding margin)
+    float rc2r;       // the same for the cell-relative |t'|^2 + |s'|^2 - 2 t'.s' form
     float Lf, invLf;  // box length for the fp32 minimum image
 };
 
@@ -128,24 +129,24 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 }
 
 // Exact fp64 evaluation of one compacted hit (target tt, source k of the
-// batch): d = x_t - (x_s + shift) (realspace.py:113-117), r < rc, the
-// coincidence check, and f = erfc(xi r)/r via 1/r = rsqrt(r^2).
-// Target side into the lane's private row; with NEWTON the source side
-// q_t f goes to the source's global accumulator (native fp64 REDG).
+// batch): d = x_t - (x_s + shift) (realspace.py:113-117), the coincidence
+// check (r < 1e-14, realspace.py:118-122), r < rc, and f = erfc(xi r)/r with
+// 1/r = rsqrt(r^2).  Target side into the lane's private row; with NEWTON
+// the source side q_t f goes to the source's global accumulator (REDG).
 template <bool MI, bool COUNT, bool NEWTON>
 __device__ __forceinline__ void eval_hit(unsigned en, const RealArgs &a, WarpBuf &wb, int lane, int jb, int tbase,
                                          double *__restrict__ acc_src, int &singular, long long &cnt) {
     const int tt = (int)(en >> 5), k = (int)(en & 31u);
     const double4 tp = wb.tst[tt];
     const double4 sp = wb.sst[k];
-    double dx = __dsub_rn(tp.x, sp.x), dy = __dsub_rn(tp.y, sp.y), dz = __dsub_rn(tp.z, sp.z);
+    double dx = tp.x - sp.x, dy = tp.y - sp.y, dz = tp.z - sp.z;
     if (MI) {
         if (a.mode[0] == 2) dx = min_image(dx, a.L);
         if (a.mode[1] == 2) dy = min_image(dy, a.L);
         if (a.mode[2] == 2) dz = min_image(dz, a.L);
     }
-    const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-    if (r2 < 1e-28) {  // r < 1e-14: the self pair or a coincidence (realspace.py:118-122)
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    if (r2 < 1e-28) {  // the self pair or a coincidence
         if (jb + k != tbase + tt) singular = 1;
         return;
     }
@@ -163,40 +164,47 @@ __device__ __forceinline__ void eval_hit(unsigned en, const RealArgs &a, WarpBuf
 }
 
 // One batch of <= 32 candidate sources [jb, jb+m) of a neighbour-cell run:
-//  1. fp32 prefilter of all 32 x m (target, source) pairs against a bound
-//     that covers the fp32 rounding of the coordinates -> per-lane hit mask
-//     (with NEWTON, sources of the target's own cell count only if j > t);
+//  1. fp32 prefilter of all 16 x m (target, source) pairs -> per-lane hit
+//     mask.  Outside minimum-image mode the test is
+//     |t'|^2 + |s'|^2 - 2 t'.s' < bound with t', s' relative to the unit's
+//     cell corner (4 fp32 ops per pair); the bound covers the fp32 rounding.
+//     With NEWTON, sources of the target's own cell count only if j > t;
 //  2. warp prefix scan of the hit counts and compaction of the hits into a
 //     target-major list;
-//  3. the list is evaluated 64 hits at a time (two per lane, independent
-//     chains) on full warps.
+//  3. the list is evaluated 64 hits at a time (two per lane) on full warps.
 template <bool MI, bool COUNT, bool NEWTON>
 __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int jb, int j1, double shx, double shy,
                                            double shz, const RealArgs &a, WarpBuf &wb, int lane, bool active,
-                                           float fx, float fy, float fz, int t, int tbase, int hs,
+                                           const float4 tq, const double3 org, int t, int tbase, int hs,
                                            double *__restrict__ acc_src, int &singular, long long &cnt) {
     const int j = jb + lane;
     if (j < j1) {
         const double4 r = rec[j];
-        const double xs = __dadd_rn(r.x, shx), ys = __dadd_rn(r.y, shy), zs = __dadd_rn(r.z, shz);
+        const double xs = r.x + shx, ys = r.y + shy, zs = r.z + shz;
         wb.sst[lane] = make_double4(xs, ys, zs, r.w);
-        wb.sf[lane] = make_float4((float)xs, (float)ys, (float)zs, 0.f);
+        if (MI) {
+            wb.sf[lane] = make_float4((float)xs, (float)ys, (float)zs, 0.f);
+        } else {
+            const float fx = (float)(xs - org.x), fy = (float)(ys - org.y), fz = (float)(zs - org.z);
+            wb.sf[lane] = make_float4(fx, fy, fz, fmaf(fz, fz, fmaf(fy, fy, fx * fx)));
+        }
     }
     __syncwarp();
     const int m = min(32, j1 - jb);
     unsigned hit = 0;
     const int k0 = (lane / kT) * kT;  // this lane's half of the batch
     if (active) {
-        auto test = [&](int kk) -> unsigned {
+        auto test = [&](int kk) -> bool {
             const float4 p = wb.sf[k0 + kk];
-            float dx = fx - p.x, dy = fy - p.y, dz = fz - p.z;
-            if (MI) {
+            if (MI) {  // tq = absolute fp32 target position
+                float dx = tq.x - p.x, dy = tq.y - p.y, dz = tq.z - p.z;
                 if (a.mode[0] == 2) dx = min_image_f(dx, a.Lf, a.invLf);
                 if (a.mode[1] == 2) dy = min_image_f(dy, a.Lf, a.invLf);
                 if (a.mode[2] == 2) dz = min_image_f(dz, a.Lf, a.invLf);
+                return fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < a.rc2f;
             }
-            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            return r2 < a.rc2f ? 1u : 0u;
+            // tq = (-2 t'x, -2 t'y, -2 t'z, |t'|^2)
+            return fmaf(tq.x, p.x, fmaf(tq.y, p.y, fmaf(tq.z, p.z, tq.w + p.w))) < a.rc2r;
         };
         if (m == 32) {  // full batch: compile-time bit positions, no bounds test
 #pragma unroll
@@ -262,7 +270,16 @@ __global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
     const double4 tp = active ? rec[t] : make_double4(0, 0, 0, 0);
     if (lane < kT) wb.tst[lane] = tp;
     for (int i = 0; i < kT; ++i) wb.acc[lane][i] = 0.0;
-    const float fx = (float)tp.x, fy = (float)tp.y, fz = (float)tp.z;
+    // prefilter operands: MI -> absolute fp32 position; otherwise -2 t' and
+    // |t'|^2 with t' relative to the cell corner
+    const double3 org = make_double3(cx * a.edge, cy * a.edge, cz * a.edge);
+    float4 tq;
+    if (MI) {
+        tq = make_float4((float)tp.x, (float)tp.y, (float)tp.z, 0.f);
+    } else {
+        const float rx = (float)(tp.x - org.x), ry = (float)(tp.y - org.y), rz = (float)(tp.z - org.z);
+        tq = make_float4(-2.f * rx, -2.f * ry, -2.f * rz, fmaf(rz, rz, fmaf(ry, ry, rx * rx)));
+    }
     int singular = 0;
     long long cnt = 0;
     __syncwarp();
@@ -287,7 +304,7 @@ __global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
     if (NEWTON) xlo = cx;  // ox >= 0
     auto run = [&](int j0, int j1, double shx, double shy, double shz, int hs) {
         for (int jb = j0; jb < j1; jb += 32)
-            pair_batch<MI, COUNT, NEWTON>(rec, jb, j1, shx, shy, shz, a, wb, lane, active, fx, fy, fz, t, un.y, hs,
+            pair_batch<MI, COUNT, NEWTON>(rec, jb, j1, shx, shy, shz, a, wb, lane, active, tq, org, t, un.y, hs,
                                           acc_src, singular, cnt);
     };
     for (int ox = xlo; ox <= xhi; ++ox) {
@@ -403,6 +420,10 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     for (int ax = 0; ax < 3; ++ax) c.mode[ax] = ax < pl->D ? (c.n >= 5 ? 1 : 2) : 0;
     a.n = c.n;
     a.edge = c.edge;
+    // cell-relative prefilter: |t'|, |s'| <= 3 sqrt(3) e, so the fp32 form
+    // |t'|^2 + |s'|^2 - 2 t'.s' is within ~1.2e-5 e^2 (+ ~1.2e-6 rc e from
+    // rounding t', s') of r^2; the bound keeps 3x that
+    a.rc2r = (float)(rc * rc + 4e-5 * c.edge * c.edge + 4e-6 * rc * c.edge);
     for (int ax = 0; ax < 3; ++ax) a.mode[ax] = c.mode[ax];
     int nbins = c.n * c.n * c.n;
     cudaStream_t st = pl->stream;
