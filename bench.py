@@ -34,25 +34,42 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG = dict(workload="cfg2", D=3, N=1_000_000, L=10.0, M=128, P=8, window="bm", beta=20.0,
-           rc=1.0, eps=1e-8, seed=2)
-CFG["xi"] = math.sqrt(-math.log(CFG["eps"])) / CFG["rc"]  # 4.2919
-METRIC = "particles/sec, full SE potential (cfg2: D=3, N=1e6, ES P=8, M=128^3, rc=1.0, fp64)"
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import workloads  # noqa: E402  (seeded BASELINE configs)
+
 FLOP_PER_PAIR = 40  # SURVEY 8d constant: erfc(xi r)/r ~ exp + rational + sqrt + div + fma
+DESCR = {
+    "cfg1": "cfg1: D=3, N=2000 uniform in L=1, Gaussian P=16, M=32^3, rc=0.3, xi=12.94",
+    "cfg2": "cfg2: D=3, N=1e6 uniform in L=10, ES P=8 beta=20, M=128^3, rc=1.0, xi=4.2919",
+    "cfg3": "cfg3 (as worded): D=2, N=2e5 in L=5, ES P=8, M=96^2 x 104, s0=4, s=2, nI=10, xi=6",
+    "cfg3_tol": "cfg3 (tolerance-meeting): D=2, N=2e5 in L=5, ES P=10, s0=4, s=4, nI=48, xi=6",
+    "cfg4": "cfg4: D=1 (cubic embedding L=8 of 4x4x8), N=2e5, Gaussian P=12, M=128, xi=4, s0=2.4674, nI=39",
+    "cfg5": "cfg5: D=0, N=5e5 (ball + 32 Gaussian clusters) in L=4, ES P=10 beta=25, M=96, xi=6, kernel path",
+}
+CFG = {}
+
+
+def load_workload(name):
+    w = workloads.ALL[name]()
+    CFG.clear()
+    CFG.update(w["prm"])
+    CFG.update(workload=name, D=w["D"], L=w["L"], N=len(w["q"]), seed=int(name[3]))
+    CFG["_pos"], CFG["_q"] = w["pos"], w["q"]
+    return w
+
+
+def metric():
+    return (f"particles/sec, full SE potential ({DESCR[CFG['workload']]}, fp64)")
 
 
 def make_inputs():
-    rng = np.random.default_rng(CFG["seed"])
-    pos = rng.random((CFG["N"], 3)) * CFG["L"]
-    q = rng.uniform(-1.0, 1.0, CFG["N"])
-    q -= q.mean()
-    return pos, q
+    return CFG["_pos"], CFG["_q"]
 
 
 def se_params():
     from paper_1712_04732_b200 import SEParams
-    return SEParams(xi=CFG["xi"], rc=CFG["rc"], M=CFG["M"], P=CFG["P"], window=CFG["window"],
-                    shape=CFG["beta"], eps=CFG["eps"])
+    keys = ("xi", "rc", "M", "P", "window", "shape", "s0", "s", "nI", "R", "eps")
+    return SEParams(**{k: CFG[k] for k in keys if k in CFG})
 
 
 def peaks():
@@ -134,33 +151,45 @@ def _oracle():
 
 
 def cpu_sample(pos, q, threads=1, n_cells=2, n_kspace=20000, seed=0):
-    """Oracle port of the reference on a bounded sample of cfg2, extrapolated
-    to the full N: real space on every target of `n_cells` random rc-cells
-    (the reference's per-home-cell dense blocks, realspace.py:100-126), spread
-    + gather for `n_kspace` particles (sekspace.py:130-178), the full 128^3
-    k-space stage, and the self term."""
+    """Oracle port of the reference on a bounded sample of the workload,
+    extrapolated to the full N: real space on every target of `n_cells`
+    random occupied rc-cells (the reference's per-home-cell dense blocks,
+    realspace.py:100-126), spread + gather for `n_kspace` particles
+    (sekspace.py:130-178), the full k-space stage (precompute excluded, as
+    cli.py:110-111), and the self term."""
     from concurrent.futures import ThreadPoolExecutor
 
     from threadpoolctl import threadpool_limits
 
     orc = _oracle()
-    N, L = len(q), CFG["L"]
+    N, L, D = len(q), CFG["L"], CFG["D"]
     rng = np.random.default_rng(seed)
-    n = int(L // CFG["rc"])
+    n = max(1, int(L // CFG["rc"]))
     cell = np.minimum((pos / (L / n)).astype(int), n - 1)
     flat = (cell[:, 0] * n + cell[:, 1]) * n + cell[:, 2]
-    cells = rng.choice(n ** 3, n_cells, replace=False)
-    g = orc.geometry(L, 3, CFG["M"], CFG["P"])
+    occupied = np.unique(flat[rng.choice(N, min(N, 64 * n_cells), replace=False)])
+    cells = rng.choice(occupied, min(n_cells, len(occupied)), replace=False)
+    g = orc.geometry(L, D, CFG["M"], CFG["P"], CFG.get("s0", 1.0), CFG.get("s", 1.0), CFG.get("R", 0.0))
     xi, rc = CFG["xi"], CFG["rc"]
+    win, shape = CFG["window"], CFG["shape"]
+    if D == 0:
+        table, kg = orc.d0_kernel_table(L, CFG["M"], CFG["P"], CFG["s0"], rc)  # precompute: untimed
+
+    def kstage(H):
+        if D == 3:
+            return orc.kspace_d3(H, g, xi, win, shape)
+        if D == 0:
+            return orc.kspace_d0_kernel(H, g, xi, win, shape, table, kg["nconv"])
+        return orc.kspace_mixed(H, g, xi, win, shape, CFG["nI"])
     with threadpool_limits(1):
         t0 = time.perf_counter()
         tsets = [np.nonzero(flat == c)[0] for c in cells]
         if threads > 1:
             with ThreadPoolExecutor(threads) as ex:
-                list(ex.map(lambda s: orc.realspace(pos, q, L, 3, xi, rc, targets=s), tsets))
+                list(ex.map(lambda s: orc.realspace(pos, q, L, D, xi, rc, targets=s), tsets))
         else:
             for s in tsets:
-                orc.realspace(pos, q, L, 3, xi, rc, targets=s)
+                orc.realspace(pos, q, L, D, xi, rc, targets=s)
         t_real = time.perf_counter() - t0
         n_t = sum(len(s) for s in tsets)
         sel = rng.choice(N, n_kspace, replace=False)
@@ -168,31 +197,31 @@ def cpu_sample(pos, q, threads=1, n_cells=2, n_kspace=20000, seed=0):
         t0 = time.perf_counter()
         if threads > 1:
             with ThreadPoolExecutor(threads) as ex:
-                parts = list(ex.map(lambda s: orc.spread(pos[s], q[s], g, CFG["window"], CFG["beta"]), chunks))
+                parts = list(ex.map(lambda s: orc.spread(pos[s], q[s], g, win, shape), chunks))
         else:
-            parts = [orc.spread(pos[s], q[s], g, CFG["window"], CFG["beta"]) for s in chunks]
+            parts = [orc.spread(pos[s], q[s], g, win, shape) for s in chunks]
         H = parts[0]
         for p_ in parts[1:]:
             H = H + p_
         t_spread = time.perf_counter() - t0
         t0 = time.perf_counter()
-        Ht = orc.kspace_d3(H, g, xi, CFG["window"], CFG["beta"])
+        Ht = kstage(H)
         t_fft = time.perf_counter() - t0
         t0 = time.perf_counter()
         if threads > 1:
             with ThreadPoolExecutor(threads) as ex:
-                list(ex.map(lambda s: orc.gather(Ht, pos[s], g, CFG["window"], CFG["beta"]), chunks))
+                list(ex.map(lambda s: orc.gather(Ht, pos[s], g, win, shape), chunks))
         else:
-            orc.gather(Ht, pos[sel], g, CFG["window"], CFG["beta"])
+            orc.gather(Ht, pos[sel], g, win, shape)
         t_gather = time.perf_counter() - t0
         t0 = time.perf_counter()
         orc.self_term(q, xi)
         t_self = time.perf_counter() - t0
     est = t_real * N / n_t + (t_spread + t_gather) * N / n_kspace + t_fft + t_self
     return {"value": N / est, "unit": "particles/s", "cores": threads, "kind": "port",
-            "sample": (f"oracle/se_oracle.py on cfg2: real space for all {n_t} targets of {n_cells} random "
-                       f"rc-cells, spread+gather of {n_kspace} particles, full 128^3 k-space, self term; "
-                       f"extrapolated to N={N} ({est:.0f} s per evaluation)"),
+            "sample": (f"oracle/se_oracle.py on {CFG['workload']}: real space for all {n_t} targets of "
+                       f"{len(cells)} random rc-cells, spread+gather of {n_kspace} particles, full k-space stage, "
+                       f"self term; extrapolated to N={N} ({est:.0f} s per evaluation)"),
             "seconds_sampled": t_real + t_spread + t_fft + t_gather + t_self,
             "est_seconds_full": est}
 
@@ -202,21 +231,22 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    load_workload(args.workload)
     pos, q = make_inputs()
     threads = os.cpu_count() or 1
     vals, last = [], None
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(pos, q, threads=threads, n_cells=threads, n_kspace=20000 * max(1, threads // 2), seed=i)
+        r = cpu_sample(pos, q, threads=threads, n_cells=threads, n_kspace=min(len(q), 20000 * max(1, threads // 2)),
+                       seed=i)
         if i >= args.warmup:
             vals.append(r["value"])
             last = r
     value = statistics.mean(vals)
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "particles/s",
+    line = {"impl": "reference", "metric": metric(), "value": value, "unit": "particles/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * CFG["N"] / value, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.md 3.1)",
-            "config": {"workload": "cfg2: D=3, N=1e6 uniform in L=10, ES P=8 beta=20, M=128^3, rc=1.0, "
-                                   f"xi={CFG['xi']:.4f}", "N": CFG["N"], "seed": CFG["seed"]},
+            "config": {"workload": DESCR[CFG["workload"]], "N": CFG["N"], "seed": CFG["seed"]},
             "cpu_baseline": {"value": value, "unit": "particles/s", "cores": threads, "kind": "port",
                              "sample": last["sample"]},
             "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -241,6 +271,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    load_workload(args.workload)
     peri = se.Periodicity(CFG["D"])
     prm = se_params()
     N, L = CFG["N"], CFG["L"]
@@ -346,7 +377,8 @@ def run_ours(args):
         if n:
             kern[k] = {"ms_per_launch": ms / n, "share_of_step": (ms / n) / ms_per_step}
     P3 = CFG["P"] ** 3
-    G = CFG["M"] ** 3
+    gshape = plan.grid().shape
+    G = gshape[0] * gshape[1] * gshape[2]
     for k in ("spread", "gather"):
         if k in kern:
             t = kern[k]["ms_per_launch"] * 1e-3
@@ -366,12 +398,11 @@ def run_ours(args):
     except Exception:
         pass
 
-    line = {"metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
+    line = {"metric": metric(), "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.md 3.1; no public dataset exists for this path)",
-            "config": {"workload": "cfg2: D=3, N=1e6 uniform in L=10, ES P=8 beta=20, M=128^3, rc=1.0, "
-                                   f"xi={CFG['xi']:.4f}", "N": N, "seed": CFG["seed"],
+            "config": {"workload": DESCR[CFG["workload"]], "N": N, "seed": CFG["seed"],
                        "parallelism": f"particle-shard x{world} (grid + phi sum-all-reduce)",
                        "l2": "flushed (256 MB write) between timed steps, outside the step events"},
             "e2e": e2e, "roofline": roofline, "kernels": kern, "gpu_launches": launches,
@@ -394,6 +425,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=sorted(workloads.ALL),
+                    help="BASELINE config (default cfg2 = configs[1], the headline)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -351,3 +351,34 @@ def test_cfg2_full_size_linearity_and_translation(cfg2_full):
     sh[sh >= L] = 0.0
     phi3 = se.total_potential(se.ParticleSystem(sh, q, L), p, se.Periodicity(3))
     assert se.relative_rms_error(phi3, phi) < 1e-11
+
+
+# ------------------------------------------ BASELINE configs at full size
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3", "cfg3_tol", "cfg4", "cfg5"])
+def test_baseline_config_full_size(name):
+    import sys as _sys
+    _sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import workloads
+
+    w = workloads.ALL[name]()
+    pos, q, L, D = w["pos"], w["q"], w["L"], w["D"]
+    p = se.SEParams(**w["prm"])
+    peri = se.Periodicity(D)
+    s = se.ParticleSystem(pos, q, L)
+    t = {}
+    phi = se.total_potential(s, p, peri, timings=t)
+    assert np.all(np.isfinite(phi))
+    phir = se.real_space_sum(s, p.xi, p.rc, peri)
+    phik = se.se_kspace(s, p, peri)
+    assert se.relative_rms_error(phi, phir + phik + se.self_term(q, p.xi)) < 1e-13
+    rng = np.random.default_rng(7)
+    sel = rng.choice(len(q), 64, replace=False)
+    ref = orc.realspace(pos, q, L, D, p.xi, p.rc, targets=sel)
+    assert se.relative_rms_error(phir[sel], ref) < 1e-12
+    # k-space parity on a neutral subset with the same grid geometry
+    sub = rng.choice(len(q), 3000, replace=False)
+    qs = q[sub] - q[sub].mean()
+    gk = se.se_kspace(se.ParticleSystem(pos[sub], qs, L), p, peri)
+    rk = orc.se_kspace(pos[sub], qs, L, D, dict(p.__dict__))
+    assert se.relative_rms_error(gk, rk) < 1e-11
