@@ -377,7 +377,7 @@ def test_baseline_config_full_size(name):
     ref = orc.realspace(pos, q, L, D, p.xi, p.rc, targets=sel)
     assert se.relative_rms_error(phir[sel], ref) < 1e-12
     # k-space parity on a neutral subset with the same grid geometry
-    sub = rng.choice(len(q), 3000, replace=False)
+    sub = rng.choice(len(q), min(3000, len(q)), replace=False)
     qs = q[sub] - q[sub].mean()
     gk = se.se_kspace(se.ParticleSystem(pos[sub], qs, L), p, peri)
     rk = orc.se_kspace(pos[sub], qs, L, D, dict(p.__dict__))
