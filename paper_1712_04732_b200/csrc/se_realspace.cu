@@ -90,6 +90,8 @@ __device__ __forceinline__ double erfc_fast(double x) {
     if (x > SE_ERFC_XMAX) return erfc(x);
     const double t = (x - SE_ERFC_K) * rcp_nr(x + SE_ERFC_K);
     const double s = fma(t, SE_ERFC_A, SE_ERFC_B);
+    // Horner (Estrin's shorter chains measured slower: the kernel is
+    // fp64-issue bound, not latency bound)
     double p = se_erfcx_c[SE_ERFC_NE];
 #pragma unroll
     for (int i = SE_ERFC_NE - 1; i >= 0; --i) p = fma(p, s, se_erfcx_c[i]);
@@ -146,21 +148,24 @@ __device__ __forceinline__ void eval_hit(unsigned en, const RealArgs &a, WarpBuf
         if (a.mode[2] == 2) dz = min_image(dz, a.L);
     }
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-    if (r2 < 1e-28) {  // the self pair or a coincidence
-        if (jb + k != tbase + tt) singular = 1;
-        return;
-    }
-    const double rinv = rsqrt_nr(r2);
-    const double rr = r2 * rinv;
-    if (!(rr < a.rc)) return;
+    // r < 1e-14: the self pair (never compacted with NEWTON) or a coincidence
+    const bool zero = r2 < 1e-28;
+    if (NEWTON)
+        singular |= zero ? 1 : 0;
+    else if (zero && jb + k != tbase + tt)
+        singular = 1;
+    const double r2s = zero ? 1.0 : r2;
+    const double rinv = rsqrt_nr(r2s);
+    const double rr = r2s * rinv;
+    const bool ok = !zero && rr < a.rc;
     if (COUNT) {
-        cnt += NEWTON ? 2 : 1;
+        cnt += ok ? (NEWTON ? 2 : 1) : 0;
         return;
     }
-    const double f = erfc_fast(a.xi * rr) * rinv;
+    const double f = ok ? erfc_fast(a.xi * rr) * rinv : 0.0;
     double *slot = &wb.acc[lane][(tt + lane) & (kT - 1)];
     *slot = fma(sp.w, f, *slot);
-    if (NEWTON) atomicAdd(acc_src + jb + k, tp.w * f);
+    if (NEWTON && ok) atomicAdd(acc_src + jb + k, tp.w * f);
 }
 
 // One batch of <= 32 candidate sources [jb, jb+m) of a neighbour-cell run:
@@ -230,10 +235,13 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     const int incl = warp_incl_scan(c, lane);
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     int pos = incl - c;
-    while (hit) {
-        const int k = __ffs(hit) - 1;
-        hit &= hit - 1;
-        wb.ent[pos++] = (unsigned short)(((lane & (kT - 1)) << 5) | k);
+    {   // fixed, fully predicated compaction of this lane's <= 16 hit bits
+        const unsigned h16 = hit >> k0;
+        const unsigned tag = ((unsigned)(lane & (kT - 1)) << 5) | (unsigned)k0;
+        unsigned short *dst = wb.ent + pos;
+#pragma unroll
+        for (int kk = 0; kk < kT; ++kk)
+            if (h16 & (1u << kk)) *dst++ = (unsigned short)(tag | kk);
     }
     __syncwarp();
     for (int e0 = 0; e0 < total; e0 += 64) {
