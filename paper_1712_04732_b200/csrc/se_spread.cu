@@ -23,6 +23,7 @@
 // Windows whose padded tile cannot fit in shared memory (P > ~24) use a
 // direct kernel (one warp per particle, global fp64 reductions / loads).
 #include "se_common.h"
+#include "se_erfc_coeffs.h"
 
 namespace se {
 
@@ -37,22 +38,35 @@ struct SpreadArgs {
     // window
     int window;
     double w, shapep, peak, mm, ww2, i0b;
+    double invw, gcoef;  // 1/w and -m^2/(2 w^2)
     int64_t rlo, rhi;  // sorted-particle range of this shard
 };
 
 // ---------------------------------------------------------------- windows
+// exp(v) for v <= 0 by Cody-Waite reduction and the degree-12 polynomial of
+// se_erfc_coeffs.h (coefficients as constant-bank operands; ~1 ulp).
+__device__ __forceinline__ double exp_nonpos(double v) {
+    if (v < -700.0) return 0.0;
+    const double n = rint(v * SE_LOG2E);
+    const double r = fma(n, -SE_LN2_LO, fma(n, -SE_LN2_HI, v));
+    double e = se_exp_c[SE_EXP_NX];
+#pragma unroll
+    for (int i = SE_EXP_NX - 1; i >= 0; --i) e = fma(e, r, se_exp_c[i]);
+    return e * __hiloint2double(((int)n + 1023) << 20, 0);
+}
+
+// windows.py:74-84 (Gaussian), 106-112 (KB), 148-154 (ES / BM); the
+// divisions by w and 2w^2 are multiplications by host-computed reciprocals
+// (<= 1 ulp from the reference's rounding).
 template <int WIN>
 __device__ __forceinline__ double window_eval(double x, const SpreadArgs &a) {
     if (!(fabs(x) <= a.w)) return 0.0;
-    if (WIN == SE_WINDOW_GAUSSIAN) {
-        // windows.py:81-83: peak * exp(-(m*m)*(x*x)/(2*w*w))
-        return a.peak * exp(__ddiv_rn(__dmul_rn(-a.mm, __dmul_rn(x, x)), a.ww2));
-    }
-    double r = __ddiv_rn(x, a.w);
-    double t = __dsub_rn(1.0, __dmul_rn(r, r));
+    if (WIN == SE_WINDOW_GAUSSIAN) return a.peak * exp_nonpos(a.gcoef * (x * x));  // gcoef = -m^2 / (2 w^2)
+    const double r = x * a.invw;
+    double t = fma(-r, r, 1.0);
     t = t < 0.0 ? 0.0 : t;
-    if (WIN == SE_WINDOW_BM) return exp(__dmul_rn(a.shapep, __dsub_rn(sqrt(t), 1.0)));  // windows.py:151-153
-    return __ddiv_rn(cyl_bessel_i0(__dmul_rn(a.shapep, sqrt(t))), a.i0b);                 // windows.py:110-111
+    if (WIN == SE_WINDOW_BM) return exp_nonpos(a.shapep * (sqrt(t) - 1.0));
+    return cyl_bessel_i0(a.shapep * sqrt(t)) / a.i0b;
 }
 
 // first stencil index along one axis (sekspace.py:113-114), IEEE division.
@@ -126,18 +140,37 @@ __device__ __forceinline__ void unit_origin(int bin, const SpreadArgs &a, int or
     org[2] = a.lo[2] + tz * a.T;
 }
 
-// global linear index of padded-tile cell (lx,ly,lz); -1 if off the grid
-__device__ __forceinline__ long long tile_to_global(int lx, int ly, int lz, const int org[3], const SpreadArgs &a) {
-    int gidx[3] = {org[0] + lx, org[1] + ly, org[2] + lz};
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-        if (ax < a.D) {
-            gidx[ax] %= a.M;
-        } else if (gidx[ax] < 0 || gidx[ax] >= a.Mt) {
-            return -1;
+// Per-axis grid index of every padded-tile coordinate (-1 off the grid),
+// wrapped on periodic axes: gmap[ax * Tp + l].
+__device__ __forceinline__ void build_axis_maps(const int org[3], const SpreadArgs &a, int *gmap) {
+    for (int i = threadIdx.x; i < 3 * a.Tp; i += blockDim.x) {
+        const int ax = i / a.Tp, l = i - ax * a.Tp;
+        int g = org[ax] + l;
+        if (ax < a.D)
+            g %= a.M;
+        else if (g < 0 || g >= a.Mt)
+            g = -1;
+        gmap[i] = g;
+    }
+}
+
+// Visit every padded-tile cell with its grid index: one warp per (lx, ly)
+// row, lanes along z (coalesced in the grid's z-fastest layout).
+template <class F>
+__device__ __forceinline__ void for_tile_cells(const SpreadArgs &a, const int *gmap, F f) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    const int Tp = a.Tp;
+    for (int row = warp; row < Tp * Tp; row += nwarp) {
+        const int lx = row / Tp, ly = row - lx * Tp;
+        const int gx = gmap[lx], gy = gmap[Tp + ly];
+        const bool rok = gx >= 0 && gy >= 0;
+        const long long gbase = ((long long)gx * a.shape[1] + gy) * a.shape[2];
+        const int tbase = (lx * Tp + ly) * a.pitch;
+        for (int lz = lane; lz < Tp; lz += 32) {
+            const int gz = gmap[2 * Tp + lz];
+            f(tbase + lz, rok && gz >= 0 ? gbase + gz : -1LL);
         }
     }
-    return ((long long)gidx[0] * a.shape[1] + gidx[1]) * a.shape[2] + gidx[2];
 }
 
 // Per-lane share of the P x P (y, z) footprint: lane handles pairs
@@ -146,13 +179,14 @@ __device__ __forceinline__ long long tile_to_global(int lx, int ly, int lz, cons
 template <int PC>
 struct LanePairs {
     static constexpr int NPI = PC > 0 ? (PC * PC + 31) / 32 : 1;
-    int ty[NPI], tz[NPI];
-    __device__ __forceinline__ void init(int lane) {
+    int ty[NPI], tz[NPI], off[NPI];
+    __device__ __forceinline__ void init(int lane, int pitch) {
 #pragma unroll
         for (int it = 0; it < NPI; ++it) {
             const int pi = lane + 32 * it;
             ty[it] = pi / (PC > 0 ? PC : 1);
             tz[it] = pi - ty[it] * (PC > 0 ? PC : 1);
+            off[it] = ty[it] * pitch + tz[it];
         }
     }
     __device__ __forceinline__ bool valid(int lane, int it) const { return lane + 32 * it < PC * PC; }
@@ -172,14 +206,16 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
     double *tile = smem;
     double *wts = tile + ncell;
     int *loc = reinterpret_cast<int *>(wts + a.batch * 3 * P);
+    int *gmap = loc + 4 * a.batch;
     int org[3];
     unit_origin(un.x, a, org);
     for (int i = threadIdx.x; i < ncell; i += blockDim.x) tile[i] = 0.0;
+    build_axis_maps(org, a, gmap);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = a.nwarps;
     const int npair = P * P;
     LanePairs<PC> lp;
-    lp.init(lane);
+    lp.init(lane, pitch);
     for (int b0 = ubeg; b0 < uend; b0 += a.batch) {
         int nb = min(a.batch, uend - b0);
         __syncthreads();  // tile zeroed / previous batch consumed
@@ -197,7 +233,7 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
 #pragma unroll
                 for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
                     if (lp.valid(lane, it)) {
-                        double *c = base + lp.ty[it] * pitch + lp.tz[it];
+                        double *c = base + lp.off[it];
                         *c = fma(wxt, __dmul_rn(wy[lp.ty[it]], wz[lp.tz[it]]), *c);
                     }
                 }
@@ -218,14 +254,10 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < ncell; i += blockDim.x) {
-        double v = tile[i];
-        if (v == 0.0) continue;
-        int lx = i / plane, rem = i - lx * plane, ly = rem / pitch, lz = rem - ly * pitch;
-        if (lz >= Tp) continue;
-        long long gi = tile_to_global(lx, ly, lz, org, a);
-        if (gi >= 0) atomicAdd(grid + gi, v);
-    }
+    for_tile_cells(a, gmap, [&](int ti, long long gi) {
+        const double v = tile[ti];
+        if (gi >= 0 && v != 0.0) atomicAdd(grid + gi, v);
+    });
 }
 
 template <int WIN, int PC>
@@ -243,21 +275,16 @@ __global__ void __launch_bounds__(512) gather_tile_kernel(const double4 *__restr
     double *tile = smem;
     double *wts = tile + ncell;
     int *loc = reinterpret_cast<int *>(wts + a.batch * 3 * P);
+    int *gmap = loc + 4 * a.batch;
     int org[3];
     unit_origin(un.x, a, org);
-    for (int i = threadIdx.x; i < ncell; i += blockDim.x) {
-        int lx = i / plane, rem = i - lx * plane, ly = rem / pitch, lz = rem - ly * pitch;
-        double v = 0.0;
-        if (lz < Tp) {
-            long long gi = tile_to_global(lx, ly, lz, org, a);
-            if (gi >= 0) v = grid[gi];
-        }
-        tile[i] = v;
-    }
+    build_axis_maps(org, a, gmap);
+    __syncthreads();
+    for_tile_cells(a, gmap, [&](int ti, long long gi) { tile[ti] = gi >= 0 ? grid[gi] : 0.0; });
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = a.nwarps;
     const int npair = P * P;
     LanePairs<PC> lp;
-    lp.init(lane);
+    lp.init(lane, pitch);
     for (int b0 = ubeg; b0 < uend; b0 += a.batch) {
         int nb = min(a.batch, uend - b0);
         __syncthreads();
@@ -272,7 +299,7 @@ __global__ void __launch_bounds__(512) gather_tile_kernel(const double4 *__restr
 #pragma unroll
                 for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
                     if (lp.valid(lane, it)) {
-                        const double *c = base + lp.ty[it] * pitch + lp.tz[it];
+                        const double *c = base + lp.off[it];
                         double s = 0.0;
 #pragma unroll
                         for (int t = 0; t < PC; ++t) s = fma(wx[t], c[t * plane], s);
@@ -378,6 +405,8 @@ static SpreadArgs make_args(se_plan *pl) {
     a.peak = p.shape / (a.w * std::sqrt(2.0 * M_PI));
     a.mm = p.shape * p.shape;
     a.ww2 = 2.0 * a.w * a.w;
+    a.invw = 1.0 / a.w;
+    a.gcoef = -a.mm / a.ww2;
     a.i0b = 1.0;
     if (p.window == SE_WINDOW_KB) a.i0b = bessel_i0(p.shape);
     const TileGeom &t = pl->tile;
@@ -395,6 +424,9 @@ static SpreadArgs make_args(se_plan *pl) {
 
 static const int kUnit = 1024;     // particles per spreading work unit
 static const size_t kSmemCap = 200 * 1024;
+// preferred per-CTA budget: 4 CTAs per SM (the per-particle loop is latency
+// bound, so occupancy beats the smaller halo of larger tiles)
+static size_t kSmemFirst = 57 * 1024;  // measured: 98 KB 0.78/0.73 ms, 57 KB 0.60/0.45, 46 KB 0.65/0.55 (cfg2)
 
 void tile_setup(se_plan *pl) {
     TileGeom &t = pl->tile;
@@ -408,12 +440,13 @@ void tile_setup(se_plan *pl) {
     const int cand[] = {16, 14, 12, 10, 8, 6, 4, 2, 1};
     t.T = 0;
     for (size_t pass = 0; pass < 2 && !t.T; ++pass) {
-        size_t cap = pass == 0 ? 110 * 1024 : kSmemCap;
+        size_t cap = pass == 0 ? kSmemFirst : kSmemCap;
         for (int T : cand) {
             int Tp = T + P - 1;
             int pitch = Tp;
             if (P % 16 == 8) pitch = Tp + ((8 - Tp % 16) + 16) % 16;
-            size_t bytes = sizeof(double) * ((size_t)Tp * Tp * pitch + (size_t)t.batch * 3 * P) + sizeof(int) * 4 * t.batch;
+            size_t bytes = sizeof(double) * ((size_t)Tp * Tp * pitch + (size_t)t.batch * 3 * P) +
+                           sizeof(int) * (4 * t.batch + 3 * Tp);
             if (bytes <= cap) {
                 t.T = T;
                 t.Tp = Tp;
