@@ -202,6 +202,33 @@ int se_realspace_host(se_plan_t plan, const double *pos, const double *q, int64_
  * (`out` must hold nconv*nconv*(nconv/2+1) doubles). */
 int se_d0_kernel_table_host(se_plan_t plan, double *out);
 
+/* ------------------------------------------------------------------ *
+ * Stage-level API of the reference (aft.py / sekspace.scale).         *
+ * ------------------------------------------------------------------ */
+
+/* The FFT-engine plugin (aft.py:24-53, numpy semantics) on cuFFT, for a
+ * C-ordered array of `ndim` dims and the contiguous axis block [ax0, ax1];
+ * complex data are interleaved (re, im) doubles.  c2c: same shape in and
+ * out, inverse carries 1/n.  r2c: real `shape` in, the last transformed axis
+ * becomes n/2+1.  c2r: `out_shape` is the real output shape, 1/n included.
+ * Host pointers; `device` selects the GPU. */
+int se_fft_c2c_host(int device, int ndim, const int64_t *shape, int ax0, int ax1, int inverse,
+                    const double *in, double *out);
+int se_fft_r2c_host(int device, int ndim, const int64_t *shape, int ax0, int ax1,
+                    const double *in, double *out);
+int se_fft_c2r_host(int device, int ndim, const int64_t *out_shape, int ax0, int ax1,
+                    const double *in, double *out);
+/* sekspace.scale (sekspace.py:192-254) in place on a SpectralField's blocks
+ * (aft.py:124-152): D=3 `full` (M^3) or D=0 `zero` (g0^3) in cube_or_zero;
+ * D in {1,2}: zero block, I rows (gs^{3-D} each) with I_idx (nI x D periodic
+ * mode indices) and J rows (Mt^{3-D}) with J_idx.  kp/wp, k0/w0, ks/ws,
+ * kt/wt: wavenumbers and window transforms on the M, g0, gs and Mt mode sets. */
+int se_scale_blocks_host(int device, int D, int M, int Mt, int g0, int gs, double xi, double R,
+                         const double *kp, const double *wp, const double *k0, const double *w0,
+                         const double *ks, const double *ws, const double *kt, const double *wt,
+                         double *cube_or_zero, double *Iblk, const int *I_idx, int64_t nI,
+                         double *Jblk, const int *J_idx, int64_t nJ);
+
 /* Thread-local message of the last failing call. */
 const char *se_last_error(void);
 /* Library version string. */

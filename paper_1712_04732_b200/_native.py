@@ -84,6 +84,12 @@ SIGNATURES = {
     "se_self_term_host": [_P, ctypes.c_int64, ctypes.c_double, _P],
     "se_self_term_dev": [_P, ctypes.c_int64, ctypes.c_double, _P, _P],
     "se_d0_kernel_table_host": [_P, _P],
+    "se_fft_c2c_host": [ctypes.c_int, ctypes.c_int, c_int64_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P],
+    "se_fft_r2c_host": [ctypes.c_int, ctypes.c_int, c_int64_p, ctypes.c_int, ctypes.c_int, _P, _P],
+    "se_fft_c2r_host": [ctypes.c_int, ctypes.c_int, c_int64_p, ctypes.c_int, ctypes.c_int, _P, _P],
+    "se_scale_blocks_host": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                             ctypes.c_double, ctypes.c_double] + [_P] * 8 + [_P, _P, _P, ctypes.c_int64, _P, _P,
+                                                                              ctypes.c_int64],
     "se_last_error": [],
     "se_version": [],
 }

@@ -120,6 +120,59 @@ def gather(field: GridField, system: ParticleSystem, wspec: windows.WindowSpec,
     return phi
 
 
+def _window_table(wspec: windows.WindowSpec, k) -> np.ndarray:
+    """Window transform on a mode set with the underflow guard (sekspace.py:181-185)."""
+    vals = np.ascontiguousarray(windows.fourier(k, wspec), dtype=np.float64)
+    if vals.size and np.min(np.abs(vals)) < 1e-30:
+        raise AssertionError("window transform underflow: P/M misconfigured")
+    return vals
+
+
+def scale(F, xi: float, wspec: windows.WindowSpec, gspec, grid: Grid, periodicity: Periodicity):
+    """Multiply every retained mode by 4 pi e^{-k^2/4 xi^2} G_hat / w_hat^2
+    (sekspace.py:192-254), on the device (se_scale_blocks_host); returns a
+    new SpectralField."""
+    from . import aft
+
+    D, h = periodicity.D, grid.h
+
+    def tab(n):
+        k = np.ascontiguousarray(mode_values(n, h))
+        return k, _window_table(wspec, k)
+
+    def c(a):
+        return np.array(a, dtype=np.complex128, order="C", copy=True)
+
+    kp, wp = tab(grid.M)
+    R = float(getattr(gspec, "R", 0.0))
+    args = dict(full=None, zero=None, Iblk=None, Jblk=None)
+    if D == 3:
+        cube = c(F.full)
+        _native.call("se_scale_blocks_host", 0, 3, grid.M, grid.Mt, F.g0, F.gs, float(xi), R,
+                     _native.ptr(kp), _native.ptr(wp), None, None, None, None, None, None,
+                     _native.ptr(cube), None, None, 0, None, None, 0)
+        args["full"] = cube
+        return aft.SpectralField(D, F.M, F.Mt, F.g0, F.gs, **args)
+    k0, w0 = tab(F.g0)
+    zero = c(F.zero)
+    if D == 0:
+        _native.call("se_scale_blocks_host", 0, 0, grid.M, grid.Mt, F.g0, F.gs, float(xi), R,
+                     _native.ptr(kp), _native.ptr(wp), _native.ptr(k0), _native.ptr(w0), None, None, None, None,
+                     _native.ptr(zero), None, None, 0, None, None, 0)
+        return aft.SpectralField(D, F.M, F.Mt, F.g0, F.gs, zero=zero)
+    ks, ws = tab(F.gs)
+    kt, wt = tab(F.Mt)
+    Ib, Jb = c(F.Iblk), c(F.Jblk)
+    Ii = np.ascontiguousarray(F.I_idx, dtype=np.int32)
+    Ji = np.ascontiguousarray(F.J_idx, dtype=np.int32)
+    _native.call("se_scale_blocks_host", 0, D, grid.M, F.Mt, F.g0, F.gs, float(xi), R,
+                 _native.ptr(kp), _native.ptr(wp), _native.ptr(k0), _native.ptr(w0), _native.ptr(ks),
+                 _native.ptr(ws), _native.ptr(kt), _native.ptr(wt), _native.ptr(zero),
+                 _native.ptr(Ib) if Ib.size else None, _native.ptr(Ii) if Ii.size else None, len(Ii),
+                 _native.ptr(Jb) if Jb.size else None, _native.ptr(Ji) if Ji.size else None, len(Ji))
+    return aft.SpectralField(D, F.M, F.Mt, F.g0, F.gs, zero=zero, Iblk=Ib, Jblk=Jb, I_idx=F.I_idx, J_idx=F.J_idx)
+
+
 def apply_kspace(field: GridField, params: SEParams, periodicity: Periodicity,
                  use_kernel: bool | None = None) -> GridField:
     """H -> H~: aft_forward, scale, aft_inverse, real part (sekspace.py:366-381),
