@@ -64,18 +64,19 @@ class NativeBackend:
 def total_potential_sharded(pos, q, backend, group=None):
     """core.total_potential across the ranks of `group`; returns the full phi
     on every rank.  pos (N,3) / q (N,) are this rank's replicated inputs."""
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    init = dist.is_initialized()
+    rank = dist.get_rank(group) if init else 0
+    world = dist.get_world_size(group) if init else 1
     N = q.shape[0]
     grid = backend.empty_grid()
     backend.spread_shard(pos, q, rank, world, grid)
-    if world > 1:
+    if init:
         dist.all_reduce(grid, op=dist.ReduceOp.SUM, group=group)
     backend.kspace_apply(grid)
     phi = backend.empty_phi(N)
     backend.realspace_shard(pos, q, rank, world, phi)
     backend.gather_shard(grid, pos, rank, world, phi)
-    if world > 1:
+    if init:
         dist.all_reduce(phi, op=dist.ReduceOp.SUM, group=group)
     return phi
 

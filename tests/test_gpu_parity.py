@@ -382,3 +382,28 @@ def test_baseline_config_full_size(name):
     gk = se.se_kspace(se.ParticleSystem(pos[sub], qs, L), p, peri)
     rk = orc.se_kspace(pos[sub], qs, L, D, dict(p.__dict__))
     assert se.relative_rms_error(gk, rk) < 1e-11
+
+
+def test_sharded_pipeline_nccl_single_rank():
+    # the torch.distributed orchestration with a real NCCL communicator (1 rank)
+    import socket
+
+    import torch.distributed as dist
+    from paper_1712_04732_b200.distributed import NativeBackend, total_potential_sharded
+
+    s = rand_system(4000, 1.0, 43)
+    p = se.SEParams(xi=8.0, rc=0.4, M=24, P=8, window="bm", shape=20.0, eps=1e-8)
+    full = se.total_potential(s, p, se.Periodicity(3))
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        dev = torch.device("cuda", 0)
+        pos = torch.from_numpy(s.positions).to(dev)
+        q = torch.from_numpy(s.charges).to(dev)
+        phi = total_potential_sharded(pos, q, NativeBackend(s.L, p, se.Periodicity(3), dev))
+        assert se.relative_rms_error(phi.cpu().numpy(), full) < 1e-13
+    finally:
+        dist.destroy_process_group()
