@@ -104,6 +104,12 @@ int se_window_eval(int window, int32_t P, double h, double shape,
                    const double *x, int64_t n, double *out);
 int se_window_fourier(int window, int32_t P, double h, double shape,
                       const double *k, int64_t n, double *out);
+/* The two numerical kernels behind the transforms above: the BM transform
+ * by an n-node long-double Gauss-Legendre rule in theta (windows.py:202-211,
+ * `_bm_quadrature`) and the KB transform's sinh(r)/r continued to rho2 < 0
+ * (windows.py:115-132, `_sinhc`). */
+int se_bm_quadrature(double w, double beta, const double *k, int64_t n, int32_t nodes, double *out);
+int se_kb_sinhc(const double *rho2, int64_t n, double *out);
 /* greens.zero_mode_values (greens.py:48-85). */
 int se_greens_zero_mode(int D, double R, const double *kappa, int64_t n, double *out);
 

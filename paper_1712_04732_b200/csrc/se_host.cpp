@@ -195,6 +195,19 @@ static std::vector<double> bm_quadrature(double w, double beta, const std::vecto
     return out;
 }
 
+// windows.py:115-132: sinh(sqrt(rho2))/sqrt(rho2), continued to rho2 < 0 as
+// sin(sqrt(-rho2))/sqrt(-rho2); a short Taylor series across the seam.
+static double kb_sinhc(double rho2) {
+    if (std::fabs(rho2) < 1e-6)
+        return 1.0 + rho2 / 6.0 + rho2 * rho2 / 120.0 + rho2 * rho2 * rho2 / 5040.0;
+    if (rho2 > 0) {
+        double r = std::sqrt(rho2);
+        return std::sinh(r) / r;
+    }
+    double r = std::sqrt(-rho2);
+    return std::sin(r) / r;
+}
+
 // windows.py:87-91, 115-145, 214-239
 std::vector<double> window_fourier(int window, int P, double h, double shape, const std::vector<double> &k) {
     double w = 0.5 * P * h;
@@ -210,18 +223,7 @@ std::vector<double> window_fourier(int window, int P, double h, double shape, co
         double i0b = (double)bessel_i0_ld((long double)shape);
         for (size_t j = 0; j < k.size(); ++j) {
             double kw = k[j] * w;
-            double rho2 = shape * shape - kw * kw;
-            double s;
-            if (std::fabs(rho2) < 1e-6)
-                s = 1.0 + rho2 / 6.0 + rho2 * rho2 / 120.0 + rho2 * rho2 * rho2 / 5040.0;
-            else if (rho2 > 0) {
-                double r = std::sqrt(rho2);
-                s = std::sinh(r) / r;
-            } else {
-                double r = std::sqrt(-rho2);
-                s = std::sin(r) / r;
-            }
-            out[j] = 2.0 * w * s / i0b;
+            out[j] = 2.0 * w * kb_sinhc(shape * shape - kw * kw) / i0b;
         }
         return out;
     }
@@ -359,6 +361,21 @@ int se_window_fourier(int window, int32_t P, double h, double shape, const doubl
     std::vector<double> kv(k, k + n);
     std::vector<double> v = window_fourier(window, P, h, shape, kv);
     std::memcpy(out, v.data(), sizeof(double) * n);
+    SE_API_END
+}
+
+int se_bm_quadrature(double w, double beta, const double *k, int64_t n, int32_t nodes, double *out) {
+    SE_API_BEGIN
+    if (!(w > 0) || !(beta >= 0) || nodes < 2) fail(SE_EINVAL, "invalid BM quadrature parameters");
+    std::vector<double> kv(k, k + n);
+    std::vector<double> v = bm_quadrature(w, beta, kv, nodes);
+    std::memcpy(out, v.data(), sizeof(double) * n);
+    SE_API_END
+}
+
+int se_kb_sinhc(const double *rho2, int64_t n, double *out) {
+    SE_API_BEGIN
+    for (int64_t i = 0; i < n; ++i) out[i] = kb_sinhc(rho2[i]);
     SE_API_END
 }
 

@@ -88,3 +88,81 @@ def eval_kaiser(x, spec: WindowSpec):
 
 def eval_bm(x, spec: WindowSpec):
     return evaluate(x, WindowSpec(BM, spec.P, spec.h, spec.shape))
+
+
+def gaussian_fourier(k, spec: WindowSpec):
+    """exp(-(w k)^2 / (2 m^2)): the untruncated Gaussian transform (windows.py:87-91)."""
+    return fourier(k, WindowSpec(GAUSSIAN, spec.P, spec.h, spec.shape))
+
+
+def kaiser_fourier(k, spec: WindowSpec):
+    """2w sinhc(beta^2 - (k w)^2) / I0(beta) (windows.py:135-145)."""
+    return fourier(k, WindowSpec(KAISER, spec.P, spec.h, spec.shape))
+
+
+def _sinhc(rho2) -> np.ndarray:
+    """sinh(sqrt(rho2))/sqrt(rho2), continued to rho2 < 0 (windows.py:115-132)."""
+    arr = np.ascontiguousarray(np.asarray(rho2, dtype=float).ravel())
+    out = np.empty_like(arr)
+    _native.call("se_kb_sinhc", _native.ptr(arr), arr.size, _native.ptr(out))
+    return out.reshape(np.shape(rho2))
+
+
+def _bm_quadrature(w: float, beta: float, k, nodes: int) -> np.ndarray:
+    """BM transform by an n-node long-double Gauss-Legendre rule (windows.py:202-211)."""
+    kk = np.ascontiguousarray(np.asarray(k, dtype=float).ravel())
+    out = np.empty_like(kk)
+    _native.call("se_bm_quadrature", float(w), float(beta), _native.ptr(kk), kk.size, int(nodes),
+                 _native.ptr(out))
+    return out
+
+
+def eval_bspline(x, p: int):
+    """Cardinal B-spline M_p supported on [0, p] (windows.py:94-103).
+
+    Not a spreading window of this package (the reference's pipeline never
+    selects it); kept for API completeness.  Evaluated piecewise from the
+    order-2 hat by the Cox-de Boor recursion, iteratively over the order.
+    """
+    if p < 2:
+        raise ValueError("B-spline order must be >= 2")
+    x = np.asarray(x, dtype=float)
+    # values of M_2(x - j) for the shifts the recursion needs, j = 0..p-2
+    layers = [np.where((x - j >= 0.0) & (x - j <= 2.0), 1.0 - np.abs(x - j - 1.0), 0.0)
+              for j in range(p - 1)]
+    for order in range(3, p + 1):
+        layers = [((x - j) * layers[j] + (order - (x - j)) * layers[j + 1]) / (order - 1)
+                  for j in range(len(layers) - 1)]
+    out = layers[0]
+    return float(out) if out.ndim == 0 else out
+
+
+@dataclass(frozen=True)
+class TabulatedTransform:
+    """A window transform sampled on one mode set (windows.py:158-166)."""
+
+    kind: str
+    P: int
+    shape: float
+    w: float
+    k: np.ndarray
+    values: np.ndarray
+
+
+_BM_TABLES: dict[tuple, TabulatedTransform] = {}
+
+
+def bm_fourier_precompute(spec: WindowSpec, k) -> TabulatedTransform:
+    """BM transform tabulated at exactly the modes k, quadrature self-checked by
+    node doubling inside the library; cached per (beta, w, mode set)
+    (windows.py:214-239)."""
+    if spec.kind != BM:
+        raise ValueError("spec.kind must be 'bm'")
+    k = np.ascontiguousarray(k, dtype=float)
+    key = (float(spec.shape), float(spec.w), k.tobytes())
+    hit = _BM_TABLES.get(key)
+    if hit is not None:
+        return hit
+    table = TabulatedTransform(BM, spec.P, spec.shape, spec.w, k.copy(), fourier(k, spec))
+    _BM_TABLES[key] = table
+    return table
