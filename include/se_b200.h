@@ -110,6 +110,11 @@ int se_window_fourier(int window, int32_t P, double h, double shape,
  * (windows.py:115-132, `_sinhc`). */
 int se_bm_quadrature(double w, double beta, const double *k, int64_t n, int32_t nodes, double *out);
 int se_kb_sinhc(const double *rho2, int64_t n, double *out);
+/* realspace.build_cell_list (realspace.py:43-59): n^3 cells of edge L/n;
+ * order[bounds[c] .. bounds[c+1]) are the particles of flat cell
+ * c = (cx*n + cy)*n + cz in ascending index order.  order: N, bounds: n^3+1.
+ * Inspection utility; the device kernels bin on their own finer grid. */
+int se_cell_list_host(const double *pos, int64_t N, double L, int32_t n, int64_t *order, int64_t *bounds);
 /* greens.zero_mode_values (greens.py:48-85). */
 int se_greens_zero_mode(int D, double R, const double *kappa, int64_t n, double *out);
 

@@ -56,6 +56,7 @@ SIGNATURES = {
                           ctypes.c_int64, _P],
     "se_bm_quadrature": [ctypes.c_double, ctypes.c_double, _P, ctypes.c_int64, ctypes.c_int32, _P],
     "se_kb_sinhc": [_P, ctypes.c_int64, _P],
+    "se_cell_list_host": [_P, ctypes.c_int64, ctypes.c_double, ctypes.c_int32, _P, _P],
     "se_greens_zero_mode": [ctypes.c_int, ctypes.c_double, _P, ctypes.c_int64, _P],
     "se_plan_create": [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_double, ctypes.POINTER(se_params_t),
                        ctypes.c_int],

@@ -159,6 +159,11 @@ class CuFftEngine:
         return out
 
 
+
+# The reference's default engine (aft.py:24-41) by name.  Its contract is
+# numpy's FFT semantics, which the cuFFT engine above implements.
+NumpyFftEngine = CuFftEngine
+
 _ENGINE = CuFftEngine()
 
 

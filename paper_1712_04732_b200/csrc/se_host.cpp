@@ -373,6 +373,32 @@ int se_bm_quadrature(double w, double beta, const double *k, int64_t n, int32_t 
     SE_API_END
 }
 
+// realspace.py:43-59: bucket particles into n^3 cells of edge L/n, members of
+// each cell in ascending index order (a stable counting sort).
+int se_cell_list_host(const double *pos, int64_t N, double L, int32_t n, int64_t *order, int64_t *bounds) {
+    SE_API_BEGIN
+    if (n < 1 || !(L > 0)) fail(SE_EINVAL, "invalid cell list geometry");
+    const int64_t nc = (int64_t)n * n * n;
+    const double edge = L / n;
+    std::vector<int64_t> cell(N);
+    for (int64_t c = 0; c <= nc; ++c) bounds[c] = 0;
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t f = 0;
+        for (int a = 0; a < 3; ++a) {
+            int64_t c = (int64_t)(pos[3 * i + a] / edge);
+            if (c > n - 1) c = n - 1;
+            if (c < 0) c = 0;
+            f = f * n + c;
+        }
+        cell[i] = f;
+        bounds[f + 1]++;
+    }
+    for (int64_t c = 0; c < nc; ++c) bounds[c + 1] += bounds[c];
+    std::vector<int64_t> fill(bounds, bounds + nc);
+    for (int64_t i = 0; i < N; ++i) order[fill[cell[i]]++] = i;
+    SE_API_END
+}
+
 int se_kb_sinhc(const double *rho2, int64_t n, double *out) {
     SE_API_BEGIN
     for (int64_t i = 0; i < n; ++i) out[i] = kb_sinhc(rho2[i]);

@@ -7,10 +7,45 @@ realspace.py:138-165); self_term runs the library's elementwise kernel.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
 from . import _native
 from .core import ParticleSystem, Periodicity, SEParams
+
+
+@dataclass(frozen=True)
+class CellList:
+    """Particles bucketed into n^3 cells of edge >= rc (realspace.py:24-40);
+    members[flat cell] lists each particle exactly once."""
+
+    ncells: tuple[int, int, int]
+    edge: float
+    members: list[np.ndarray]
+    periodic_mask: tuple[bool, bool, bool]
+    rc: float
+
+    def flat(self, cx: int, cy: int, cz: int) -> int:
+        nx, ny, nz = self.ncells
+        return (cx * ny + cy) * nz + cz
+
+
+def build_cell_list(system: ParticleSystem, rc: float, periodicity: Periodicity) -> CellList:
+    """Cell list with edge L / floor(L / rc) (realspace.py:43-59), built by the
+    library's counting sort (se_cell_list_host).  An inspection utility: the
+    device real-space kernel bins on its own rc/2 grid."""
+    if rc <= 0:
+        raise ValueError("rc must be positive")
+    if periodicity.D >= 1 and rc > system.L / 2 + 1e-12:
+        raise ValueError("cell list requires rc <= L/2 on periodic axes (minimum image)")
+    n = max(1, int(np.floor(system.L / rc)))
+    order = np.empty(system.N, dtype=np.int64)
+    bounds = np.empty(n ** 3 + 1, dtype=np.int64)
+    _native.call("se_cell_list_host", _native.ptr(system.positions), system.N, float(system.L), n,
+                 _native.ptr(order), _native.ptr(bounds))
+    members = [order[bounds[c]:bounds[c + 1]] for c in range(n ** 3)]
+    return CellList((n, n, n), system.L / n, members, periodicity.mask, float(rc))
 
 
 def _real_params(xi: float, rc: float) -> SEParams:

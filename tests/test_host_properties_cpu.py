@@ -427,3 +427,31 @@ def test_periodicity_axes():
     assert Periodicity(0).periodic_axes == () and Periodicity(3).free_axes == ()
     with pytest.raises(ValueError):
         Periodicity(4)
+
+
+# --------------------------------------------------------------- cell list / engine
+
+def test_cell_list_buckets_every_particle_once():
+    from paper_1712_04732_b200 import realspace
+    s = se.generate_random_system(300, 2.0, seed=11)
+    cl = realspace.build_cell_list(s, 0.35, Periodicity(3))
+    n = cl.ncells[0]
+    assert n == 5 and cl.edge >= cl.rc and cl.periodic_mask == (True, True, True)
+    seen = np.sort(np.concatenate([m for m in cl.members if m.size]))
+    assert np.array_equal(seen, np.arange(300))
+    for c, m in enumerate(cl.members):
+        assert np.all(np.diff(m) > 0)
+        for i in m:
+            idx = np.minimum((s.positions[i] / cl.edge).astype(int), n - 1)
+            assert cl.flat(*idx) == c
+    one = se.ParticleSystem(np.array([[0.5, 0.5, 0.5]]), np.array([1.0]), 1.0)
+    occ = [m for m in realspace.build_cell_list(one, 0.3, Periodicity(0)).members if m.size]
+    assert len(occ) == 1 and occ[0].tolist() == [0]
+    with pytest.raises(ValueError):
+        realspace.build_cell_list(s, 1.01, Periodicity(1))
+    assert realspace.build_cell_list(s, 1.5, Periodicity(0)).ncells == (1, 1, 1)
+
+
+def test_reference_engine_name_is_available():
+    from paper_1712_04732_b200 import aft
+    assert hasattr(aft.NumpyFftEngine(), "rfftn") and hasattr(aft.NumpyFftEngine(), "irfftn")
