@@ -61,50 +61,64 @@ __global__ void cell_keys_kernel(const double *__restrict__ pos, int64_t N, Real
 }
 
 // erfc(x), x >= 0, as exp(-x^2) erfcx(x): erfcx by a degree-17 polynomial in
-// s = A t + B, t = (x - K)/(x + K), and exp by Cody-Waite reduction with the
-// x^2 rounding residual folded in; coefficients are __constant__ operands
-// (tools/gen_erfc_coeffs.py; max relative error 4e-15 on [0, 6], the same
-// as scipy's erfc).  Beyond SE_ERFC_XMAX the library erfc is used.
-// 1/d and 1/sqrt(d) from the MUFU approximations plus two Newton steps,
-// branch-free (d is a positive normal number here; error ~1 ulp).
+// s = A t + B, t = (x - K)/(x + K), and exp by Cody-Waite reduction;
+// coefficients are __constant__ operands (tools/gen_erfc_coeffs.py; max
+// relative error of the polynomial 4e-15 on [0, 6]).  The x^2 rounding
+// residual is not carried: it moves exp(-x^2) by <= x^2 2^-53 relative,
+// i.e. <= 4e-17 absolute, below the 1/r rounding of the pair term.
+// Beyond SE_ERFC_XMAX the library erfc is used.
+//
+// 1/d and 1/sqrt(d): the MUFU approximations (~2^-22 relative) and one
+// third-order correction each (error O(e^3): ~1 ulp), branch-free; d is a
+// positive normal number here.
 __device__ __forceinline__ double rcp_nr(double d) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-    double e = fma(-d, y, 1.0);
-    y = fma(y, e, y);
-    e = fma(-d, y, 1.0);
-    return fma(y, e, y);
+    const double e = fma(-d, y, 1.0);  // 1/d = y / (1 - e) = y (1 + e + e^2 + ...)
+    return fma(y, fma(e, e, e), y);
 }
 __device__ __forceinline__ double rsqrt_nr(double d) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-    double hy = 0.5 * y;
-    double e = fma(-d * y, y, 1.0);
-    y = fma(hy, e, y);
-    hy = 0.5 * y;
-    e = fma(-d * y, y, 1.0);
-    return fma(hy, e, y);
+    const double e = fma(-d * y, y, 1.0);  // d^-1/2 = y (1 - e)^-1/2 = y (1 + e/2 + 3e^2/8 + ...)
+    return fma(y, e * fma(e, 0.375, 0.5), y);
 }
 
-__device__ __forceinline__ double erfc_fast(double x) {
-    if (x > SE_ERFC_XMAX) return erfc(x);
-    const double t = (x - SE_ERFC_K) * rcp_nr(x + SE_ERFC_K);
-    const double s = fma(t, SE_ERFC_A, SE_ERFC_B);
+// Scalar constants of erfc_fast as one constant-bank block (read two per
+// LDCU.128 instead of materialised as 64-bit immediates per use).
+__constant__ double se_erfc_k[6] = {
+    SE_ERFC_A + SE_ERFC_B,                // s = ((A+B) x + K (B-A)) / (x + K)
+    SE_ERFC_K * (SE_ERFC_B - SE_ERFC_A),  //
+    SE_ERFC_K,                            //
+    -SE_LOG2E,                            // n = rint(-x^2 log2 e)
+    -SE_LN2_HI,                           // r = -x^2 - n ln2 (Cody-Waite)
+    -SE_LN2_LO};
+
+// erfc(x) * w.  WIDE: x may exceed SE_ERFC_XMAX (xi rc > 6, i.e. eps < 2e-16).
+// Otherwise the caller guarantees x <= SE_ERFC_XMAX (1 + 1e-4) for every
+// evaluated pair (beyond the cutoff the result is multiplied by w = 0), and
+// the code is branch-free so that two evaluations form one basic block the
+// scheduler can interleave.
+template <bool WIDE>
+__device__ __forceinline__ double erfc_fast(double x, double w) {
+    if (WIDE) {
+        if (x > SE_ERFC_XMAX) return erfc(x) * w;
+    }
+    const double s = fma(x, se_erfc_k[0], se_erfc_k[1]) * rcp_nr(x + se_erfc_k[2]);
     // Horner (Estrin's shorter chains measured slower: the kernel is
-    // fp64-issue bound, not latency bound)
+    // issue bound)
     double p = se_erfcx_c[SE_ERFC_NE];
 #pragma unroll
     for (int i = SE_ERFC_NE - 1; i >= 0; --i) p = fma(p, s, se_erfcx_c[i]);
     const double u = x * x;
-    const double ul = fma(x, x, -u);
-    const double n = rint(u * -SE_LOG2E);
-    double r = fma(n, -SE_LN2_HI, -u);
-    r = fma(n, -SE_LN2_LO, r) - ul;
+    const double n = rint(u * se_erfc_k[3]);
+    const double r = fma(n, se_erfc_k[5], fma(n, se_erfc_k[4], -u));
     double e = se_exp_c[SE_EXP_NX];
 #pragma unroll
     for (int i = SE_EXP_NX - 1; i >= 0; --i) e = fma(e, r, se_exp_c[i]);
-    const double scale = __hiloint2double(((int)n + 1023) << 20, 0);
-    return p * (e * scale);
+    // e * 2^n by an exponent add (n in [-27, 0]: e 2^n stays normal)
+    e = __hiloint2double(__double2hiint(e) + (int)n * (1 << 20), __double2loint(e));
+    return p * (e * w);
 }
 
 __device__ __forceinline__ double min_image(double d, double L) { return d - L * rint(d / L); }
@@ -116,9 +130,9 @@ constexpr int kT = 16;     // targets per warp unit: lane l tests target l % 16 
 // Shared-memory workspace of one warp unit (7 KB: 8 blocks x 4 warps per SM).
 struct __align__(16) WarpBuf {
     double4 tst[kT];             // the unit's targets (x, y, z, q)
-    double4 sst[32];             // current source batch, image shift applied
+    double sx[32], sy[32], sz[32], sq[32];  // current source batch (SoA: hits read random k)
     float4 sf[32];               // the same in fp32 for the prefilter
-    double acc[32][kT];          // per-lane private accumulators, acc[lane][(t + lane) % kT]
+    double acc[kT][32];          // per-lane private accumulators acc[t][lane]: lane-owned banks
     unsigned short ent[kT * 32];  // compacted hits of a batch: (target << 5) | source
 };
 
@@ -133,15 +147,22 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 // Exact fp64 evaluation of one compacted hit (target tt, source k of the
 // batch): d = x_t - (x_s + shift) (realspace.py:113-117), the coincidence
 // check (r < 1e-14, realspace.py:118-122), r < rc, and f = erfc(xi r)/r with
-// 1/r = rsqrt(r^2).  Target side into the lane's private row; with NEWTON
-// the source side q_t f goes to the source's global accumulator (REDG).
-template <bool MI, bool COUNT, bool NEWTON>
-__device__ __forceinline__ void eval_hit(unsigned en, const RealArgs &a, WarpBuf &wb, int lane, int jb, int tbase,
-                                         double *__restrict__ acc_src, int &singular, long long &cnt) {
-    const int tt = (int)(en >> 5), k = (int)(en & 31u);
-    const double4 tp = wb.tst[tt];
-    const double4 sp = wb.sst[k];
-    double dx = tp.x - sp.x, dy = tp.y - sp.y, dz = tp.z - sp.z;
+// 1/r = rsqrt(r^2).  Branch-free; the caller applies the result.
+struct Hit {
+    double f;   // erfc(xi r)/r, 0 outside the cutoff
+    double qt;  // target charge (source-side update with NEWTON)
+    int tt, k;
+    bool ok;
+};
+
+template <bool MI, bool NEWTON, bool WIDE>
+__device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const WarpBuf &wb, int jb, int tbase,
+                                        int &singular) {
+    Hit h;
+    h.tt = (int)(en >> 5);
+    h.k = (int)(en & 31u);
+    const double4 tp = wb.tst[h.tt];
+    double dx = tp.x - wb.sx[h.k], dy = tp.y - wb.sy[h.k], dz = tp.z - wb.sz[h.k];
     if (MI) {
         if (a.mode[0] == 2) dx = min_image(dx, a.L);
         if (a.mode[1] == 2) dy = min_image(dy, a.L);
@@ -152,20 +173,26 @@ __device__ __forceinline__ void eval_hit(unsigned en, const RealArgs &a, WarpBuf
     const bool zero = r2 < 1e-28;
     if (NEWTON)
         singular |= zero ? 1 : 0;
-    else if (zero && jb + k != tbase + tt)
-        singular = 1;
-    const double r2s = zero ? 1.0 : r2;
+    else
+        singular |= (zero && jb + h.k != tbase + h.tt) ? 1 : 0;
+    // a coincident pair is evaluated at r = rc (keeps x in range) and dropped
+    const double r2s = zero ? a.rc2 : r2;
     const double rinv = rsqrt_nr(r2s);
     const double rr = r2s * rinv;
-    const bool ok = !zero && rr < a.rc;
-    if (COUNT) {
-        cnt += ok ? (NEWTON ? 2 : 1) : 0;
-        return;
-    }
-    const double f = ok ? erfc_fast(a.xi * rr) * rinv : 0.0;
-    double *slot = &wb.acc[lane][(tt + lane) & (kT - 1)];
-    *slot = fma(sp.w, f, *slot);
-    if (NEWTON && ok) atomicAdd(acc_src + jb + k, tp.w * f);
+    h.ok = !zero && rr < a.rc;
+    // evaluated unconditionally (a select, not a branch, on ok)
+    h.f = erfc_fast<WIDE>(a.xi * rr, h.ok ? rinv : 0.0);
+    h.qt = tp.w;
+    return h;
+}
+
+// Target side into the lane's private slot; with NEWTON the source side
+// q_t f goes to the source's global accumulator (REDG).
+template <bool NEWTON>
+__device__ __forceinline__ void apply_hit(const Hit &h, WarpBuf &wb, int lane, int jb, double *__restrict__ acc_src) {
+    double *slot = &wb.acc[h.tt][lane];
+    *slot = fma(wb.sq[h.k], h.f, *slot);
+    if (NEWTON && h.ok) atomicAdd(acc_src + jb + h.k, h.qt * h.f);
 }
 
 // One batch of <= 32 candidate sources [jb, jb+m) of a neighbour-cell run:
@@ -177,7 +204,7 @@ __device__ __forceinline__ void eval_hit(unsigned en, const RealArgs &a, WarpBuf
 //  2. warp prefix scan of the hit counts and compaction of the hits into a
 //     target-major list;
 //  3. the list is evaluated 64 hits at a time (two per lane) on full warps.
-template <bool MI, bool COUNT, bool NEWTON>
+template <bool MI, bool COUNT, bool NEWTON, bool WIDE>
 __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int jb, int j1, double shx, double shy,
                                            double shz, const RealArgs &a, WarpBuf &wb, int lane, bool active,
                                            const float4 tq, const double3 org, int t, int tbase, int hs,
@@ -186,7 +213,10 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     if (j < j1) {
         const double4 r = rec[j];
         const double xs = r.x + shx, ys = r.y + shy, zs = r.z + shz;
-        wb.sst[lane] = make_double4(xs, ys, zs, r.w);
+        wb.sx[lane] = xs;
+        wb.sy[lane] = ys;
+        wb.sz[lane] = zs;
+        wb.sq[lane] = r.w;
         if (MI) {
             wb.sf[lane] = make_float4((float)xs, (float)ys, (float)zs, 0.f);
         } else {
@@ -245,9 +275,30 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     }
     __syncwarp();
     for (int e0 = 0; e0 < total; e0 += 64) {
-        const int e1 = e0 + lane, e2 = e0 + 32 + lane;
-        if (e1 < total) eval_hit<MI, COUNT, NEWTON>(wb.ent[e1], a, wb, lane, jb, tbase, acc_src, singular, cnt);
-        if (e2 < total) eval_hit<MI, COUNT, NEWTON>(wb.ent[e2], a, wb, lane, jb, tbase, acc_src, singular, cnt);
+        const int rem = total - e0;
+        if (rem > 32) {
+            // two hits per lane in one basic block (the second one a masked
+            // duplicate of the first on lanes past the end of the list)
+            const bool v2 = lane < rem - 32;
+            const unsigned en1 = wb.ent[e0 + lane];
+            const unsigned en2 = v2 ? wb.ent[e0 + 32 + lane] : en1;
+            Hit h1 = eval_hit<MI, NEWTON, WIDE>(en1, a, wb, jb, tbase, singular);
+            Hit h2 = eval_hit<MI, NEWTON, WIDE>(en2, a, wb, jb, tbase, singular);
+            h2.ok = h2.ok && v2;
+            h2.f = v2 ? h2.f : 0.0;
+            if (COUNT) {
+                cnt += (h1.ok ? (NEWTON ? 2 : 1) : 0) + (h2.ok ? (NEWTON ? 2 : 1) : 0);
+            } else {
+                apply_hit<NEWTON>(h1, wb, lane, jb, acc_src);
+                apply_hit<NEWTON>(h2, wb, lane, jb, acc_src);
+            }
+        } else if (lane < rem) {
+            const Hit h = eval_hit<MI, NEWTON, WIDE>(wb.ent[e0 + lane], a, wb, jb, tbase, singular);
+            if (COUNT)
+                cnt += h.ok ? (NEWTON ? 2 : 1) : 0;
+            else
+                apply_hit<NEWTON>(h, wb, lane, jb, acc_src);
+        }
     }
     __syncwarp();
 }
@@ -257,7 +308,7 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
 // partial sums of both sides go to acc_src (sorted order, zeroed before) and
 // a finishing kernel scatters them.  Otherwise the full 5x5x5 neighbourhood
 // and direct writes of phi (minimum-image mode for < 5 cells per axis).
-template <bool MI, bool COUNT, bool NEWTON>
+template <bool MI, bool COUNT, bool NEWTON, bool WIDE>
 __global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
     const double4 *__restrict__ rec, const int *__restrict__ sidx, const int *__restrict__ starts,
     const int4 *__restrict__ units, const int *__restrict__ nunits, RealArgs a, double *__restrict__ phi,
@@ -277,7 +328,7 @@ __global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
     if (__ballot_sync(0xffffffffu, active) == 0) return;
     const double4 tp = active ? rec[t] : make_double4(0, 0, 0, 0);
     if (lane < kT) wb.tst[lane] = tp;
-    for (int i = 0; i < kT; ++i) wb.acc[lane][i] = 0.0;
+    for (int i = 0; i < kT; ++i) wb.acc[i][lane] = 0.0;
     // prefilter operands: MI -> absolute fp32 position; otherwise -2 t' and
     // |t'|^2 with t' relative to the cell corner
     const double3 org = make_double3(cx * a.edge, cy * a.edge, cz * a.edge);
@@ -312,7 +363,7 @@ __global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
     if (NEWTON) xlo = cx;  // ox >= 0
     auto run = [&](int j0, int j1, double shx, double shy, double shz, int hs) {
         for (int jb = j0; jb < j1; jb += 32)
-            pair_batch<MI, COUNT, NEWTON>(rec, jb, j1, shx, shy, shz, a, wb, lane, active, tq, org, t, un.y, hs,
+            pair_batch<MI, COUNT, NEWTON, WIDE>(rec, jb, j1, shx, shy, shz, a, wb, lane, active, tq, org, t, un.y, hs,
                                           acc_src, singular, cnt);
     };
     for (int ox = xlo; ox <= xhi; ++ox) {
@@ -355,7 +406,7 @@ __global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
     __syncwarp();
     if (active && lane < kT) {
         double v = 0.0;
-        for (int i = 0; i < 32; ++i) v += wb.acc[i][(tl + i) & (kT - 1)];
+        for (int i = 0; i < 32; ++i) v += wb.acc[tl][(tl + i) & 31];
         if (NEWTON) {
             atomicAdd(acc_src + t, v);
         } else {
@@ -468,10 +519,12 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
                                                 pl->cbin.nunits.as<int>(), a, phi, acc, pl->flag.as<int>(), npairs);
     };
     if (!COUNT) prof_begin(pl, SE_K_REALSPACE);
+    // narrow kernels: x = xi r <= xi rc (1 + 2e-5) for every prefiltered pair
+    const bool wide = a.xi * a.rc * (1.0 + 1e-4) > SE_ERFC_XMAX;
     if (mi)
-        args(realspace_cell_kernel<true, COUNT, false>);
+        args(wide ? realspace_cell_kernel<true, COUNT, false, true> : realspace_cell_kernel<true, COUNT, false, false>);
     else
-        args(realspace_cell_kernel<false, COUNT, true>);
+        args(wide ? realspace_cell_kernel<false, COUNT, true, true> : realspace_cell_kernel<false, COUNT, true, false>);
     SE_LAUNCH_CHECK();
     pl->launches += 1;
     if (!mi && !COUNT) {

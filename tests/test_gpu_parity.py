@@ -239,6 +239,34 @@ def test_two_particle_single_term_and_cutoff():
     assert np.all(se.real_space_sum(far, 5.0, rc, se.Periodicity(0)) == 0.0)
 
 
+@pytest.mark.parametrize("xi,rc", [(4.2919, 1.0), (12.0, 0.45)])
+def test_isolated_pairs_sweep_pair_kernel(xi, rc):
+    # K isolated +-1 pairs at separations spanning (0, rc): each potential is
+    # one kernel term q erfc(xi r)/r, checked against 30-digit values.  The
+    # bound is on the absolute error of erfc (the pair term carries the 1/r
+    # rounding anyway): 4 ulp of 1/r.
+    import mpmath as mp
+    mp.mp.dps = 30
+    K = 400
+    d = np.linspace(1e-3, 0.999, K) * rc
+    d[-1] = rc * (1 - 1e-9)
+    L = 4.0 * rc * K ** (1 / 3) + 10 * rc
+    g = int(np.ceil(K ** (1 / 3)))
+    ij = np.array([(i, j, k) for i in range(g) for j in range(g) for k in range(g)][:K], dtype=float)
+    base = 2.0 * rc + ij * 3.0 * rc
+    pos = np.concatenate([base, base + np.stack([d, np.zeros(K), np.zeros(K)], 1)])
+    q = np.concatenate([np.ones(K), -np.ones(K)])
+    s = se.ParticleSystem(pos, q, L)
+    phi = se.real_space_sum(s, xi, rc, se.Periodicity(0))
+    r = np.linalg.norm(pos[K:] - pos[:K], axis=1)
+    want = np.array([float(mp.erfc(mp.mpf(xi) * mp.mpf(v)) / mp.mpf(v)) for v in r])
+    err = np.abs(-phi[:K] - want) * r
+    assert np.max(err) < 4.5e-16, np.max(err)
+    assert np.max(np.abs(phi[K:] - want) * r) < 4.5e-16
+    rel = np.abs(-phi[:K] - want) / want
+    assert np.max(rel) < 1e-12
+
+
 def test_threads_argument_and_determinism():
     s = rand_system(4000, 1.0, 8)
     p = se.SEParams(xi=8.0, rc=0.4, M=32, P=8, window="bm", shape=20.0, eps=1e-8)
