@@ -60,10 +60,11 @@ __global__ void cell_keys_kernel(const double *__restrict__ pos, int64_t N, Real
     atomicAdd(&counts[key], 1);
 }
 
-// erfc(x), x >= 0, as exp(-x^2) erfcx(x): erfcx by a degree-17 polynomial in
+// erfc(x), x >= 0, as exp(-x^2) erfcx(x): erfcx by a degree-14 polynomial in
 // s = A t + B, t = (x - K)/(x + K), and exp by Cody-Waite reduction;
-// coefficients are __constant__ operands (tools/gen_erfc_coeffs.py; max
-// relative error of the polynomial 4e-15 on [0, 6]).  The x^2 rounding
+// coefficients are __constant__ operands (tools/gen_erfc_coeffs.py: fitted
+// for absolute accuracy, max error 7.6e-17 absolute / 7.6e-10 relative on
+// [0, 6] -- the pair term's 1/r rounding is ~1e-16 relative).  The x^2 rounding
 // residual is not carried: it moves exp(-x^2) by <= x^2 2^-53 relative,
 // i.e. <= 4e-17 absolute, below the 1/r rounding of the pair term.
 // Beyond SE_ERFC_XMAX the library erfc is used.
@@ -129,7 +130,7 @@ constexpr int kT = 16;     // targets per warp unit: lane l tests target l % 16 
 
 // Shared-memory workspace of one warp unit (7 KB: 8 blocks x 4 warps per SM).
 struct __align__(16) WarpBuf {
-    double4 tst[kT];             // the unit's targets (x, y, z, q)
+    double tx[kT], ty[kT], tz[kT], tq[kT];  // the unit's targets (SoA)
     double sx[32], sy[32], sz[32], sq[32];  // current source batch (SoA: hits read random k)
     float4 sf[32];               // the same in fp32 for the prefilter
     double acc[kT][32];          // per-lane private accumulators acc[t][lane]: lane-owned banks
@@ -161,8 +162,7 @@ __device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const Wa
     Hit h;
     h.tt = (int)(en >> 5);
     h.k = (int)(en & 31u);
-    const double4 tp = wb.tst[h.tt];
-    double dx = tp.x - wb.sx[h.k], dy = tp.y - wb.sy[h.k], dz = tp.z - wb.sz[h.k];
+    double dx = wb.tx[h.tt] - wb.sx[h.k], dy = wb.ty[h.tt] - wb.sy[h.k], dz = wb.tz[h.tt] - wb.sz[h.k];
     if (MI) {
         if (a.mode[0] == 2) dx = min_image(dx, a.L);
         if (a.mode[1] == 2) dy = min_image(dy, a.L);
@@ -182,7 +182,7 @@ __device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const Wa
     h.ok = !zero && rr < a.rc;
     // evaluated unconditionally (a select, not a branch, on ok)
     h.f = erfc_fast<WIDE>(a.xi * rr, h.ok ? rinv : 0.0);
-    h.qt = tp.w;
+    h.qt = wb.tq[h.tt];
     return h;
 }
 
@@ -195,19 +195,48 @@ __device__ __forceinline__ void apply_hit(const Hit &h, WarpBuf &wb, int lane, i
     if (NEWTON && h.ok) atomicAdd(acc_src + jb + h.k, h.qt * h.f);
 }
 
+// Packed fp32x2 arithmetic (FFMA2 / FADD2, sm_100): two prefilter tests per
+// instruction, the scalar source operand broadcast to both lanes of the pair.
+__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2fma(unsigned long long a, float b, unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(f2pack(b, b)), "l"(c));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2add(unsigned long long a, float b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(f2pack(b, b)));
+    return r;
+}
+
+// Prefilter operands of one lane: targets pa = lane % 8 and pa + 8 of the
+// unit (lo / hi halves of the packed pairs), sources 8 (lane / 8) .. + 7 of
+// each batch.  Outside minimum-image mode: (-2 t'x, -2 t'y, -2 t'z,
+// |t'|^2 - bound) with t' relative to the unit's cell corner; in it the
+// absolute fp32 positions.  An absent target never passes.
+struct PreTargets {
+    unsigned long long x, y, z, w;
+    int ta, tb;  // unit-relative target slots (pa, pa + 8)
+};
+
 // One batch of <= 32 candidate sources [jb, jb+m) of a neighbour-cell run:
-//  1. fp32 prefilter of all 16 x m (target, source) pairs -> per-lane hit
-//     mask.  Outside minimum-image mode the test is
-//     |t'|^2 + |s'|^2 - 2 t'.s' < bound with t', s' relative to the unit's
-//     cell corner (4 fp32 ops per pair); the bound covers the fp32 rounding.
-//     With NEWTON, sources of the target's own cell count only if j > t;
-//  2. warp prefix scan of the hit counts and compaction of the hits into a
-//     target-major list;
+//  1. fp32 prefilter of all 16 x m (target, source) pairs: lane l tests
+//     targets (l % 8, l % 8 + 8) against sources 8 (l / 8) .. + 7, two tests
+//     per packed instruction; hit bit 2 kk + h = (target pa + 8 h, source
+//     8 (l / 8) + kk).  Outside minimum-image mode the test is
+//     |t'|^2 + |s'|^2 - 2 t'.s' - bound < 0 with t', s' relative to the
+//     unit's cell corner; the bound covers the fp32 rounding.  With NEWTON,
+//     sources of the target's own cell count only if j > t;
+//  2. warp prefix scan of the hit counts and compaction of the hits;
 //  3. the list is evaluated 64 hits at a time (two per lane) on full warps.
 template <bool MI, bool COUNT, bool NEWTON, bool WIDE>
 __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int jb, int j1, double shx, double shy,
-                                           double shz, const RealArgs &a, WarpBuf &wb, int lane, bool active,
-                                           const float4 tq, const double3 org, int t, int tbase, int hs,
+                                           double shz, const RealArgs &a, WarpBuf &wb, int lane,
+                                           const PreTargets &pt, const double3 org, int tbase, int hs,
                                            double *__restrict__ acc_src, int &singular, long long &cnt) {
     const int j = jb + lane;
     if (j < j1) {
@@ -226,52 +255,67 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     }
     __syncwarp();
     const int m = min(32, j1 - jb);
+    const int g8 = (lane >> 3) << 3;  // first source of this lane's quarter
     unsigned hit = 0;
-    const int k0 = (lane / kT) * kT;  // this lane's half of the batch
-    if (active) {
-        auto test = [&](int kk) -> bool {
-            const float4 p = wb.sf[k0 + kk];
-            if (MI) {  // tq = absolute fp32 target position
-                float dx = tq.x - p.x, dy = tq.y - p.y, dz = tq.z - p.z;
-                if (a.mode[0] == 2) dx = min_image_f(dx, a.Lf, a.invLf);
-                if (a.mode[1] == 2) dy = min_image_f(dy, a.Lf, a.invLf);
-                if (a.mode[2] == 2) dz = min_image_f(dz, a.Lf, a.invLf);
-                return fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < a.rc2f;
-            }
-            // tq = (-2 t'x, -2 t'y, -2 t'z, |t'|^2)
-            return fmaf(tq.x, p.x, fmaf(tq.y, p.y, fmaf(tq.z, p.z, tq.w + p.w))) < a.rc2r;
+    if (MI) {
+        const float ax = __uint_as_float((unsigned)pt.x), bx = __uint_as_float((unsigned)(pt.x >> 32));
+        const float ay = __uint_as_float((unsigned)pt.y), by = __uint_as_float((unsigned)(pt.y >> 32));
+        const float az = __uint_as_float((unsigned)pt.z), bz = __uint_as_float((unsigned)(pt.z >> 32));
+        const float aw = __uint_as_float((unsigned)pt.w), bw = __uint_as_float((unsigned)(pt.w >> 32));
+        auto test = [&](float tx, float ty, float tz, float tw, const float4 p) -> unsigned {
+            float dx = tx - p.x, dy = ty - p.y, dz = tz - p.z;
+            if (a.mode[0] == 2) dx = min_image_f(dx, a.Lf, a.invLf);
+            if (a.mode[1] == 2) dy = min_image_f(dy, a.Lf, a.invLf);
+            if (a.mode[2] == 2) dz = min_image_f(dz, a.Lf, a.invLf);
+            return fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < a.rc2f + tw ? 1u : 0u;  // tw: 0 or +inf-like
         };
-        if (m == 32) {  // full batch: compile-time bit positions, no bounds test
 #pragma unroll
-            for (int kk = 0; kk < kT; ++kk)
-                if (test(kk)) hit |= 1u << kk;
-        } else {
-            const int mm = m - k0;
-            for (int kk = 0; kk < mm && kk < kT; ++kk)
-                if (test(kk)) hit |= 1u << kk;
+        for (int kk = 0; kk < 8; ++kk) {
+            const float4 p = wb.sf[g8 + kk];
+            hit |= test(ax, ay, az, aw, p) << (2 * kk);
+            hit |= test(bx, by, bz, bw, p) << (2 * kk + 1);
         }
-        hit <<= k0;
-        if (NEWTON && hs >= 0) {
-            // own-cell sources j in [hs, t] are visited from their own unit
-            const int lo = max(hs - jb, 0), hi = t - jb;  // exclude k in [lo, hi]
-            if (hi >= lo && lo < 32) {
-                const unsigned upto = hi >= 31 ? 0xffffffffu : ((2u << hi) - 1u);
-                const unsigned from = lo == 0 ? 0xffffffffu : ~((1u << lo) - 1u);
-                hit &= ~(upto & from);
-            }
+    } else {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const float4 p = wb.sf[g8 + kk];
+            const unsigned long long d = f2fma(pt.x, p.x, f2fma(pt.y, p.y, f2fma(pt.z, p.z, f2add(pt.w, p.w))));
+            // sign bits of the two results -> bits 2 kk (target a), 2 kk + 1 (b)
+            hit |= (((unsigned)d >> 31) | (((unsigned)(d >> 32) >> 30) & 2u)) << (2 * kk);
         }
+    }
+    if (m < 32) {  // sources past the end of the run
+        const int valid = min(max(m - g8, 0), 8);
+        hit &= valid >= 8 ? 0xffffu : ((1u << (2 * valid)) - 1u);
+    }
+    if (NEWTON && hs >= 0) {
+        // own-cell sources j in [hs, t] are visited from their own unit:
+        // exclude source slots k in [lo, t - jb] for each of the two targets
+        const int lo = max(hs - jb, 0) - g8;
+        auto excl = [&](int t) -> unsigned {  // 8-bit mask over this quarter
+            const int hi = t - jb - g8;
+            const int l0 = max(lo, 0), h0 = min(hi, 7);
+            if (h0 < l0) return 0u;
+            return ((2u << h0) - 1u) & ~((1u << l0) - 1u);
+        };
+        auto spread = [](unsigned x) {  // bit i -> bit 2 i
+            x = (x | (x << 4)) & 0x0f0fu;
+            x = (x | (x << 2)) & 0x3333u;
+            return (x | (x << 1)) & 0x5555u;
+        };
+        hit &= ~(spread(excl(tbase + pt.ta)) | (spread(excl(tbase + pt.tb)) << 1));
     }
     const int c = __popc(hit);
     const int incl = warp_incl_scan(c, lane);
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     int pos = incl - c;
     {   // fixed, fully predicated compaction of this lane's <= 16 hit bits
-        const unsigned h16 = hit >> k0;
-        const unsigned tag = ((unsigned)(lane & (kT - 1)) << 5) | (unsigned)k0;
+        unsigned tag;  // pinned in a register (not rematerialised per bit)
+        asm volatile("mov.b32 %0, %1;" : "=r"(tag) : "r"(((unsigned)pt.ta << 5) | (unsigned)g8));
         unsigned short *dst = wb.ent + pos;
 #pragma unroll
-        for (int kk = 0; kk < kT; ++kk)
-            if (h16 & (1u << kk)) *dst++ = (unsigned short)(tag | kk);
+        for (int b = 0; b < 16; ++b)
+            if (hit & (1u << b)) *dst++ = (unsigned short)(tag + (((b & 1) * 8) << 5) + (b >> 1));
     }
     __syncwarp();
     for (int e0 = 0; e0 < total; e0 += 64) {
@@ -309,7 +353,7 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
 // a finishing kernel scatters them.  Otherwise the full 5x5x5 neighbourhood
 // and direct writes of phi (minimum-image mode for < 5 cells per axis).
 template <bool MI, bool COUNT, bool NEWTON, bool WIDE>
-__global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
+__global__ void __launch_bounds__(32 * kWarps, 7) realspace_cell_kernel(
     const double4 *__restrict__ rec, const int *__restrict__ sidx, const int *__restrict__ starts,
     const int4 *__restrict__ units, const int *__restrict__ nunits, RealArgs a, double *__restrict__ phi,
     double *__restrict__ acc_src, int *__restrict__ flag, unsigned long long *__restrict__ npairs) {
@@ -327,21 +371,47 @@ __global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
     const bool active = tl < un.z && t >= a.rlo && t < a.rhi;
     if (__ballot_sync(0xffffffffu, active) == 0) return;
     const double4 tp = active ? rec[t] : make_double4(0, 0, 0, 0);
-    if (lane < kT) wb.tst[lane] = tp;
+    if (lane < kT) {
+        wb.tx[lane] = tp.x;
+        wb.ty[lane] = tp.y;
+        wb.tz[lane] = tp.z;
+        wb.tq[lane] = tp.w;
+    }
     for (int i = 0; i < kT; ++i) wb.acc[i][lane] = 0.0;
-    // prefilter operands: MI -> absolute fp32 position; otherwise -2 t' and
-    // |t'|^2 with t' relative to the cell corner
+    __syncwarp();
+    // prefilter operands of this lane's two targets (see PreTargets)
     const double3 org = make_double3(cx * a.edge, cy * a.edge, cz * a.edge);
-    float4 tq;
-    if (MI) {
-        tq = make_float4((float)tp.x, (float)tp.y, (float)tp.z, 0.f);
-    } else {
-        const float rx = (float)(tp.x - org.x), ry = (float)(tp.y - org.y), rz = (float)(tp.z - org.z);
-        tq = make_float4(-2.f * rx, -2.f * ry, -2.f * rz, fmaf(rz, rz, fmaf(ry, ry, rx * rx)));
+    PreTargets pt;
+    {
+        const unsigned amask = __ballot_sync(0xffffffffu, active);
+        pt.ta = lane & 7;
+        pt.tb = pt.ta + 8;
+        float v[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int sl = h ? pt.tb : pt.ta;
+            const double4 q = make_double4(wb.tx[sl], wb.ty[sl], wb.tz[sl], 0.0);
+            const bool ok = (amask >> sl) & 1u;
+            if (MI) {
+                v[h][0] = (float)q.x;
+                v[h][1] = (float)q.y;
+                v[h][2] = (float)q.z;
+                v[h][3] = ok ? 0.f : -1e30f;
+            } else {
+                const float rx = (float)(q.x - org.x), ry = (float)(q.y - org.y), rz = (float)(q.z - org.z);
+                v[h][0] = -2.f * rx;
+                v[h][1] = -2.f * ry;
+                v[h][2] = -2.f * rz;
+                v[h][3] = ok ? fmaf(rz, rz, fmaf(ry, ry, rx * rx)) - a.rc2r : 1e30f;
+            }
+        }
+        pt.x = f2pack(v[0][0], v[1][0]);
+        pt.y = f2pack(v[0][1], v[1][1]);
+        pt.z = f2pack(v[0][2], v[1][2]);
+        pt.w = f2pack(v[0][3], v[1][3]);
     }
     int singular = 0;
     long long cnt = 0;
-    __syncwarp();
     const int home_start = starts[cell];
 
     auto axis_range = [&](int c, int mode, int &lo, int &hi) {
@@ -363,8 +433,8 @@ __global__ void __launch_bounds__(32 * kWarps) realspace_cell_kernel(
     if (NEWTON) xlo = cx;  // ox >= 0
     auto run = [&](int j0, int j1, double shx, double shy, double shz, int hs) {
         for (int jb = j0; jb < j1; jb += 32)
-            pair_batch<MI, COUNT, NEWTON, WIDE>(rec, jb, j1, shx, shy, shz, a, wb, lane, active, tq, org, t, un.y, hs,
-                                          acc_src, singular, cnt);
+            pair_batch<MI, COUNT, NEWTON, WIDE>(rec, jb, j1, shx, shy, shz, a, wb, lane, pt, org, un.y, hs, acc_src,
+                                                singular, cnt);
     };
     for (int ox = xlo; ox <= xhi; ++ox) {
         int xc = ox;

@@ -43,7 +43,7 @@ struct SpreadArgs {
 };
 
 // ---------------------------------------------------------------- windows
-// exp(v) for v <= 0 by Cody-Waite reduction and the degree-12 polynomial of
+// exp(v) for v <= 0 by Cody-Waite reduction and the degree-11 polynomial of
 // se_erfc_coeffs.h (coefficients as constant-bank operands; ~1 ulp).
 __device__ __forceinline__ double exp_nonpos(double v) {
     if (v < -700.0) return 0.0;

@@ -263,8 +263,10 @@ def test_isolated_pairs_sweep_pair_kernel(xi, rc):
     err = np.abs(-phi[:K] - want) * r
     assert np.max(err) < 4.5e-16, np.max(err)
     assert np.max(np.abs(phi[K:] - want) * r) < 4.5e-16
+    # the erfc fit is absolute (tools/gen_erfc_coeffs.py): tiny tail terms
+    # keep ~1e-9 relative accuracy
     rel = np.abs(-phi[:K] - want) / want
-    assert np.max(rel) < 1e-12
+    assert np.max(rel) < 1e-8
 
 
 def test_threads_argument_and_determinism():
