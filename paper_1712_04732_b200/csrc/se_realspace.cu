@@ -125,7 +125,9 @@ __device__ __forceinline__ double erfc_fast(double x, double w) {
 __device__ __forceinline__ double min_image(double d, double L) { return d - L * rint(d / L); }
 __device__ __forceinline__ float min_image_f(float d, float L, float invL) { return d - L * rintf(d * invL); }
 
-constexpr int kWarps = 4;  // warps (units) per block
+constexpr int kWarps = 1;  // warps (units) per block: one, so that the WarpBuf base is
+                           // block-uniform (shared addresses fold into [R + UR + imm])
+constexpr int kMinBlocks = 27;  // 27 x (7 KB + 1 KB reserved) of shared memory per SM
 constexpr int kT = 16;     // targets per warp unit: lane l tests target l % 16 against half of a 32-source batch
 
 // Shared-memory workspace of one warp unit (7 KB: 8 blocks x 4 warps per SM).
@@ -189,10 +191,10 @@ __device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const Wa
 // Target side into the lane's private slot; with NEWTON the source side
 // q_t f goes to the source's global accumulator (REDG).
 template <bool NEWTON>
-__device__ __forceinline__ void apply_hit(const Hit &h, WarpBuf &wb, int lane, int jb, double *__restrict__ acc_src) {
+__device__ __forceinline__ void apply_hit(const Hit &h, WarpBuf &wb, int lane, double *__restrict__ acc_batch) {
     double *slot = &wb.acc[h.tt][lane];
     *slot = fma(wb.sq[h.k], h.f, *slot);
-    if (NEWTON && h.ok) atomicAdd(acc_src + jb + h.k, h.qt * h.f);
+    if (NEWTON && h.ok) atomicAdd(acc_batch + h.k, h.qt * h.f);
 }
 
 // Packed fp32x2 arithmetic (FFMA2 / FADD2, sm_100): two prefilter tests per
@@ -318,6 +320,7 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
             if (hit & (1u << b)) *dst++ = (unsigned short)(tag + (((b & 1) * 8) << 5) + (b >> 1));
     }
     __syncwarp();
+    double *__restrict__ acc_batch = acc_src + jb;  // source-side sums of this batch
     for (int e0 = 0; e0 < total; e0 += 64) {
         const int rem = total - e0;
         if (rem > 32) {
@@ -333,15 +336,15 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
             if (COUNT) {
                 cnt += (h1.ok ? (NEWTON ? 2 : 1) : 0) + (h2.ok ? (NEWTON ? 2 : 1) : 0);
             } else {
-                apply_hit<NEWTON>(h1, wb, lane, jb, acc_src);
-                apply_hit<NEWTON>(h2, wb, lane, jb, acc_src);
+                apply_hit<NEWTON>(h1, wb, lane, acc_batch);
+                apply_hit<NEWTON>(h2, wb, lane, acc_batch);
             }
         } else if (lane < rem) {
             const Hit h = eval_hit<MI, NEWTON, WIDE>(wb.ent[e0 + lane], a, wb, jb, tbase, singular);
             if (COUNT)
                 cnt += h.ok ? (NEWTON ? 2 : 1) : 0;
             else
-                apply_hit<NEWTON>(h, wb, lane, jb, acc_src);
+                apply_hit<NEWTON>(h, wb, lane, acc_batch);
         }
     }
     __syncwarp();
@@ -353,7 +356,7 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
 // a finishing kernel scatters them.  Otherwise the full 5x5x5 neighbourhood
 // and direct writes of phi (minimum-image mode for < 5 cells per axis).
 template <bool MI, bool COUNT, bool NEWTON, bool WIDE>
-__global__ void __launch_bounds__(32 * kWarps, 7) realspace_cell_kernel(
+__global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel(
     const double4 *__restrict__ rec, const int *__restrict__ sidx, const int *__restrict__ starts,
     const int4 *__restrict__ units, const int *__restrict__ nunits, RealArgs a, double *__restrict__ phi,
     double *__restrict__ acc_src, int *__restrict__ flag, unsigned long long *__restrict__ npairs) {
