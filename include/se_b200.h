@@ -240,6 +240,26 @@ int se_scale_blocks_host(int device, int D, int M, int Mt, int g0, int gs, doubl
                          double *cube_or_zero, double *Iblk, const int *I_idx, int64_t nI,
                          double *Jblk, const int *J_idx, int64_t nJ);
 
+/* ------------------------------------------------------------------ *
+ * Direct Ewald sums (the reference's oracle.py evaluators) on the      *
+ * device, for validating the SE path at full size.  pos (N,3) AoS, q   *
+ * (N,); targets = indices into the system (NULL: all N, T ignored);    *
+ * phi has T (resp. N) entries.  _dev: device pointers, synchronous on  *
+ * `stream`; _host: host buffers.                                       *
+ * ------------------------------------------------------------------ */
+/* oracle.kspace_direct_3p (oracle.py:109-118): Fourier-space Ewald sum over
+ * the integer modes |n_a| <= kmax, n != 0. */
+int se_direct_kspace_3p_dev(const double *pos, const double *q, int64_t N, double L, double xi, int32_t kmax,
+                            const int64_t *targets, int64_t T, double *phi, void *stream);
+int se_direct_kspace_3p_host(const double *pos, const double *q, int64_t N, double L, double xi, int32_t kmax,
+                             const int64_t *targets, int64_t T, double *phi);
+/* oracle.kspace_direct_0p (oracle.py:181-192): sum_{n != m} q_n erf(xi r)/r
+ * + q_m 2 xi / sqrt(pi); SE_ESINGULAR for coincident distinct particles. */
+int se_direct_kspace_0p_dev(const double *pos, const double *q, int64_t N, double xi, const int64_t *targets,
+                            int64_t T, double *phi, void *stream);
+int se_direct_kspace_0p_host(const double *pos, const double *q, int64_t N, double xi, const int64_t *targets,
+                             int64_t T, double *phi);
+
 /* Thread-local message of the last failing call. */
 const char *se_last_error(void);
 /* Library version string. */

@@ -22,7 +22,7 @@ from __future__ import annotations
 import math
 
 import numpy as np
-from scipy.special import erfc as _erfc, i0 as _i0, j0 as _j0, j1 as _j1
+from scipy.special import erf as _erf, erfc as _erfc, i0 as _i0, j0 as _j0, j1 as _j1
 
 FOUR_PI = 4.0 * math.pi
 
@@ -541,6 +541,43 @@ def total_potential(pos, q, L, D, prm, use_kernel=None):
     return (realspace(pos, q, L, D, prm["xi"], prm["rc"])
             + se_kspace(pos, q, L, D, prm, use_kernel)
             + self_term(q, prm["xi"]))
+
+
+# --------------------------------------------------------------- direct sums
+
+def direct_kspace_3p(pos, q, L, xi, kmax, targets=None):
+    """Ewald Fourier sum over integer modes |n_a| <= kmax, n != 0 (oracle.py:109-118):
+    (4 pi / L^3) sum_k e^{-k^2/4xi^2}/k^2 Re(e^{i k.x_m} S_k), S_k = sum_n q_n e^{-i k.x_n}.
+    Separable per-axis phases; modes in slabs of n1 to bound memory."""
+    pos = np.asarray(pos, float)
+    tg = np.arange(len(pos)) if targets is None else np.asarray(targets)
+    n = np.arange(-kmax, kmax + 1)
+    c = 2.0 * np.pi / L
+    ex, ey, ez = (np.exp(-1j * c * np.outer(pos[:, a], n)) for a in range(3))  # (N, 2kmax+1)
+    out = np.zeros(len(tg))
+    for i1, n1 in enumerate(n):
+        # S[n2, n3] = sum_n q ex[n, n1] ey[n, n2] ez[n, n3]
+        S = np.einsum("n,nb,nc->bc", q * ex[:, i1], ey, ez)
+        k2 = c * c * (n1 * n1 + n[:, None] ** 2 + n[None, :] ** 2)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            coef = np.where(k2 > 0, np.exp(-k2 / (4.0 * xi * xi)) / k2, 0.0)
+        E = np.einsum("t,tb,tc->tbc", np.conj(ex[tg, i1]), np.conj(ey[tg]), np.conj(ez[tg]))
+        out += np.einsum("tbc,bc->t", E, coef * S).real
+    return (4.0 * np.pi / L ** 3) * out
+
+
+def direct_kspace_0p(pos, q, xi, targets=None):
+    """sum_{n != m} q_n erf(xi r)/r + q_m 2 xi / sqrt(pi) (oracle.py:181-192)."""
+    pos = np.asarray(pos, float)
+    tg = np.arange(len(pos)) if targets is None else np.asarray(targets)
+    d = pos[tg, None, :] - pos[None, :, :]
+    r = np.sqrt(np.sum(d * d, axis=2))
+    same = tg[:, None] == np.arange(len(pos))[None, :]
+    if np.any((r < 1e-14) & ~same):
+        raise ValueError("coincident distinct particles")
+    with np.errstate(divide="ignore", invalid="ignore"):
+        kern = np.where(same, 0.0, _erf(xi * r) / r)
+    return kern @ q + q[tg] * (2.0 * xi / math.sqrt(math.pi))
 
 
 def relative_rms(phi, ref):

@@ -84,6 +84,12 @@ SIGNATURES = {
     "se_gather_host": [_P, _P, _P, ctypes.c_int64, _P],
     "se_kspace_apply_host": [_P, _P, ctypes.c_int],
     "se_realspace_host": [_P, _P, _P, ctypes.c_int64, _P, ctypes.c_int],
+    "se_direct_kspace_3p_dev": [_P, _P, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, _P,
+                                ctypes.c_int64, _P, _P],
+    "se_direct_kspace_3p_host": [_P, _P, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, _P,
+                                 ctypes.c_int64, _P],
+    "se_direct_kspace_0p_dev": [_P, _P, ctypes.c_int64, ctypes.c_double, _P, ctypes.c_int64, _P, _P],
+    "se_direct_kspace_0p_host": [_P, _P, ctypes.c_int64, ctypes.c_double, _P, ctypes.c_int64, _P],
     "se_self_term_host": [_P, ctypes.c_int64, ctypes.c_double, _P],
     "se_self_term_dev": [_P, ctypes.c_int64, ctypes.c_double, _P, _P],
     "se_d0_kernel_table_host": [_P, _P],

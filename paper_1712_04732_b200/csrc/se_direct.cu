@@ -1,0 +1,313 @@
+// Direct Ewald sums on the device: the reference's independently coded
+// evaluators (oracle.py) for large-N validation of the SE path (SURVEY.md
+// 8(f).3).  Not on the hot path.
+//
+//  * D = 3, oracle.py:109-118: phi_m = (4 pi / L^3) sum_{k != 0}
+//    e^{-k^2/4xi^2}/k^2 Re(e^{i k.x_m} S_k), S_k = sum_n q_n e^{-i k.x_n}, over
+//    the integer modes |n_a| <= kmax.  S(-k) = conj S(k), so only the half
+//    space (n1 > 0, or n1 = 0 and n2 > 0, or n1 = n2 = 0 and n3 > 0) is
+//    formed, with weight 2.
+//      structure_factor_kernel: one CTA per (n1, 16 rows of n2, 128 columns
+//      of n3); particles staged 16 at a time as q e^{-i(k1 x + k2 y)} per row
+//      and e^{-i k3 z} per column (sincospi of the reduced phase), each
+//      thread accumulating 2 x 4 modes;
+//      weight_kernel: W_k = 2 e^{-k^2/4xi^2}/k^2 S_k on the half space, 0
+//      elsewhere;
+//      potential_kernel: one target per thread, modes in storage order with
+//      the n3 phase advanced by a rotation (rows restarted by sincospi).
+//  * D = 0, oracle.py:181-192: phi_m = sum_{n != m} q_n erf(xi r)/r +
+//    q_m 2 xi / sqrt(pi); coincident distinct particles are an error.
+#include <cstring>
+
+#include "se_common.h"
+
+using namespace se;
+
+#define SE_API_BEGIN try {
+#define SE_API_END                            \
+    return SE_OK;                             \
+    }                                         \
+    catch (const se::Error &e) {              \
+        se::set_last_error(e.what());         \
+        return e.code;                        \
+    }                                         \
+    catch (const std::exception &e) {         \
+        se::set_last_error(e.what());         \
+        return SE_EDEVICE;                    \
+    }
+
+namespace {
+
+constexpr int kRows = 16, kCols = 128, kChunk = 16;  // 36 KB of static shared memory
+
+// S[n1][n2 + kmax][n3 + kmax], n1 in [0, kmax]; row pitch P = 2 kmax + 1
+__global__ void __launch_bounds__(256) structure_factor_kernel(const double *__restrict__ pos,
+                                                               const double *__restrict__ q, int64_t N, double invL,
+                                                               int kmax, double2 *__restrict__ S) {
+    __shared__ double2 qab[kChunk][kRows];
+    __shared__ double2 cz[kChunk][kCols];
+    const int P = 2 * kmax + 1;
+    const int n1 = blockIdx.x;
+    const int r0 = blockIdx.y * kRows, c0 = blockIdx.z * kCols;
+    const int tid = threadIdx.x, ty = tid >> 5, tx = tid & 31;
+    double2 acc[2][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0.0, 0.0);
+    for (int64_t p0 = 0; p0 < N; p0 += kChunk) {
+        const int np = (int)min((int64_t)kChunk, N - p0);
+        __syncthreads();
+        // rows: q e^{-2 pi i (n1 x + n2 y)/L}; columns: e^{-2 pi i n3 z / L}
+        for (int e = tid; e < kChunk * (kRows + kCols); e += 256) {
+            const int p = e / (kRows + kCols), j = e % (kRows + kCols);
+            double2 v = make_double2(0.0, 0.0);
+            if (p < np) {
+                const int64_t n = p0 + p;
+                double s, c;
+                if (j < kRows) {
+                    const int n2 = r0 + j - kmax;
+                    const double ph = -2.0 * ((double)n1 * pos[3 * n] + (double)n2 * pos[3 * n + 1]) * invL;
+                    sincospi(ph, &s, &c);
+                    const double qn = q[n];
+                    v = make_double2(qn * c, qn * s);
+                } else {
+                    const int n3 = c0 + (j - kRows) - kmax;
+                    sincospi(-2.0 * (double)n3 * pos[3 * n + 2] * invL, &s, &c);
+                    v = make_double2(c, s);
+                }
+            }
+            if (j < kRows)
+                qab[p][j] = v;
+            else
+                cz[p][j - kRows] = v;
+        }
+        __syncthreads();
+        for (int p = 0; p < np; ++p) {
+            const double2 a0 = qab[p][2 * ty], a1 = qab[p][2 * ty + 1];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const double2 c = cz[p][tx + 32 * b];
+                acc[0][b].x = fma(a0.x, c.x, fma(-a0.y, c.y, acc[0][b].x));
+                acc[0][b].y = fma(a0.x, c.y, fma(a0.y, c.x, acc[0][b].y));
+                acc[1][b].x = fma(a1.x, c.x, fma(-a1.y, c.y, acc[1][b].x));
+                acc[1][b].y = fma(a1.x, c.y, fma(a1.y, c.x, acc[1][b].y));
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        const int row = r0 + 2 * ty + a;
+        if (row >= P) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int col = c0 + tx + 32 * b;
+            if (col < P) S[((int64_t)n1 * P + row) * P + col] = acc[a][b];
+        }
+    }
+}
+
+__global__ void weight_kernel(double2 *__restrict__ S, int kmax, double twopi_L, double inv4xi2) {
+    const int P = 2 * kmax + 1;
+    const int64_t total = (int64_t)(kmax + 1) * P * P;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int n3 = (int)(i % P) - kmax, n2 = (int)((i / P) % P) - kmax, n1 = (int)(i / ((int64_t)P * P));
+        const bool half = n1 > 0 || (n1 == 0 && (n2 > 0 || (n2 == 0 && n3 > 0)));
+        double w = 0.0;
+        if (half) {
+            const double k2 = twopi_L * twopi_L * ((double)n1 * n1 + (double)n2 * n2 + (double)n3 * n3);
+            w = 2.0 * exp(-k2 * inv4xi2) / k2;
+        }
+        S[i] = make_double2(S[i].x * w, S[i].y * w);
+    }
+}
+
+__global__ void __launch_bounds__(256) potential_kernel(const double *__restrict__ pos,
+                                                        const int64_t *__restrict__ targets, int64_t T, double invL,
+                                                        int kmax, const double2 *__restrict__ W, double scale,
+                                                        double *__restrict__ phi) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const int64_t m = targets ? targets[t] : t;
+    const double x = pos[3 * m], y = pos[3 * m + 1], z = pos[3 * m + 2];
+    const int P = 2 * kmax + 1;
+    double sz, cz, s0, c0;
+    sincospi(2.0 * z * invL, &sz, &cz);                 // e^{+i 2 pi z / L}: step along n3
+    sincospi(-2.0 * (double)kmax * z * invL, &s0, &c0);  // n3 = -kmax
+    double acc = 0.0;
+    const double2 *w = W;
+    for (int n1 = 0; n1 <= kmax; ++n1) {
+        for (int n2 = -kmax; n2 <= kmax; ++n2) {
+            double sa, ca;
+            sincospi(2.0 * ((double)n1 * x + (double)n2 * y) * invL, &sa, &ca);
+            // e = e^{i(k1 x + k2 y)} e^{i k3 z}, advanced by the n3 step
+            double er = ca * c0 - sa * s0, ei = ca * s0 + sa * c0;
+            for (int c = 0; c < P; ++c) {
+                const double2 v = w[c];
+                acc = fma(er, v.x, fma(-ei, v.y, acc));
+                const double nr = er * cz - ei * sz;
+                ei = er * sz + ei * cz;
+                er = nr;
+            }
+            w += P;
+        }
+    }
+    phi[t] = scale * acc;
+}
+
+__global__ void __launch_bounds__(256) erf_pair_kernel(const double *__restrict__ pos, const double *__restrict__ q,
+                                                       int64_t N, const int64_t *__restrict__ targets, int64_t T,
+                                                       double xi, double *__restrict__ phi, int *__restrict__ flag) {
+    __shared__ double4 src[256];
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool live = t < T;
+    const int64_t m = live ? (targets ? targets[t] : t) : -1;
+    const double x = live ? pos[3 * m] : 0.0, y = live ? pos[3 * m + 1] : 0.0, z = live ? pos[3 * m + 2] : 0.0;
+    double acc = 0.0;
+    int bad = 0;
+    for (int64_t j0 = 0; j0 < N; j0 += 256) {
+        __syncthreads();
+        const int64_t j = j0 + threadIdx.x;
+        if (j < N) src[threadIdx.x] = make_double4(pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], q[j]);
+        __syncthreads();
+        const int nj = (int)min((int64_t)256, N - j0);
+        if (!live) continue;
+        for (int k = 0; k < nj; ++k) {
+            const double4 s = src[k];
+            const double dx = x - s.x, dy = y - s.y, dz = z - s.z;
+            const double r = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
+            if (j0 + k == m) continue;
+            if (r < 1e-14) {
+                bad = 1;
+                continue;
+            }
+            acc += s.w * erf(xi * r) / r;
+        }
+    }
+    if (bad) atomicExch(flag, 1);
+    if (live) phi[t] = acc + q[m] * (2.0 * xi / sqrt(M_PI));
+}
+
+void check_common(int64_t N, int64_t T, const double *pos) {
+    if (N < 0 || T < 0) fail(SE_EINVAL, "negative particle or target count");
+    if (N > 0 && !pos) fail(SE_EINVAL, "null positions");
+}
+
+struct DevBuf {
+    void *p = nullptr;
+    explicit DevBuf(size_t bytes) {
+        if (bytes) SE_CUDA(cudaMalloc(&p, bytes));
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+void require_device() {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        fail(SE_EDEVICE, "no CUDA device available (the SE B200 library has no CPU fallback)");
+    }
+}
+
+void direct_3p(const double *pos, const double *q, int64_t N, double L, double xi, int kmax,
+               const int64_t *targets, int64_t T, double *phi, cudaStream_t st) {
+    check_common(N, T, pos);
+    if (!(L > 0) || !(xi > 0)) fail(SE_EINVAL, "L and xi must be positive");
+    if (kmax < 1 || kmax > 1000) fail(SE_EINVAL, "kmax must lie in [1, 1000]");
+    if (T == 0) return;
+    const int P = 2 * kmax + 1;
+    DevBuf S(sizeof(double2) * (size_t)(kmax + 1) * P * P);
+    const double invL = 1.0 / L;
+    dim3 grid((unsigned)(kmax + 1), (unsigned)((P + kRows - 1) / kRows), (unsigned)((P + kCols - 1) / kCols));
+    structure_factor_kernel<<<grid, 256, 0, st>>>(pos, q, N, invL, kmax, (double2 *)S.p);
+    SE_LAUNCH_CHECK();
+    weight_kernel<<<1184, 256, 0, st>>>((double2 *)S.p, kmax, 2.0 * M_PI / L, 1.0 / (4.0 * xi * xi));
+    SE_LAUNCH_CHECK();
+    potential_kernel<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(pos, targets, T, invL, kmax,
+                                                                 (const double2 *)S.p, 4.0 * M_PI / (L * L * L), phi);
+    SE_LAUNCH_CHECK();
+    SE_CUDA(cudaStreamSynchronize(st));
+}
+
+void direct_0p(const double *pos, const double *q, int64_t N, double xi, const int64_t *targets, int64_t T,
+               double *phi, cudaStream_t st) {
+    check_common(N, T, pos);
+    if (!(xi > 0)) fail(SE_EINVAL, "xi must be positive");
+    if (T == 0) return;
+    DevBuf flag(sizeof(int));
+    SE_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+    erf_pair_kernel<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(pos, q, N, targets, T, xi, phi, (int *)flag.p);
+    SE_LAUNCH_CHECK();
+    int h = 0;
+    SE_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SE_CUDA(cudaStreamSynchronize(st));
+    if (h) fail(SE_ESINGULAR, "coincident distinct particles");
+}
+
+// host buffers -> device, run, phi back
+template <class F>
+void via_device(const double *pos, const double *q, int64_t N, const int64_t *targets, int64_t T, double *phi,
+                F &&run) {
+    require_device();
+    const int64_t nt = targets ? T : N;
+    DevBuf dpos(sizeof(double) * 3 * (size_t)N), dq(sizeof(double) * (size_t)N),
+        dt(targets ? sizeof(int64_t) * (size_t)T : 0), dphi(sizeof(double) * (size_t)nt);
+    if (N) {
+        SE_CUDA(cudaMemcpy(dpos.p, pos, sizeof(double) * 3 * N, cudaMemcpyHostToDevice));
+        SE_CUDA(cudaMemcpy(dq.p, q, sizeof(double) * N, cudaMemcpyHostToDevice));
+    }
+    if (targets && T) SE_CUDA(cudaMemcpy(dt.p, targets, sizeof(int64_t) * T, cudaMemcpyHostToDevice));
+    run((const double *)dpos.p, (const double *)dq.p, (const int64_t *)dt.p, nt, (double *)dphi.p);
+    if (nt) SE_CUDA(cudaMemcpy(phi, dphi.p, sizeof(double) * nt, cudaMemcpyDeviceToHost));
+}
+
+void check_targets_host(const int64_t *targets, int64_t T, int64_t N) {
+    if (!targets) return;
+    for (int64_t i = 0; i < T; ++i)
+        if (targets[i] < 0 || targets[i] >= N) fail(SE_EINVAL, "target index out of range");
+}
+
+}  // namespace
+
+extern "C" {
+
+int se_direct_kspace_3p_dev(const double *pos, const double *q, int64_t N, double L, double xi, int32_t kmax,
+                            const int64_t *targets, int64_t T, double *phi, void *stream) {
+    SE_API_BEGIN
+    direct_3p(pos, q, N, L, xi, kmax, targets, targets ? T : N, phi, (cudaStream_t)stream);
+    SE_API_END
+}
+
+int se_direct_kspace_3p_host(const double *pos, const double *q, int64_t N, double L, double xi, int32_t kmax,
+                             const int64_t *targets, int64_t T, double *phi) {
+    SE_API_BEGIN
+    check_targets_host(targets, T, N);
+    via_device(pos, q, N, targets, T, phi,
+               [&](const double *dp, const double *dq, const int64_t *dt, int64_t nt, double *dphi) {
+                   direct_3p(dp, dq, N, L, xi, kmax, targets ? dt : nullptr, nt, dphi, 0);
+               });
+    SE_API_END
+}
+
+int se_direct_kspace_0p_dev(const double *pos, const double *q, int64_t N, double xi, const int64_t *targets,
+                            int64_t T, double *phi, void *stream) {
+    SE_API_BEGIN
+    direct_0p(pos, q, N, xi, targets, targets ? T : N, phi, (cudaStream_t)stream);
+    SE_API_END
+}
+
+int se_direct_kspace_0p_host(const double *pos, const double *q, int64_t N, double xi, const int64_t *targets,
+                             int64_t T, double *phi) {
+    SE_API_BEGIN
+    check_targets_host(targets, T, N);
+    via_device(pos, q, N, targets, T, phi,
+               [&](const double *dp, const double *dq, const int64_t *dt, int64_t nt, double *dphi) {
+                   direct_0p(dp, dq, N, xi, targets ? dt : nullptr, nt, dphi, 0);
+               });
+    SE_API_END
+}
+
+}  // extern "C"

@@ -24,7 +24,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
-from pmewald import aft, core, greens, params as pm, realspace, sekspace, windows  # noqa: E402
+from pmewald import aft, core, greens, oracle, params as pm, realspace, sekspace, windows  # noqa: E402
 from pmewald.core import ParticleSystem, Periodicity, SEParams  # noqa: E402
 
 
@@ -179,5 +179,26 @@ def main():
     np.savez_compressed(os.path.join(HERE, "auto_params.npz"), **ap)
 
 
+def direct_golden():
+    """The reference's direct Ewald evaluators (oracle.py:109-118, 181-192) on
+    small seeded systems: pins the device direct sums (se_direct.cu)."""
+    out = {}
+    for i, (N, L, xi, eps) in enumerate([(40, 1.0, 6.3, 1e-12), (35, 2.0, 3.0, 1e-12)]):
+        s = system(N, L, 900 + i)
+        kmax = oracle.OracleConfig.for_accuracy(xi, L, eps).kmax
+        out[f"d3_{i}_in"] = np.array([N, L, xi, kmax, 900 + i])
+        out[f"d3_{i}_pos"], out[f"d3_{i}_q"] = s.positions, s.charges
+        out[f"d3_{i}_phi"] = oracle.kspace_direct_3p(s, xi, kmax)
+    for i, (N, L, xi) in enumerate([(60, 1.0, 6.3), (50, 3.0, 2.0)]):
+        s = system(N, L, 950 + i)
+        out[f"d0_{i}_in"] = np.array([N, L, xi, 950 + i])
+        out[f"d0_{i}_pos"], out[f"d0_{i}_q"] = s.positions, s.charges
+        out[f"d0_{i}_phi"] = oracle.kspace_direct_0p(s, xi)
+    np.savez_compressed(os.path.join(HERE, "direct.npz"), **out)
+
+
 if __name__ == "__main__":
-    sys.exit(main())
+    if sys.argv[1:] == ["direct"]:
+        sys.exit(direct_golden())
+    main()
+    sys.exit(direct_golden())

@@ -90,3 +90,17 @@ def test_padded_size_and_partition_known_answers():
     assert len(I_idx) == 15 * 15 - 1 and len(J_idx) == 64 * 64 - 15 * 15
     with pytest.raises(ValueError):
         orc.padded_size(0.5, 10)
+
+
+def test_direct_sums_match_reference():
+    z = np.load(os.path.join(GOLDEN, "direct.npz"))
+    for i in range(2):
+        N, L, xi, kmax, _ = z[f"d3_{i}_in"]
+        phi = orc.direct_kspace_3p(z[f"d3_{i}_pos"], z[f"d3_{i}_q"], L, xi, int(kmax))
+        assert rms(phi, z[f"d3_{i}_phi"]) < 1e-13
+        sub = np.array([0, 3, 7])
+        part = orc.direct_kspace_3p(z[f"d3_{i}_pos"], z[f"d3_{i}_q"], L, xi, int(kmax), targets=sub)
+        assert np.allclose(part, z[f"d3_{i}_phi"][sub], rtol=1e-12, atol=1e-13)
+        N, L, xi, _ = z[f"d0_{i}_in"]
+        phi = orc.direct_kspace_0p(z[f"d0_{i}_pos"], z[f"d0_{i}_q"], xi)
+        assert rms(phi, z[f"d0_{i}_phi"]) < 1e-14
