@@ -455,3 +455,25 @@ def test_cell_list_buckets_every_particle_once():
 def test_reference_engine_name_is_available():
     from paper_1712_04732_b200 import aft
     assert hasattr(aft.NumpyFftEngine(), "rfftn") and hasattr(aft.NumpyFftEngine(), "irfftn")
+
+
+def test_run_record_csv_round_trip():
+    import io
+
+    from paper_1712_04732_b200 import records
+
+    s = se.generate_random_system(30, 1.0, seed=4)
+    for D in (3, 2, 0):
+        prm, _ = pm.auto_params(s, Periodicity(D), 6.0, 1e-8)
+        rec = records.make_record(s, prm, Periodicity(D), {"spread": 1e-3, "realspace": 2e-3}, 5e-3,
+                                  seed=4, rms_vs_oracle=1.5e-9)
+        assert list(rec) == records.CSV_COLUMNS
+        buf = io.StringIO()
+        records.write_records(buf, [rec], threads=8)
+        text = buf.getvalue()
+        assert text.startswith("# pmewald run ") and "# threads 8\n" in text
+        row = records.read_records(io.StringIO(text))[0]
+        assert int(row["D"]) == D and int(row["M"]) == prm.M and float(row["t_total"]) == 5e-3
+        assert float(row["s0_eff"]) >= (1.0 if D == 3 else prm.s0 - 1e-12)
+    with pytest.raises(RuntimeError):
+        records.write_records(io.StringIO(), [{"command": "compute"}])
