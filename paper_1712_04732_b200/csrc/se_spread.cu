@@ -261,7 +261,9 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
 }
 
 template <int WIN, int PC>
-__global__ void __launch_bounds__(512) gather_tile_kernel(const double4 *__restrict__ rec, const int *__restrict__ sidx,
+// P >= 10 (384+ threads): cap registers at 64 so that two CTAs fit per SM
+// (86 registers left a single 12-warp CTA per SM at P = 12)
+__global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(const double4 *__restrict__ rec, const int *__restrict__ sidx,
                                                           const int4 *__restrict__ units, const int *__restrict__ nunits,
                                                           SpreadArgs a, const double *__restrict__ grid,
                                                           double *__restrict__ phi, double h3, int accumulate) {
