@@ -250,7 +250,7 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": "particles/s", "cores": threads, "kind": "port",
                              "sample": last["sample"]},
             "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -414,13 +414,31 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample(pos_h, q_h, threads=1)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if sharded:
         dist.destroy_process_group()
     return 0
 
 
+_JSON_FD = None
+
+
+def emit(line):
+    """The one JSON line on the original stdout; everything else (NCCL's
+    version banner, library chatter) was redirected to stderr by main()."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)  # fd 1 (C and Python writers) -> stderr; the JSON line goes to the saved fd
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

@@ -8,7 +8,8 @@ exchange is needed inside a stage.  The exchange steps are the ones the
 method has:
 
   1. spread_shard on every rank -> partial grids; SUM all-reduce (NCCL over
-     NVLink) -> the full grid H on every rank;
+     NVLink) -> the full grid H on every rank, overlapped with the
+     real-space shard (which does not read the grid);
   2. k-space stage on every rank (the 32^3-128^3 FFTs are latency bound;
      replicating them is cheaper than a slab all-to-all at these sizes);
   3. realspace_shard (+ self term) and gather_shard write the owned entries
@@ -70,11 +71,14 @@ def total_potential_sharded(pos, q, backend, group=None):
     N = q.shape[0]
     grid = backend.empty_grid()
     backend.spread_shard(pos, q, rank, world, grid)
-    if init:
-        dist.all_reduce(grid, op=dist.ReduceOp.SUM, group=group)
-    backend.kspace_apply(grid)
+    # the grid all-reduce (NCCL over NVLink) overlaps the real-space shard,
+    # which does not read the grid
+    work = dist.all_reduce(grid, op=dist.ReduceOp.SUM, group=group, async_op=True) if init else None
     phi = backend.empty_phi(N)
     backend.realspace_shard(pos, q, rank, world, phi)
+    if work is not None:
+        work.wait()
+    backend.kspace_apply(grid)
     backend.gather_shard(grid, pos, rank, world, phi)
     if init:
         dist.all_reduce(phi, op=dist.ReduceOp.SUM, group=group)
