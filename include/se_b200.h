@@ -131,6 +131,10 @@ int se_plan_destroy(se_plan_t plan);
  * stream).  Until it is called the plan uses a stream of its own. */
 int se_plan_set_stream(se_plan_t plan, void *stream);
 int se_plan_grid(se_plan_t plan, se_grid_t *out);
+/* CUDA graphs for the fused total potential (default on): repeated calls
+ * with the same (pos, q, phi, N, stream) replay one graph of the device work
+ * (first call eager, second call captured).  0 = always launch eagerly. */
+int se_plan_set_graphs(se_plan_t plan, int on);
 /* Number of kernel launches issued by this plan since creation (for the bench). */
 int se_plan_launch_count(se_plan_t plan, int64_t *count);
 /* Warning bits raised by the last total-potential call: bit 0 = the system is

@@ -67,6 +67,7 @@ SIGNATURES = {
     "se_plan_warnings": [_P, ctypes.POINTER(ctypes.c_int)],
     "se_plan_d0_geometry": [_P, c_int32_p, c_int32_p, c_double_p],
     "se_plan_set_profiling": [_P, ctypes.c_int],
+    "se_plan_set_graphs": [_P, ctypes.c_int],
     "se_plan_kernel_times": [_P, c_double_p, c_int64_p],
     "se_realspace_pair_count_dev": [_P, _P, _P, ctypes.c_int64, c_int64_p],
     "se_spread_dev": [_P, _P, _P, ctypes.c_int64, _P],
@@ -179,6 +180,10 @@ class Plan:
     def set_stream(self, stream_ptr: int):
         """Order subsequent calls on this cudaStream_t (0 = legacy default stream)."""
         call("se_plan_set_stream", self.handle, ctypes.c_void_p(int(stream_ptr)))
+
+    def set_graphs(self, on: bool):
+        """Replay repeated total-potential calls from a CUDA graph (default on)."""
+        call("se_plan_set_graphs", self.handle, int(bool(on)))
 
     def set_profiling(self, on: bool):
         call("se_plan_set_profiling", self.handle, int(bool(on)))

@@ -124,7 +124,7 @@ struct Events {
 
 // spread -> k-space -> gather (sekspace.py:340-389); phi += or = phi_F
 void kspace_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, int use_kernel,
-                     double *timings, int accumulate, int rank, int world) {
+                     double *timings, int accumulate, int rank, int world, bool capturing = false) {
     double *grid = nullptr;
     pl->grid_dev.ensure(sizeof(double) * grid_points(pl));
     grid = pl->grid_dev.as<double>();
@@ -139,7 +139,7 @@ void kspace_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N,
     ev.mark();
     gather_run(pl, grid, pos, N, phi, accumulate, rank, world, false);
     ev.mark();
-    prof_collect(pl);
+    if (!capturing) prof_collect(pl);
     if (timings) {
         SE_CUDA(cudaStreamSynchronize(pl->stream));
         timings[SE_T_SPREAD] = ev.secs(0, 1);
@@ -151,16 +151,125 @@ void kspace_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N,
     }
 }
 
+void graph_drop(se_plan *pl) {
+    if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+    pl->gexec = nullptr;
+    pl->gwarm = false;
+    pl->gN = -1;
+}
+
+// The device work of total_potential after validation: no host syncs, so
+// it can be captured into a CUDA graph.
+void total_body(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, bool capturing) {
+    realspace_run(pl, pos, q, N, phi, 1, 0, 1);
+    kspace_pipeline(pl, pos, q, N, phi, 1, nullptr, 1, 0, 1, capturing);
+}
+
+// Repeated calls with the same (pos, q, phi, N, stream) replay a CUDA graph
+// of the body: the first call runs it eagerly (allocating every buffer and
+// table), the second captures and instantiates it, later ones launch the
+// graph -- ~40 kernel / memset / FFT launches become one.  The legacy default
+// stream cannot be captured: the graph then runs on the plan's own stream,
+// fenced after and before the caller's stream by events.
+void graph_capture(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi) {
+    const int64_t l0 = pl->launches;
+    bool pend0[SE_K_COUNT];
+    for (int id = 0; id < SE_K_COUNT; ++id) pend0[id] = pl->pending[id];
+    cudaGraph_t graph = nullptr;
+    SE_CUDA(cudaStreamBeginCapture(pl->stream, cudaStreamCaptureModeRelaxed));
+    pl->capturing = true;
+    try {
+        total_body(pl, pos, q, N, phi, true);
+    } catch (...) {
+        pl->capturing = false;
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(pl->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    pl->capturing = false;
+    SE_CUDA(cudaStreamEndCapture(pl->stream, &graph));
+    cudaError_t e = cudaGraphInstantiate(&pl->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        pl->gexec = nullptr;
+        SE_CUDA(e);
+    }
+    pl->glaunches = pl->launches - l0;
+    for (int id = 0; id < SE_K_COUNT; ++id) pl->gpending[id] = pl->pending[id] && !pend0[id];
+}
+
+void total_body_graphed(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi) {
+    const bool same = pl->gN == N && pl->gkey[0] == pos && pl->gkey[1] == q && pl->gkey[2] == phi &&
+                      pl->gstream == pl->stream && pl->gprof == pl->prof &&
+                      pl->ggen == g_buf_generation.load();
+    if (!same || !pl->gwarm) {
+        graph_drop(pl);
+        total_body(pl, pos, q, N, phi, false);
+        pl->gkey[0] = pos;
+        pl->gkey[1] = q;
+        pl->gkey[2] = phi;
+        pl->gN = N;
+        pl->gstream = pl->stream;
+        pl->gprof = pl->prof;
+        pl->ggen = g_buf_generation.load();
+        pl->gwarm = true;
+        return;
+    }
+    cudaStream_t user = pl->stream;
+    const bool legacy = user == nullptr || user == cudaStreamLegacy || user == cudaStreamPerThread;
+    cudaStream_t gs = legacy ? pl->own_stream : user;
+    if (legacy) {
+        for (auto &ev : pl->gfence)
+            if (!ev) SE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        SE_CUDA(cudaEventRecord(pl->gfence[0], user));
+        SE_CUDA(cudaStreamWaitEvent(gs, pl->gfence[0], 0));
+    }
+    if (!pl->gexec) {
+        pl->stream = gs;
+        try {
+            graph_capture(pl, pos, q, N, phi);
+        } catch (...) {
+            pl->stream = user;
+            graph_drop(pl);
+            throw;
+        }
+        pl->stream = user;
+        if (pl->ggen != g_buf_generation.load()) {  // the body allocated after all: do not keep it
+            graph_drop(pl);
+            if (legacy) {
+                SE_CUDA(cudaEventRecord(pl->gfence[1], gs));
+                SE_CUDA(cudaStreamWaitEvent(user, pl->gfence[1], 0));
+            }
+            total_body(pl, pos, q, N, phi, false);
+            return;
+        }
+    } else {
+        pl->launches += pl->glaunches;
+        for (int id = 0; id < SE_K_COUNT; ++id)
+            if (pl->gpending[id]) pl->pending[id] = true;
+    }
+    SE_CUDA(cudaGraphLaunch(pl->gexec, gs));
+    if (legacy) {
+        SE_CUDA(cudaEventRecord(pl->gfence[1], gs));
+        SE_CUDA(cudaStreamWaitEvent(user, pl->gfence[1], 0));
+    }
+}
+
 void total_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, double *timings) {
     check_system(pl, pos, q, N, true);
-    Events ev(timings != nullptr, pl->stream);
-    ev.mark();
-    realspace_run(pl, pos, q, N, phi, 1, 0, 1);
-    ev.mark();
-    kspace_pipeline(pl, pos, q, N, phi, 1, timings, 1, 0, 1);
+    if (!timings && pl->graphs && N > 0) {
+        total_body_graphed(pl, pos, q, N, phi);
+    } else {
+        Events ev(timings != nullptr, pl->stream);
+        ev.mark();
+        realspace_run(pl, pos, q, N, phi, 1, 0, 1);
+        ev.mark();
+        kspace_pipeline(pl, pos, q, N, phi, 1, timings, 1, 0, 1);
+        if (timings) timings[SE_T_REALSPACE] = ev.secs(0, 1);
+    }
     check_flag(pl);
     prof_collect(pl);
-    if (timings) timings[SE_T_REALSPACE] = ev.secs(0, 1);
 }
 
 template <class T>
@@ -189,6 +298,10 @@ void check_shard(int rank, int world) {
 
 namespace se {
 void plan_release_device(se_plan *pl) {
+    if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+    pl->gexec = nullptr;
+    for (auto &ev : pl->gfence)
+        if (ev) cudaEventDestroy(ev);
     for (cufftHandle h : {pl->fft_fwd, pl->fft_inv, pl->fft_rowJ, pl->fft_rowI, pl->fft_row0, pl->fft_c_fwd,
                           pl->fft_c_inv, pl->fft_f_fwd, pl->fft_f_inv})
         if (h) cufftDestroy(h);
@@ -254,6 +367,15 @@ int se_plan_set_stream(se_plan_t plan, void *stream) {
     SE_API_BEGIN
     se_plan *pl = checked(plan);
     pl->stream = (cudaStream_t)stream;  // 0 is the legacy default stream
+    SE_API_END
+}
+
+int se_plan_set_graphs(se_plan_t plan, int on) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    pl->graphs = on != 0;
+    if (!pl->graphs) graph_drop(pl);
     SE_API_END
 }
 

@@ -1,5 +1,6 @@
 // Internal declarations shared by the SE B200 library translation units.
 #pragma once
+#include <atomic>
 
 #include <cuda_runtime.h>
 #include <cufft.h>
@@ -61,6 +62,10 @@ double greens_zero_mode(int D, double R, double kappa);
 double bessel_i0(double x);
 
 // ---------------------------------------------------------- device buffers
+// Bumped on every device (re)allocation of a DevBuf: a captured CUDA graph
+// is replayed only while no buffer it may reference has moved.
+inline std::atomic<unsigned long long> g_buf_generation{0};
+
 struct DevBuf {
     void *ptr = nullptr;
     size_t bytes = 0;
@@ -69,12 +74,16 @@ struct DevBuf {
         if (ptr) cudaFree(ptr);
         ptr = nullptr;
         bytes = 0;
+        g_buf_generation.fetch_add(1);
         if (n == 0) return;
         SE_CUDA(cudaMalloc(&ptr, n));
         bytes = n;
     }
     void release() {
-        if (ptr) cudaFree(ptr);
+        if (ptr) {
+            cudaFree(ptr);
+            g_buf_generation.fetch_add(1);
+        }
         ptr = nullptr;
         bytes = 0;
     }
@@ -166,6 +175,19 @@ struct se_plan {
     int64_t pcount[SE_K_COUNT] = {};
     se::DevBuf pairs;  // pair counter (count mode of the real-space kernel)
     se::DevBuf racc;   // real-space pair sums in cell-sorted order (Newton path)
+    // CUDA graph of the fused total-potential body (real space + spread +
+    // k-space + gather), replayed for repeated calls with the same buffers
+    bool graphs = true;
+    cudaGraphExec_t gexec = nullptr;
+    const void *gkey[3] = {};  // pos, q, phi
+    int64_t gN = -1;
+    cudaStream_t gstream = nullptr;
+    bool gprof = false, gwarm = false;
+    int64_t glaunches = 0;           // kernels per replay (for the launch counter)
+    unsigned long long ggen = 0;     // DevBuf generation the graph was captured at
+    bool gpending[SE_K_COUNT] = {};  // profiling slots recorded by the graph
+    cudaEvent_t gfence[2] = {};      // orders the graph stream after / before a legacy caller stream
+    bool capturing = false;          // inside graph capture: profiling events become record nodes
 };
 
 namespace se {
@@ -177,11 +199,13 @@ inline void prof_begin(se_plan *pl, int id) {
         SE_CUDA(cudaEventCreate(&pl->pev[id][0]));
         SE_CUDA(cudaEventCreate(&pl->pev[id][1]));
     }
-    SE_CUDA(cudaEventRecord(pl->pev[id][0], pl->stream));
+    SE_CUDA(cudaEventRecordWithFlags(pl->pev[id][0], pl->stream,
+                                     pl->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
 }
 inline void prof_end(se_plan *pl, int id) {
     if (!pl->prof) return;
-    SE_CUDA(cudaEventRecord(pl->pev[id][1], pl->stream));
+    SE_CUDA(cudaEventRecordWithFlags(pl->pev[id][1], pl->stream,
+                                     pl->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
     pl->pending[id] = true;
 }
 inline void prof_collect(se_plan *pl) {
