@@ -234,9 +234,9 @@ void d0_kernel_prepare(se_plan *pl, double *t_precompute);
 void plan_release_device(se_plan *pl);
 
 // binning (se_sort.cu)
-void binning_reserve(Binning &b, int64_t N, int nbins, int chunk);
-void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, int64_t N,
-                  int nbins, int chunk);
+void binning_reserve(Binning &b, int64_t N, int nbins, int chunk, int extra_bits = 0);
+void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, int64_t N, int nbins, int chunk,
+                  int extra_bits = 0);
 int64_t binning_max_units(const Binning &b, int64_t N, int nbins, int chunk);
 
 // shared device helpers ---------------------------------------------------

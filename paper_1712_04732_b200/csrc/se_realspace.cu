@@ -33,7 +33,11 @@ struct RealArgs {
     float rc2f;       // fp32 prefilter bound (rc^2 plus the fp32 coordinate rounding margin)
     float rc2r;       // the same for the cell-relative |t'|^2 + |s'|^2 - 2 t'.s' form
     float Lf, invLf;  // box length for the fp32 minimum image
+    int kb;           // bits of the sub-cell z key (particles of a cell sorted by z)
+    double qinv;      // z quantum^-1 = 2^kb / edge: Q(z) = floor(z qinv), monotone along a z-run
 };
+
+__device__ __forceinline__ int zq(double z, double qinv) { return (int)floor(z * qinv); }
 
 // fp32 prefilter bound: coordinates in [-L, 2L) carry <= 2^-23 L absolute
 // rounding each, so r^2 in fp32 is within ~1.5e-6 rc L (+ fp32 products) of
@@ -55,9 +59,13 @@ __global__ void cell_keys_kernel(const double *__restrict__ pos, int64_t N, Real
         int ci = (int)(pos[3 * i + ax] / a.edge);
         c[ax] = ci < a.n - 1 ? ci : a.n - 1;
     }
-    unsigned key = (unsigned)((c[0] * a.n + c[1]) * a.n + c[2]);
-    keys[i] = key;
-    atomicAdd(&counts[key], 1);
+    const unsigned cell = (unsigned)((c[0] * a.n + c[1]) * a.n + c[2]);
+    // within a cell, order by the quantized z (clamped to the cell's range):
+    // every z-run of cells is then sorted by Q(z) up to one quantum at cell seams
+    int sub = zq(pos[3 * i + 2], a.qinv) - (c[2] << a.kb);
+    sub = sub < 0 ? 0 : (sub >= (1 << a.kb) ? (1 << a.kb) - 1 : sub);
+    keys[i] = (cell << a.kb) | (unsigned)sub;
+    atomicAdd(&counts[cell], 1);
 }
 
 // erfc(x), x >= 0, as exp(-x^2) erfcx(x): erfcx by a degree-14 polynomial in
@@ -350,6 +358,33 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     __syncwarp();
 }
 
+// First index j in [lo, hi) of a z-run with Q(z_j) >= qt (upper: > qt), or
+// hi: a warp-cooperative 32-ary search (the run is sorted by Q up to one
+// quantum at cell seams; callers widen qt by two quanta).
+__device__ __forceinline__ int zsearch(const double4 *__restrict__ rec, int lo, int hi, int qt, bool upper,
+                                       double qinv, int lane) {
+    auto pred = [&](int p) {
+        if (p >= hi) return true;
+        const int qz = zq(__ldg(&rec[p].z), qinv);
+        return upper ? qz > qt : qz >= qt;
+    };
+    while (hi - lo > 32) {
+        const int step = (hi - lo + 31) >> 5;
+        const unsigned m = __ballot_sync(0xffffffffu, pred(lo + lane * step));
+        if (m == 0) {
+            lo += 31 * step + 1;
+            continue;
+        }
+        const int k = __ffs(m) - 1;
+        if (k == 0) return lo;
+        hi = min(hi, lo + k * step);
+        lo += (k - 1) * step + 1;
+    }
+    if (lo >= hi) return hi;
+    const unsigned m = __ballot_sync(0xffffffffu, pred(lo + lane));
+    return m ? lo + __ffs(m) - 1 : hi;
+}
+
 // NEWTON: every unordered pair once -- neighbour cells in the half shell
 // o > 0 (lexicographic on (ox, oy, oz)) plus own-cell pairs with t < j; the
 // partial sums of both sides go to acc_src (sorted order, zeroed before) and
@@ -434,7 +469,24 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
     axis_range(cy, a.mode[1], ylo, yhi);
     axis_range(cz, a.mode[2], zlo, zhi);
     if (NEWTON) xlo = cx;  // ox >= 0
+    // z extent of the unit's targets (a unit is a z-slab of its cell: cells
+    // are sorted by z inside)
+    double zmin = active ? tp.z : 1e300, zmax = active ? tp.z : -1e300;
+    for (int o = 16; o > 0; o >>= 1) {
+        zmin = fmin(zmin, __shfl_xor_sync(0xffffffffu, zmin, o));
+        zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+    }
+    double hrow = a.rc;  // z half-window of the current row
     auto run = [&](int j0, int j1, double shx, double shy, double shz, int hs) {
+        if (!MI) {
+            // only sources with |z_s - z_t| <= hrow for some target can be
+            // within rc: trim the z-run to that window (two quanta of slack)
+            if (hs >= 0)
+                j0 = max(j0, un.y + 1);  // own cell: j > t for every target of the unit
+            else
+                j0 = zsearch(rec, j0, j1, zq(zmin - hrow - shz, a.qinv) - 2, false, a.qinv, lane);
+            j1 = zsearch(rec, j0, j1, zq(zmax + hrow - shz, a.qinv) + 2, true, a.qinv, lane);
+        }
         for (int jb = j0; jb < j1; jb += 32)
             pair_batch<MI, COUNT, NEWTON, WIDE>(rec, jb, j1, shx, shy, shz, a, wb, lane, pt, org, un.y, hs, acc_src,
                                                 singular, cnt);
@@ -456,6 +508,13 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
             }
             const int rowbase = (xc * n + yc) * n;
             const bool own_row = NEWTON && ox == cx && oy == cy;
+            if (!MI) {
+                // lateral gap between the target cell and this row of cells
+                const double gx = max(abs(ox - cx) - 1, 0) * a.edge, gy = max(abs(oy - cy) - 1, 0) * a.edge;
+                const double h2 = a.rc2 - gx * gx - gy * gy;
+                if (h2 < 0.0) continue;
+                hrow = sqrt(h2);
+            }
             const int zlo2 = own_row ? cz : zlo;  // (0,0): oz >= 0, own cell with j > t
             const int hs = own_row ? home_start : -1;
             if (a.mode[2] == 1) {
@@ -552,6 +611,12 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     for (int ax = 0; ax < 3; ++ax) c.mode[ax] = ax < pl->D ? (c.n >= 5 ? 1 : 2) : 0;
     a.n = c.n;
     a.edge = c.edge;
+    {
+        int cb = 1;
+        while ((1LL << cb) < (long long)c.n * c.n * c.n) ++cb;
+        a.kb = 32 - cb < 10 ? 32 - cb : 10;
+        a.qinv = (double)(1 << a.kb) / c.edge;
+    }
     // cell-relative prefilter: |t'|, |s'| <= 3 sqrt(3) e, so the fp32 form
     // |t'|^2 + |s'|^2 - 2 t'.s' is within ~1.2e-5 e^2 (+ ~1.2e-6 rc e from
     // rounding t', s') of r^2; the bound keeps 3x that
@@ -560,13 +625,13 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     int nbins = c.n * c.n * c.n;
     cudaStream_t st = pl->stream;
     prof_begin(pl, SE_K_SORT);
-    binning_reserve(pl->cbin, N, nbins, kRealUnit);
+    binning_reserve(pl->cbin, N, nbins, kRealUnit, a.kb);
     SE_CUDA(cudaMemsetAsync(pl->cbin.counts.ptr, 0, sizeof(int) * (nbins + 1), st));
     cell_keys_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(pos, N, a, pl->cbin.keys.as<unsigned>(),
                                                                    pl->cbin.counts.as<int>());
     SE_LAUNCH_CHECK();
     pl->launches += 1;
-    binning_sort(pl, pl->cbin, pos, q, N, nbins, kRealUnit);
+    binning_sort(pl, pl->cbin, pos, q, N, nbins, kRealUnit, a.kb);
     prof_end(pl, SE_K_SORT);
 }
 

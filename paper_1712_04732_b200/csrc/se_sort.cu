@@ -69,7 +69,7 @@ static int bits_for(int nbins) {
     return b;
 }
 
-void binning_reserve(Binning &b, int64_t N, int nbins, int chunk) {
+void binning_reserve(Binning &b, int64_t N, int nbins, int chunk, int extra_bits) {
     int64_t cap = N < 1 ? 1 : N;
     bool grow = cap > b.capacity;
     b.keys.ensure(sizeof(unsigned) * cap);
@@ -88,20 +88,23 @@ void binning_reserve(Binning &b, int64_t N, int nbins, int chunk) {
     b.nunits.ensure(sizeof(int) * 2);
     size_t need = 0;
     SE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, b.keys.as<unsigned>(), b.keys_sorted.as<unsigned>(),
-                                            b.idx.as<int>(), b.idx_sorted.as<int>(), (int)cap, 0, bits_for(nbins)));
+                                            b.idx.as<int>(), b.idx_sorted.as<int>(), (int)cap, 0,
+                                            bits_for(nbins) + extra_bits));
     b.cub_tmp.ensure(need);
     b.cub_bytes = b.cub_tmp.bytes;
     b.nbins = nbins;
 }
 
 // Keys must already be in b.keys and the histogram in b.counts.
-void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, int64_t N, int nbins, int chunk) {
+void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, int64_t N, int nbins, int chunk,
+                  int extra_bits) {
     cudaStream_t st = pl->stream;
     if (N > 0) {
         size_t bytes = b.cub_bytes;
         SE_CUDA(cub::DeviceRadixSort::SortPairs(b.cub_tmp.ptr, bytes, b.keys.as<unsigned>(),
                                                 b.keys_sorted.as<unsigned>(), b.idx.as<int>(),
-                                                b.idx_sorted.as<int>(), (int)N, 0, bits_for(nbins), st));
+                                                b.idx_sorted.as<int>(), (int)N, 0, bits_for(nbins) + extra_bits,
+                                                st));
         gather_records_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(pos, q, b.idx_sorted.as<int>(),
                                                                            b.rec.as<double4>(), N);
         SE_LAUNCH_CHECK();
