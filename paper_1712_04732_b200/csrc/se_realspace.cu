@@ -33,9 +33,12 @@ struct RealArgs {
     float rc2f;       // fp32 prefilter bound (rc^2 plus the fp32 coordinate rounding margin)
     float rc2r;       // the same for the cell-relative |t'|^2 + |s'|^2 - 2 t'.s' form
     float Lf, invLf;  // box length for the fp32 minimum image
-    int kb;           // bits of the sub-cell z key (particles of a cell sorted by z)
-    double qinv;      // z quantum^-1 = 2^kb / edge: Q(z) = floor(z qinv), monotone along a z-run
+    int kb;           // bits of the z key (particles of a column sorted by z)
+    double qinv;      // z quantum^-1 = 2^kb / L: Q(z) = floor(z qinv), monotone along a column
+    int zper;         // z periodic (D = 3)
 };
+
+constexpr int kReach = 3;  // columns of edge >= rc/3: neighbours within +-3 columns
 
 __device__ __forceinline__ int zq(double z, double qinv) { return (int)floor(z * qinv); }
 
@@ -53,19 +56,19 @@ __global__ void cell_keys_kernel(const double *__restrict__ pos, int64_t N, Real
                                  int *__restrict__ counts) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= N) return;
-    int c[3];
+    int c[2];
 #pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
+    for (int ax = 0; ax < 2; ++ax) {
         int ci = (int)(pos[3 * i + ax] / a.edge);
         c[ax] = ci < a.n - 1 ? ci : a.n - 1;
     }
-    const unsigned cell = (unsigned)((c[0] * a.n + c[1]) * a.n + c[2]);
-    // within a cell, order by the quantized z (clamped to the cell's range):
-    // every z-run of cells is then sorted by Q(z) up to one quantum at cell seams
-    int sub = zq(pos[3 * i + 2], a.qinv) - (c[2] << a.kb);
+    const unsigned colid = (unsigned)(c[0] * a.n + c[1]);
+    // within a column, order by the quantized z: Q(z) = floor(z qinv) is then
+    // non-decreasing along every column (z in [0, L))
+    int sub = zq(pos[3 * i + 2], a.qinv);
     sub = sub < 0 ? 0 : (sub >= (1 << a.kb) ? (1 << a.kb) - 1 : sub);
-    keys[i] = (cell << a.kb) | (unsigned)sub;
-    atomicAdd(&counts[cell], 1);
+    keys[i] = (colid << a.kb) | (unsigned)sub;
+    atomicAdd(&counts[colid], 1);
 }
 
 // erfc(x), x >= 0, as exp(-x^2) erfcx(x): erfcx by a degree-14 polynomial in
@@ -95,10 +98,9 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
 
 // Scalar constants of erfc_fast as one constant-bank block (read two per
 // LDCU.128 instead of materialised as 64-bit immediates per use).
-__constant__ double se_erfc_k[6] = {
+__constant__ double se_erfc_k[5] = {
     SE_ERFC_A + SE_ERFC_B,                // s = ((A+B) x + K (B-A)) / (x + K)
-    SE_ERFC_K * (SE_ERFC_B - SE_ERFC_A),  //
-    SE_ERFC_K,                            //
+    SE_ERFC_K * (SE_ERFC_B - SE_ERFC_A),  //   (K = 4: an immediate)
     -SE_LOG2E,                            // n = rint(-x^2 log2 e)
     -SE_LN2_HI,                           // r = -x^2 - n ln2 (Cody-Waite)
     -SE_LN2_LO};
@@ -113,18 +115,19 @@ __device__ __forceinline__ double erfc_fast(double x, double w) {
     if (WIDE) {
         if (x > SE_ERFC_XMAX) return erfc(x) * w;
     }
-    const double s = fma(x, se_erfc_k[0], se_erfc_k[1]) * rcp_nr(x + se_erfc_k[2]);
+    const double s = fma(x, se_erfc_k[0], se_erfc_k[1]) * rcp_nr(x + SE_ERFC_K);
     // Horner (Estrin's shorter chains measured slower: the kernel is
     // issue bound)
     double p = se_erfcx_c[SE_ERFC_NE];
 #pragma unroll
     for (int i = SE_ERFC_NE - 1; i >= 0; --i) p = fma(p, s, se_erfcx_c[i]);
     const double u = x * x;
-    const double n = rint(u * se_erfc_k[3]);
-    const double r = fma(n, se_erfc_k[5], fma(n, se_erfc_k[4], -u));
+    const double n = rint(u * se_erfc_k[2]);
+    const double r = fma(n, se_erfc_k[4], fma(n, se_erfc_k[3], -u));
     double e = se_exp_c[SE_EXP_NX];
 #pragma unroll
-    for (int i = SE_EXP_NX - 1; i >= 0; --i) e = fma(e, r, se_exp_c[i]);
+    for (int i = SE_EXP_NX - 1; i >= 2; --i) e = fma(e, r, se_exp_c[i]);
+    e = fma(fma(e, r, SE_EXP_C1), r, SE_EXP_C0);  // literals (1.0): no constant-bank operands
     // e * 2^n by an exponent add (n in [-27, 0]: e 2^n stays normal)
     e = __hiloint2double(__double2hiint(e) + (int)n * (1 << 20), __double2loint(e));
     return p * (e * w);
@@ -402,8 +405,8 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
     if (u >= *nunits) return;
     const int4 un = units[u];
     const int n = a.n;
-    const int cell = un.x;
-    const int cz = cell % n, cy = (cell / n) % n, cx = cell / (n * n);
+    const int col = un.x;  // bins are columns (cx, cy) of edge >= rc/3, sorted by z inside
+    const int cx = col / n, cy = col - cx * n;
     const int tl = lane & (kT - 1);
     const int t = un.y + tl;
     const bool active = tl < un.z && t >= a.rlo && t < a.rhi;
@@ -416,11 +419,21 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
         wb.tq[lane] = tp.w;
     }
     for (int i = 0; i < kT; ++i) wb.acc[i][lane] = 0.0;
+    // z extent of the unit's targets (a unit is a z-slab of its column)
+    double zmin = active ? tp.z : 1e300, zmax = active ? tp.z : -1e300;
+    for (int o = 16; o > 0; o >>= 1) {
+        zmin = fmin(zmin, __shfl_xor_sync(0xffffffffu, zmin, o));
+        zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+    }
     __syncwarp();
-    // prefilter operands of this lane's two targets (see PreTargets)
-    const double3 org = make_double3(cx * a.edge, cy * a.edge, cz * a.edge);
+    // prefilter operands of this lane's two targets (see PreTargets), relative
+    // to org = (column corner, zmin); the fp32 rounding margin of the expanded
+    // form scales with the operand magnitudes: |t'| <= Rt, |s'| <= Rt + rc
+    const double3 org = make_double3(cx * a.edge, cy * a.edge, zmin);
     PreTargets pt;
     {
+        const double Rt = 1.4143 * a.edge + (zmax - zmin), Rs = Rt + 1.01 * a.rc;
+        const float bound = (float)(a.rc2 + 4e-7 * (Rt + Rs) * (Rt + Rs));
         const unsigned amask = __ballot_sync(0xffffffffu, active);
         pt.ta = lane & 7;
         pt.tb = pt.ta + 8;
@@ -440,7 +453,7 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
                 v[h][0] = -2.f * rx;
                 v[h][1] = -2.f * ry;
                 v[h][2] = -2.f * rz;
-                v[h][3] = ok ? fmaf(rz, rz, fmaf(ry, ry, rx * rx)) - a.rc2r : 1e30f;
+                v[h][3] = ok ? fmaf(rz, rz, fmaf(ry, ry, rx * rx)) - bound : 1e30f;
             }
         }
         pt.x = f2pack(v[0][0], v[1][0]);
@@ -450,43 +463,24 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
     }
     int singular = 0;
     long long cnt = 0;
-    const int home_start = starts[cell];
 
     auto axis_range = [&](int c, int mode, int &lo, int &hi) {
         if (mode == 2) {
             lo = 0;
             hi = n - 1;
         } else if (mode == 1) {
-            lo = c - 2;
-            hi = c + 2;
+            lo = c - kReach;
+            hi = c + kReach;
         } else {
-            lo = max(0, c - 2);
-            hi = min(n - 1, c + 2);
+            lo = max(0, c - kReach);
+            hi = min(n - 1, c + kReach);
         }
     };
-    int xlo, xhi, ylo, yhi, zlo, zhi;
+    int xlo, xhi, ylo, yhi;
     axis_range(cx, a.mode[0], xlo, xhi);
     axis_range(cy, a.mode[1], ylo, yhi);
-    axis_range(cz, a.mode[2], zlo, zhi);
     if (NEWTON) xlo = cx;  // ox >= 0
-    // z extent of the unit's targets (a unit is a z-slab of its cell: cells
-    // are sorted by z inside)
-    double zmin = active ? tp.z : 1e300, zmax = active ? tp.z : -1e300;
-    for (int o = 16; o > 0; o >>= 1) {
-        zmin = fmin(zmin, __shfl_xor_sync(0xffffffffu, zmin, o));
-        zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
-    }
-    double hrow = a.rc;  // z half-window of the current row
     auto run = [&](int j0, int j1, double shx, double shy, double shz, int hs) {
-        if (!MI) {
-            // only sources with |z_s - z_t| <= hrow for some target can be
-            // within rc: trim the z-run to that window (two quanta of slack)
-            if (hs >= 0)
-                j0 = max(j0, un.y + 1);  // own cell: j > t for every target of the unit
-            else
-                j0 = zsearch(rec, j0, j1, zq(zmin - hrow - shz, a.qinv) - 2, false, a.qinv, lane);
-            j1 = zsearch(rec, j0, j1, zq(zmax + hrow - shz, a.qinv) + 2, true, a.qinv, lane);
-        }
         for (int jb = j0; jb < j1; jb += 32)
             pair_batch<MI, COUNT, NEWTON, WIDE>(rec, jb, j1, shx, shy, shz, a, wb, lane, pt, org, un.y, hs, acc_src,
                                                 singular, cnt);
@@ -506,25 +500,36 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
                 if (yc < 0) { yc += n; shy = -a.L; }
                 else if (yc >= n) { yc -= n; shy = a.L; }
             }
-            const int rowbase = (xc * n + yc) * n;
-            const bool own_row = NEWTON && ox == cx && oy == cy;
-            if (!MI) {
-                // lateral gap between the target cell and this row of cells
-                const double gx = max(abs(ox - cx) - 1, 0) * a.edge, gy = max(abs(oy - cy) - 1, 0) * a.edge;
-                const double h2 = a.rc2 - gx * gx - gy * gy;
-                if (h2 < 0.0) continue;
-                hrow = sqrt(h2);
+            const int cs = starts[xc * n + yc], ce = starts[xc * n + yc + 1];
+            if (cs == ce) continue;
+            if (MI) {  // whole column; minimum image in the distance
+                run(cs, ce, shx, shy, 0.0, -1);
+                continue;
             }
-            const int zlo2 = own_row ? cz : zlo;  // (0,0): oz >= 0, own cell with j > t
-            const int hs = own_row ? home_start : -1;
-            if (a.mode[2] == 1) {
-                // up to three contiguous runs: wrapped below, in range, wrapped above
-                if (zlo2 < 0) run(starts[rowbase + zlo2 + n], starts[rowbase + n], shx, shy, -a.L, -1);
-                const int blo = max(zlo2, 0), bhi = min(zhi, n - 1);
-                if (blo <= bhi) run(starts[rowbase + blo], starts[rowbase + bhi + 1], shx, shy, 0.0, hs);
-                if (zhi > n - 1) run(starts[rowbase], starts[rowbase + zhi - n + 1], shx, shy, a.L, -1);
-            } else {
-                run(starts[rowbase + zlo2], starts[rowbase + zhi + 1], shx, shy, 0.0, hs);
+            // only sources with |z_s - z_t| <= h, h^2 = rc^2 - (lateral gap)^2,
+            // for some target can be within rc: the column is searched for
+            // that z-window (one quantum of slack each side)
+            const double gx = max(abs(ox - cx) - 1, 0) * a.edge, gy = max(abs(oy - cy) - 1, 0) * a.edge;
+            const double h2 = a.rc2 - gx * gx - gy * gy;
+            if (h2 < 0.0) continue;
+            const double h = sqrt(h2);
+            const double wlo = zmin - h, whi = zmax + h;
+            const bool own = NEWTON && ox == cx && oy == cy;
+            // in-box images: own column -> sources above the unit (j > t)
+            const int j0 = own ? un.y + 1 : zsearch(rec, cs, ce, zq(wlo, a.qinv) - 1, false, a.qinv, lane);
+            const int j1 = zsearch(rec, j0, ce, zq(whi, a.qinv) + 1, true, a.qinv, lane);
+            if (j0 < j1) run(j0, j1, shx, shy, 0.0, own ? un.y : -1);
+            if (a.zper) {
+                // periodic z: the window's parts beyond [0, L) as shifted images
+                // (the own column takes only the images above: half shell)
+                if (!own && wlo < 0.0) {
+                    const int k0 = zsearch(rec, cs, ce, zq(wlo + a.L, a.qinv) - 1, false, a.qinv, lane);
+                    if (k0 < ce) run(k0, ce, shx, shy, -a.L, -1);
+                }
+                if (whi >= a.L) {
+                    const int k1 = zsearch(rec, cs, ce, zq(whi - a.L, a.qinv) + 1, true, a.qinv, lane);
+                    if (cs < k1) run(cs, k1, shx, shy, a.L, -1);
+                }
             }
         }
     }
@@ -603,26 +608,28 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     const double L = pl->L, rc = pl->p.rc;
     if (N >= (1LL << 27)) fail(SE_EINVAL, "real-space kernel supports N < 2^27 particles per call");
     CellGeom &c = pl->cell;
-    long long nn = (long long)std::floor(2.0 * L / rc);
+    // columns (cx, cy) of edge >= rc/3 in x, y; z is not binned but sorted
+    long long nn = (long long)std::floor(kReach * L / rc);
     if (nn < 1) nn = 1;
-    if (nn > 160) nn = 160;
+    if (nn > 1024) nn = 1024;
     c.n = (int)nn;
     c.edge = L / c.n;
-    for (int ax = 0; ax < 3; ++ax) c.mode[ax] = ax < pl->D ? (c.n >= 5 ? 1 : 2) : 0;
+    // x, y: periodic axes wrap +-kReach columns if there are enough of them,
+    // else all columns with the minimum image (then z too, if periodic)
+    for (int ax = 0; ax < 2; ++ax) c.mode[ax] = ax < pl->D ? (c.n >= 2 * kReach + 1 ? 1 : 2) : 0;
+    const bool mi = c.mode[0] == 2 || c.mode[1] == 2;
+    c.mode[2] = pl->D == 3 ? (mi ? 2 : 1) : 0;
     a.n = c.n;
     a.edge = c.edge;
+    a.zper = c.mode[2] == 1;
+    int nbins = c.n * c.n;
     {
         int cb = 1;
-        while ((1LL << cb) < (long long)c.n * c.n * c.n) ++cb;
-        a.kb = 32 - cb < 10 ? 32 - cb : 10;
-        a.qinv = (double)(1 << a.kb) / c.edge;
+        while ((1LL << cb) < (long long)nbins) ++cb;
+        a.kb = 32 - cb < 20 ? 32 - cb : 20;
+        a.qinv = (double)(1 << a.kb) / L;
     }
-    // cell-relative prefilter: |t'|, |s'| <= 3 sqrt(3) e, so the fp32 form
-    // |t'|^2 + |s'|^2 - 2 t'.s' is within ~1.2e-5 e^2 (+ ~1.2e-6 rc e from
-    // rounding t', s') of r^2; the bound keeps 3x that
-    a.rc2r = (float)(rc * rc + 4e-5 * c.edge * c.edge + 4e-6 * rc * c.edge);
     for (int ax = 0; ax < 3; ++ax) a.mode[ax] = c.mode[ax];
-    int nbins = c.n * c.n * c.n;
     cudaStream_t st = pl->stream;
     prof_begin(pl, SE_K_SORT);
     binning_reserve(pl->cbin, N, nbins, kRealUnit, a.kb);
@@ -638,7 +645,7 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
 template <bool COUNT>
 static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, unsigned long long *npairs) {
     const CellGeom &c = pl->cell;
-    int nbins = c.n * c.n * c.n;
+    int nbins = c.n * c.n;
     int64_t maxu = binning_max_units(pl->cbin, N, nbins, kRealUnit);
     const bool mi = c.mode[0] == 2 || c.mode[1] == 2 || c.mode[2] == 2;
     unsigned blocks = (unsigned)((maxu + kWarps - 1) / kWarps);
