@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libse_b200.so")
+# SE_B200_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("SE_B200_LIB") or os.path.join(_HERE, "_lib", "libse_b200.so")
 
 SE_OK, SE_EINVAL, SE_ECONFIG, SE_ESINGULAR, SE_ENUMERIC, SE_EDEVICE = range(6)
 WINDOWS = {"gaussian": 0, "kb": 1, "bm": 2}

@@ -40,9 +40,14 @@ struct RealArgs {
     int kb;           // bits of the z key (particles of a column sorted by z)
     double qinv;      // z quantum^-1 = 2^kb / L: Q(z) = floor(z qinv), monotone along a column
     int zper;         // z periodic (D = 3)
+    int reach;        // neighbour columns within +-reach (column edge >= rc / reach)
 };
 
-constexpr int kReach = 3;  // columns of edge >= rc/3: neighbours within +-3 columns
+// columns of edge >= rc/reach: neighbours within +-reach columns; reach 3
+// (fewer candidates) unless columns would be short (small N: every visited
+// column costs at least one batch, so fewer, longer columns win)
+constexpr int kReachMax = 3;
+constexpr double kShortColumn = 256.0;  // mean particles per column below which reach = 2
 
 __device__ __forceinline__ int zq(double z, double qinv) { return (int)floor(z * qinv); }
 
@@ -473,11 +478,11 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
             lo = 0;
             hi = n - 1;
         } else if (mode == 1) {
-            lo = c - kReach;
-            hi = c + kReach;
+            lo = c - a.reach;
+            hi = c + a.reach;
         } else {
-            lo = max(0, c - kReach);
-            hi = min(n - 1, c + kReach);
+            lo = max(0, c - a.reach);
+            hi = min(n - 1, c + a.reach);
         }
     };
     int xlo, xhi, ylo, yhi;
@@ -605,22 +610,30 @@ __global__ void realspace_image_kernel(const double *__restrict__ pos, const dou
     phi[t] = v;
 }
 
-static const int kRealUnit = kT;
+// targets per work unit: kT, or half of it for small systems (latency bound:
+// more, shorter units keep more warps in flight)
+static int real_unit(int64_t N) { return N < 50000 ? kT / 2 : kT; }
 
 // cells of edge >= rc/2 and the particle binning by cell
 static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N, RealArgs &a) {
     const double L = pl->L, rc = pl->p.rc;
     if (N >= (1LL << 27)) fail(SE_EINVAL, "real-space kernel supports N < 2^27 particles per call");
     CellGeom &c = pl->cell;
-    // columns (cx, cy) of edge >= rc/3 in x, y; z is not binned but sorted
-    long long nn = (long long)std::floor(kReach * L / rc);
-    if (nn < 1) nn = 1;
-    if (nn > 1024) nn = 1024;
+    // columns (cx, cy) of edge >= rc/reach in x, y; z is not binned but sorted
+    int reach = kReachMax;
+    long long nn = 1;
+    for (;; --reach) {
+        nn = (long long)std::floor(reach * L / rc);
+        if (nn < 1) nn = 1;
+        if (nn > 1024) nn = 1024;
+        if (reach == 2 || (double)N / ((double)nn * nn) >= kShortColumn) break;
+    }
+    a.reach = reach;
     c.n = (int)nn;
     c.edge = L / c.n;
-    // x, y: periodic axes wrap +-kReach columns if there are enough of them,
+    // x, y: periodic axes wrap +-reach columns if there are enough of them,
     // else all columns with the minimum image (then z too, if periodic)
-    for (int ax = 0; ax < 2; ++ax) c.mode[ax] = ax < pl->D ? (c.n >= 2 * kReach + 1 ? 1 : 2) : 0;
+    for (int ax = 0; ax < 2; ++ax) c.mode[ax] = ax < pl->D ? (c.n >= 2 * reach + 1 ? 1 : 2) : 0;
     const bool mi = c.mode[0] == 2 || c.mode[1] == 2;
     c.mode[2] = pl->D == 3 ? (mi ? 2 : 1) : 0;
     a.n = c.n;
@@ -636,13 +649,13 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     for (int ax = 0; ax < 3; ++ax) a.mode[ax] = c.mode[ax];
     cudaStream_t st = pl->stream;
     prof_begin(pl, SE_K_SORT);
-    binning_reserve(pl->cbin, N, nbins, kRealUnit, a.kb);
+    binning_reserve(pl->cbin, N, nbins, real_unit(N), a.kb);
     SE_CUDA(cudaMemsetAsync(pl->cbin.counts.ptr, 0, sizeof(int) * (nbins + 1), st));
     cell_keys_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(pos, N, a, pl->cbin.keys.as<unsigned>(),
                                                                    pl->cbin.counts.as<int>());
     SE_LAUNCH_CHECK();
     pl->launches += 1;
-    binning_sort(pl, pl->cbin, pos, q, N, nbins, kRealUnit, a.kb);
+    binning_sort(pl, pl->cbin, pos, q, N, nbins, real_unit(N), a.kb);
     prof_end(pl, SE_K_SORT);
 }
 
@@ -650,7 +663,7 @@ template <bool COUNT>
 static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, unsigned long long *npairs) {
     const CellGeom &c = pl->cell;
     int nbins = c.n * c.n;
-    int64_t maxu = binning_max_units(pl->cbin, N, nbins, kRealUnit);
+    int64_t maxu = binning_max_units(pl->cbin, N, nbins, real_unit(N));
     const bool mi = c.mode[0] == 2 || c.mode[1] == 2 || c.mode[2] == 2;
     unsigned blocks = (unsigned)((maxu + kWarps - 1) / kWarps);
     cudaStream_t st = pl->stream;
