@@ -411,7 +411,12 @@ def run_ours(args):
             "config": {"workload": DESCR[CFG["workload"]], "N": N, "seed": CFG["seed"],
                        "parallelism": f"particle-shard x{world} (grid + phi sum-all-reduce)",
                        "l2": "flushed (256 MB write) between timed steps, outside the step events"},
-            "e2e": e2e, "roofline": roofline, "kernels": kern, "gpu_launches": launches,
+            "e2e": e2e, "roofline": roofline, "kernels": kern,
+            "kernels_note": ("event spans per stage on the stream it runs on; the k-space pipeline "
+                             "(spread, kspace, gather, its sort) runs on a side stream concurrently with "
+                             "the real-space kernel, so its spans include waiting for SM resources and "
+                             "the shares do not add up to 1"),
+            "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps, "wall_s_timed_region": t_wall,
             "clocks": clk.summary() if rank == 0 else None,
             "pairs_in_cutoff": pairs}

@@ -158,11 +158,43 @@ void graph_drop(se_plan *pl) {
     pl->gN = -1;
 }
 
+__global__ void add_kernel(double *__restrict__ phi, const double *__restrict__ add, int64_t N) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < N) phi[i] += add[i];
+}
+
 // The device work of total_potential after validation: no host syncs, so
-// it can be captured into a CUDA graph.
+// it can be captured into a CUDA graph.  The k-space pipeline (spread ->
+// FFT / multiplier -> gather, shared-memory / LSU bound) runs on a
+// higher-priority side stream concurrently with the real-space kernel
+// (issue / fp64 bound) and lands in its own buffer; phi_R + self is written
+// by the real-space finish, then phi += phi_F after the join.
 void total_body(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, bool capturing) {
+    if (!pl->side) {
+        int lo = 0, hi = 0;
+        SE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        SE_CUDA(cudaStreamCreateWithPriority(&pl->side, cudaStreamNonBlocking, hi));
+        SE_CUDA(cudaEventCreateWithFlags(&pl->fork_ev, cudaEventDisableTiming));
+        SE_CUDA(cudaEventCreateWithFlags(&pl->join_ev, cudaEventDisableTiming));
+    }
+    pl->phik.ensure(sizeof(double) * (N ? N : 1));
+    cudaStream_t main_st = pl->stream;
+    SE_CUDA(cudaEventRecord(pl->fork_ev, main_st));
+    SE_CUDA(cudaStreamWaitEvent(pl->side, pl->fork_ev, 0));
+    pl->stream = pl->side;
+    try {
+        kspace_pipeline(pl, pos, q, N, pl->phik.as<double>(), 1, nullptr, 0, 0, 1, capturing);
+    } catch (...) {
+        pl->stream = main_st;
+        throw;
+    }
+    pl->stream = main_st;
+    SE_CUDA(cudaEventRecord(pl->join_ev, pl->side));
     realspace_run(pl, pos, q, N, phi, 1, 0, 1);
-    kspace_pipeline(pl, pos, q, N, phi, 1, nullptr, 1, 0, 1, capturing);
+    SE_CUDA(cudaStreamWaitEvent(main_st, pl->join_ev, 0));
+    add_kernel<<<(unsigned)((N + 255) / 256), 256, 0, main_st>>>(phi, pl->phik.as<double>(), N);
+    SE_LAUNCH_CHECK();
+    pl->launches += 1;
 }
 
 // Repeated calls with the same (pos, q, phi, N, stream) replay a CUDA graph
@@ -258,8 +290,11 @@ void total_body_graphed(se_plan *pl, const double *pos, const double *q, int64_t
 
 void total_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, double *timings) {
     check_system(pl, pos, q, N, true);
-    if (!timings && pl->graphs && N > 0) {
-        total_body_graphed(pl, pos, q, N, phi);
+    if (!timings && N > 0) {
+        if (pl->graphs)
+            total_body_graphed(pl, pos, q, N, phi);
+        else
+            total_body(pl, pos, q, N, phi, false);
     } else {
         Events ev(timings != nullptr, pl->stream);
         ev.mark();
@@ -298,6 +333,11 @@ void check_shard(int rank, int world) {
 
 namespace se {
 void plan_release_device(se_plan *pl) {
+    if (pl->side) cudaStreamSynchronize(pl->side);
+    if (pl->side) cudaStreamDestroy(pl->side);
+    if (pl->fork_ev) cudaEventDestroy(pl->fork_ev);
+    if (pl->join_ev) cudaEventDestroy(pl->join_ev);
+    pl->phik.release();
     if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
     pl->gexec = nullptr;
     for (auto &ev : pl->gfence)

@@ -188,6 +188,11 @@ struct se_plan {
     bool gpending[SE_K_COUNT] = {};  // profiling slots recorded by the graph
     cudaEvent_t gfence[2] = {};      // orders the graph stream after / before a legacy caller stream
     bool capturing = false;          // inside graph capture: profiling events become record nodes
+    // overlap of the k-space pipeline (side stream, higher priority) with the
+    // real-space kernel in total_potential
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    se::DevBuf phik;  // phi_F of the overlapped k-space pipeline
 };
 
 namespace se {
