@@ -238,7 +238,7 @@ __device__ __forceinline__ unsigned long long f2add(unsigned long long a, float 
 // Prefilter operands of one lane: targets pa = lane % 8 and pa + 8 of the
 // unit (lo / hi halves of the packed pairs), sources 8 (lane / 8) .. + 7 of
 // each batch.  Outside minimum-image mode: (-2 t'x, -2 t'y, -2 t'z,
-// |t'|^2 - bound) with t' relative to the unit's cell corner; in it the
+// |t'|^2 - bound) with t' relative to org = (column corner, lowest target z); in it the
 // absolute fp32 positions.  An absent target never passes.
 struct PreTargets {
     unsigned long long x, y, z, w;
@@ -251,8 +251,8 @@ struct PreTargets {
 //     per packed instruction; hit bit 2 kk + h = (target pa + 8 h, source
 //     8 (l / 8) + kk).  Outside minimum-image mode the test is
 //     |t'|^2 + |s'|^2 - 2 t'.s' - bound < 0 with t', s' relative to the
-//     unit's cell corner; the bound covers the fp32 rounding.  With NEWTON,
-//     sources of the target's own cell count only if j > t;
+//     unit's origin; the bound covers the fp32 rounding.  With NEWTON,
+//     sources of the target's own column count only if j > t;
 //  2. warp prefix scan of the hit counts and compaction of the hits;
 //  3. the list is evaluated 64 hits at a time (two per lane) on full warps.
 template <bool MI, bool COUNT, bool NEWTON, bool WIDE>
@@ -311,7 +311,7 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
         hit &= valid >= 8 ? 0xffffu : ((1u << (2 * valid)) - 1u);
     }
     if (NEWTON && hs >= 0) {
-        // own-cell sources j in [hs, t] are visited from their own unit:
+        // own-column sources j in [hs, t] are visited from their own unit:
         // exclude source slots k in [lo, t - jb] for each of the two targets
         const int lo = max(hs - jb, 0) - g8;
         auto excl = [&](int t) -> unsigned {  // 8-bit mask over this quarter
@@ -398,9 +398,9 @@ __device__ __forceinline__ int zsearch(const double4 *__restrict__ rec, int lo, 
 }
 
 // NEWTON: every unordered pair once -- neighbour cells in the half shell
-// o > 0 (lexicographic on (ox, oy, oz)) plus own-cell pairs with t < j; the
+// (ox, oy) > 0 (lexicographic) plus own-column pairs with t < j; the
 // partial sums of both sides go to acc_src (sorted order, zeroed before) and
-// a finishing kernel scatters them.  Otherwise the full 5x5x5 neighbourhood
+// a finishing kernel scatters them.  Otherwise the full column neighbourhood
 // and direct writes of phi (minimum-image mode for < 5 cells per axis).
 template <bool MI, bool COUNT, bool NEWTON, bool WIDE>
 __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel(
@@ -614,7 +614,7 @@ __global__ void realspace_image_kernel(const double *__restrict__ pos, const dou
 // more, shorter units keep more warps in flight)
 static int real_unit(int64_t N) { return N < 50000 ? kT / 2 : kT; }
 
-// cells of edge >= rc/2 and the particle binning by cell
+// columns of edge >= rc/reach and the particle binning by (column, z)
 static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N, RealArgs &a) {
     const double L = pl->L, rc = pl->p.rc;
     if (N >= (1LL << 27)) fail(SE_EINVAL, "real-space kernel supports N < 2^27 particles per call");

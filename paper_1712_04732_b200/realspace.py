@@ -34,7 +34,7 @@ class CellList:
 def build_cell_list(system: ParticleSystem, rc: float, periodicity: Periodicity) -> CellList:
     """Cell list with edge L / floor(L / rc) (realspace.py:43-59), built by the
     library's counting sort (se_cell_list_host).  An inspection utility: the
-    device real-space kernel bins on its own rc/2 grid."""
+    device real-space kernel bins into z-sorted columns of edge rc/3."""
     if rc <= 0:
         raise ValueError("rc must be positive")
     if periodicity.D >= 1 and rc > system.L / 2 + 1e-12:
