@@ -61,23 +61,48 @@ static inline void set_prefilter(RealArgs &a) {
     a.invLf = (float)(1.0 / a.L);
 }
 
-__global__ void cell_keys_kernel(const double *__restrict__ pos, int64_t N, RealArgs a, unsigned *__restrict__ keys,
-                                 int *__restrict__ counts) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= N) return;
+__device__ __forceinline__ unsigned column_key(const double *__restrict__ pos, int64_t i, const RealArgs &a,
+                                               unsigned &colid) {
     int c[2];
 #pragma unroll
     for (int ax = 0; ax < 2; ++ax) {
         int ci = (int)(pos[3 * i + ax] / a.edge);
         c[ax] = ci < a.n - 1 ? ci : a.n - 1;
     }
-    const unsigned colid = (unsigned)(c[0] * a.n + c[1]);
+    colid = (unsigned)(c[0] * a.n + c[1]);
     // within a column, order by the quantized z: Q(z) = floor(z qinv) is then
     // non-decreasing along every column (z in [0, L))
     int sub = zq(pos[3 * i + 2], a.qinv);
     sub = sub < 0 ? 0 : (sub >= (1 << a.kb) ? (1 << a.kb) - 1 : sub);
-    keys[i] = (colid << a.kb) | (unsigned)sub;
+    return (colid << a.kb) | (unsigned)sub;
+}
+
+__global__ void cell_keys_kernel(const double *__restrict__ pos, int64_t N, RealArgs a, unsigned *__restrict__ keys,
+                                 int *__restrict__ counts) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    unsigned colid;
+    keys[i] = column_key(pos, i, a, colid);
     atomicAdd(&counts[colid], 1);
+}
+
+// Few columns (<= kHistSmem): per-block shared-memory histogram, flushed
+// once per non-empty column (~1000 particles per column contend on one
+// global counter otherwise).
+constexpr int kHistSmem = 8192;
+__global__ void cell_keys_hist_kernel(const double *__restrict__ pos, int64_t N, RealArgs a, int nbins,
+                                      unsigned *__restrict__ keys, int *__restrict__ counts) {
+    extern __shared__ int hist[];
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned colid;
+        keys[i] = column_key(pos, i, a, colid);
+        atomicAdd(&hist[colid], 1);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+        if (hist[b]) atomicAdd(&counts[b], hist[b]);
 }
 
 // erfc(x), x >= 0, as exp(-x^2) erfcx(x): erfcx by a degree-14 polynomial in
@@ -651,8 +676,15 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     prof_begin(pl, SE_K_SORT);
     binning_reserve(pl->cbin, N, nbins, real_unit(N), a.kb);
     SE_CUDA(cudaMemsetAsync(pl->cbin.counts.ptr, 0, sizeof(int) * (nbins + 1), st));
-    cell_keys_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(pos, N, a, pl->cbin.keys.as<unsigned>(),
-                                                                   pl->cbin.counts.as<int>());
+    if (nbins <= kHistSmem) {
+        int64_t blocks = (N + 4095) / 4096;  // ~16 particles per thread
+        if (blocks > 1184) blocks = 1184;
+        cell_keys_hist_kernel<<<(unsigned)blocks, 256, sizeof(int) * nbins, st>>>(
+            pos, N, a, nbins, pl->cbin.keys.as<unsigned>(), pl->cbin.counts.as<int>());
+    } else {
+        cell_keys_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(pos, N, a, pl->cbin.keys.as<unsigned>(),
+                                                                       pl->cbin.counts.as<int>());
+    }
     SE_LAUNCH_CHECK();
     pl->launches += 1;
     binning_sort(pl, pl->cbin, pos, q, N, nbins, real_unit(N), a.kb);
