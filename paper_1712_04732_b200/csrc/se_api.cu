@@ -59,10 +59,20 @@ __global__ void check_kernel(const double *__restrict__ pos, const double *__res
         a += __shfl_xor_sync(0xffffffffu, a, o);
         bad += __shfl_xor_sync(0xffffffffu, bad, o);
     }
+    // block reduction, then one atomic per block and quantity (per-warp
+    // atomics on three addresses serialise: ~50 us at N = 1e6)
+    __shared__ double red[3][32];
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(out, s);
-        atomicAdd(out + 1, a);
-        atomicAdd(out + 2, bad);
+        red[0][w] = s;
+        red[1][w] = a;
+        red[2][w] = bad;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double v = 0.0;
+        for (int i = 0; i < nw; ++i) v += red[threadIdx.x][i];
+        atomicAdd(out + threadIdx.x, v);
     }
 }
 
