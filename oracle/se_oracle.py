@@ -22,7 +22,7 @@ from __future__ import annotations
 import math
 
 import numpy as np
-from scipy.special import erf as _erf, erfc as _erfc, i0 as _i0, j0 as _j0, j1 as _j1
+from scipy.special import erf as _erf, erfc as _erfc, erfcx as _erfcx, i0 as _i0, j0 as _j0, j1 as _j1
 
 FOUR_PI = 4.0 * math.pi
 
@@ -564,6 +564,35 @@ def direct_kspace_3p(pos, q, L, xi, kmax, targets=None):
         E = np.einsum("t,tb,tc->tbc", np.conj(ex[tg, i1]), np.conj(ey[tg]), np.conj(ez[tg]))
         out += np.einsum("tbc,bc->t", E, coef * S).real
     return (4.0 * np.pi / L ** 3) * out
+
+
+def direct_kspace_2p(pos, q, L, xi, kmax, targets=None):
+    """Closed-form doubly periodic Fourier sum (oracle.py:120-153): per mode
+    k = 2 pi (n1, n2)/L != 0, (pi/L^2) sum_n q_n e^{i k.d} B(k, z)/k with
+    B = e^{kz} erfc(k/2xi + xi z) + e^{-kz} erfc(k/2xi - xi z) (erfcx form where
+    the argument is >= 0), minus (2 sqrt(pi)/L^2) sum_n q_n [e^{-xi^2 z^2}/xi +
+    sqrt(pi) z erf(xi z)]; modes over the half plane with weight 2."""
+    pos = np.asarray(pos, float)
+    tg = np.arange(len(pos)) if targets is None else np.asarray(targets)
+    d = pos[tg, None, :] - pos[None, :, :]
+    z = d[..., 2]
+    out = np.zeros(len(tg))
+    for n1 in range(0, kmax + 1):
+        for n2 in range(-kmax, kmax + 1):
+            if n1 == 0 and n2 <= 0:
+                continue
+            kx, ky = 2 * np.pi * n1 / L, 2 * np.pi * n2 / L
+            k = math.hypot(kx, ky)
+            guard = -(k * k / (4 * xi * xi) + (xi * z) ** 2)
+            b = np.zeros_like(z)
+            for sgn in (1.0, -1.0):
+                u = k / (2 * xi) + sgn * xi * z
+                pos_u = u >= 0
+                b += np.where(pos_u, _erfcx(np.where(pos_u, u, 0.0)) * np.exp(guard),
+                              np.exp(sgn * k * np.where(pos_u, 0.0, z)) * _erfc(u))
+            out += 2.0 * (np.cos(kx * d[..., 0] + ky * d[..., 1]) * b / k) @ q
+    zero = (np.exp(-(xi * z) ** 2) / xi + math.sqrt(math.pi) * z * _erf(xi * z)) @ q
+    return (np.pi / L ** 2) * out - (2 * math.sqrt(math.pi) / L ** 2) * zero
 
 
 def direct_kspace_0p(pos, q, xi, targets=None):

@@ -17,7 +17,14 @@
 //      the n3 phase advanced by a rotation (rows restarted by sincospi).
 //  * D = 0, oracle.py:181-192: phi_m = sum_{n != m} q_n erf(xi r)/r +
 //    q_m 2 xi / sqrt(pi); coincident distinct particles are an error.
+//  * D = 2, oracle.py:120-153: per periodic mode k = (n1, n2) 2 pi / L != 0 the
+//    closed form (pi / L^2) sum_n q_n e^{i k.(x_m - x_n)} [e^{kz} erfc(k/2xi +
+//    xi z) + e^{-kz} erfc(k/2xi - xi z)] / k, z = z_m - z_n, in its overflow-safe
+//    erfcx form, minus (2 sqrt(pi) / L^2) sum_n q_n [e^{-xi^2 z^2}/xi +
+//    sqrt(pi) z erf(xi z)]; one CTA per target, threads over sources, modes
+//    over the half plane (weight 2) with e^{-k^2/4xi^2}, 1/k tabulated.
 #include <cstring>
+#include <vector>
 
 #include "se_common.h"
 
@@ -189,6 +196,51 @@ __global__ void __launch_bounds__(256) erf_pair_kernel(const double *__restrict_
     if (live) phi[t] = acc + q[m] * (2.0 * xi / sqrt(M_PI));
 }
 
+struct Mode2 {
+    double k, ek, invk;  // |k|, e^{-k^2/4xi^2}, 1/|k|
+    int n1, n2;
+};
+
+__global__ void __launch_bounds__(256) direct2p_kernel(const double *__restrict__ pos, const double *__restrict__ q,
+                                                       int64_t N, const int64_t *__restrict__ targets, double L,
+                                                       double xi, const Mode2 *__restrict__ modes, int nmodes,
+                                                       double *__restrict__ phi) {
+    const int64_t m = targets ? targets[blockIdx.x] : (int64_t)blockIdx.x;
+    const double xm = pos[3 * m], ym = pos[3 * m + 1], zm = pos[3 * m + 2];
+    const double twopiL = 2.0 * M_PI / L, inv2xi = 0.5 / xi;
+    double acc = 0.0, zero = 0.0;
+    for (int64_t n = threadIdx.x; n < N; n += blockDim.x) {
+        const double dx = xm - pos[3 * n], dy = ym - pos[3 * n + 1], z = zm - pos[3 * n + 2];
+        const double qn = q[n];
+        const double ez = exp(-(xi * z) * (xi * z));
+        zero += qn * (ez / xi + sqrt(M_PI) * z * erf(xi * z));
+        double s = 0.0;
+        for (int j = 0; j < nmodes; ++j) {
+            const Mode2 md = modes[j];
+            const double u1 = md.k * inv2xi + xi * z, u2 = md.k * inv2xi - xi * z;
+            const double g = md.ek * ez;  // e^{guard}, guard = -(k^2/4xi^2 + xi^2 z^2)
+            const double b1 = u1 >= 0.0 ? erfcx(u1) * g : exp(md.k * z) * erfc(u1);
+            const double b2 = u2 >= 0.0 ? erfcx(u2) * g : exp(-md.k * z) * erfc(u2);
+            const double ph = twopiL * (md.n1 * dx + md.n2 * dy);
+            s += cos(ph) * (b1 + b2) * md.invk;
+        }
+        acc += qn * s;
+    }
+    __shared__ double ra[256], rz[256];
+    ra[threadIdx.x] = acc;
+    rz[threadIdx.x] = zero;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            ra[threadIdx.x] += ra[threadIdx.x + o];
+            rz[threadIdx.x] += rz[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        phi[blockIdx.x] = (M_PI / (L * L)) * 2.0 * ra[0] - (2.0 * sqrt(M_PI) / (L * L)) * rz[0];
+}
+
 void check_common(int64_t N, int64_t T, const double *pos) {
     if (N < 0 || T < 0) fail(SE_EINVAL, "negative particle or target count");
     if (N > 0 && !pos) fail(SE_EINVAL, "null positions");
@@ -245,6 +297,27 @@ void direct_0p(const double *pos, const double *q, int64_t N, double xi, const i
     SE_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     SE_CUDA(cudaStreamSynchronize(st));
     if (h) fail(SE_ESINGULAR, "coincident distinct particles");
+}
+
+void direct_2p(const double *pos, const double *q, int64_t N, double L, double xi, int kmax,
+               const int64_t *targets, int64_t T, double *phi, cudaStream_t st) {
+    check_common(N, T, pos);
+    if (!(L > 0) || !(xi > 0)) fail(SE_EINVAL, "L and xi must be positive");
+    if (kmax < 1 || kmax > 1000) fail(SE_EINVAL, "kmax must lie in [1, 1000]");
+    if (T == 0) return;
+    std::vector<Mode2> md;
+    for (int n1 = 0; n1 <= kmax; ++n1)
+        for (int n2 = -kmax; n2 <= kmax; ++n2) {
+            if (n1 == 0 && n2 <= 0) continue;  // half plane, weight 2
+            const double k = 2.0 * M_PI / L * std::sqrt((double)n1 * n1 + (double)n2 * n2);
+            md.push_back(Mode2{k, std::exp(-k * k / (4.0 * xi * xi)), 1.0 / k, n1, n2});
+        }
+    DevBuf dm(sizeof(Mode2) * md.size());
+    SE_CUDA(cudaMemcpyAsync(dm.p, md.data(), sizeof(Mode2) * md.size(), cudaMemcpyHostToDevice, st));
+    direct2p_kernel<<<(unsigned)T, 256, 0, st>>>(pos, q, N, targets, L, xi, (const Mode2 *)dm.p, (int)md.size(),
+                                                 phi);
+    SE_LAUNCH_CHECK();
+    SE_CUDA(cudaStreamSynchronize(st));
 }
 
 // host buffers -> device, run, phi back
@@ -306,6 +379,24 @@ int se_direct_kspace_0p_host(const double *pos, const double *q, int64_t N, doub
     via_device(pos, q, N, targets, T, phi,
                [&](const double *dp, const double *dq, const int64_t *dt, int64_t nt, double *dphi) {
                    direct_0p(dp, dq, N, xi, targets ? dt : nullptr, nt, dphi, 0);
+               });
+    SE_API_END
+}
+
+int se_direct_kspace_2p_dev(const double *pos, const double *q, int64_t N, double L, double xi, int32_t kmax,
+                            const int64_t *targets, int64_t T, double *phi, void *stream) {
+    SE_API_BEGIN
+    direct_2p(pos, q, N, L, xi, kmax, targets, targets ? T : N, phi, (cudaStream_t)stream);
+    SE_API_END
+}
+
+int se_direct_kspace_2p_host(const double *pos, const double *q, int64_t N, double L, double xi, int32_t kmax,
+                             const int64_t *targets, int64_t T, double *phi) {
+    SE_API_BEGIN
+    check_targets_host(targets, T, N);
+    via_device(pos, q, N, targets, T, phi,
+               [&](const double *dp, const double *dq, const int64_t *dt, int64_t nt, double *dphi) {
+                   direct_2p(dp, dq, N, L, xi, kmax, targets ? dt : nullptr, nt, dphi, 0);
                });
     SE_API_END
 }

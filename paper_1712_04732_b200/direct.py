@@ -7,13 +7,15 @@ package's SE path and run here as CUDA kernels of the SE B200 library
 
   * kspace_direct_3p  (oracle.py:109-118): the Ewald Fourier sum over all
     integer modes |n_a| <= kmax (structure factors + per-target mode sum);
+  * kspace_direct_2p  (oracle.py:120-153): the closed-form doubly periodic
+    sum (per-mode erfc form in its overflow-safe erfcx variant + zero mode);
   * kspace_direct_0p  (oracle.py:181-192): the free-space complement
     sum q erf(xi r)/r plus the self limit.
 
-Both accept `targets` (indices into the system) so that a full-size system
-(all N sources) can be checked at a sample of targets.  The closed-form
-doubly / singly periodic sums (oracle.py:134-178) are not provided on the
-device; tests use the CPU restatement for small systems.
+All accept `targets` (indices into the system) so that a full-size system
+(all N sources) can be checked at a sample of targets.  The singly periodic sum
+(oracle.py:156-178: incomplete Bessel K0 by quadrature) is not provided on
+the device.
 """
 
 from __future__ import annotations
@@ -58,6 +60,17 @@ def kspace_direct_3p(system: ParticleSystem, xi: float, kmax: int, targets=None)
     return phi
 
 
+def kspace_direct_2p(system: ParticleSystem, xi: float, kmax: int, targets=None) -> np.ndarray:
+    """Closed-form doubly periodic Fourier sum (per-mode erfc form + zero mode),
+    oracle.py:134-153; periodic axes x, y."""
+    t, T = _targets(system, targets)
+    phi = np.empty(T)
+    _native.call("se_direct_kspace_2p_host", _native.ptr(system.positions), _native.ptr(system.charges),
+                 system.N, float(system.L), float(xi), int(kmax),
+                 _native.ptr(t) if t is not None else None, T, _native.ptr(phi))
+    return phi
+
+
 def kspace_direct_0p(system: ParticleSystem, xi: float, targets=None) -> np.ndarray:
     """sum_{n != m} q_n erf(xi r)/r + q_m 2 xi / sqrt(pi); SingularConfigurationError
     for coincident distinct particles."""
@@ -70,12 +83,14 @@ def kspace_direct_0p(system: ParticleSystem, xi: float, targets=None) -> np.ndar
 
 def kspace_direct(system: ParticleSystem, xi: float, periodicity: Periodicity, kmax: int,
                   targets=None) -> np.ndarray:
-    """Dispatch by periodicity (oracle.py:195-204); D = 1, 2 are CPU-only in the reference."""
+    """Dispatch by periodicity (oracle.py:195-204); D = 1 is not provided on the device."""
     if periodicity.D == 3:
         return kspace_direct_3p(system, xi, kmax, targets)
+    if periodicity.D == 2:
+        return kspace_direct_2p(system, xi, kmax, targets)
     if periodicity.D == 0:
         return kspace_direct_0p(system, xi, targets)
-    raise NotImplementedError("direct sums for D = 1, 2 are not provided on the device")
+    raise NotImplementedError("the singly periodic direct sum is not provided on the device")
 
 
 def self_limit(q, xi: float) -> np.ndarray:

@@ -1,7 +1,7 @@
 """Device direct Ewald sums (paper_1712_04732_b200.direct, csrc/se_direct.cu)
 against the reference's own oracle outputs, and the SE k-space path checked
-against them at FULL size (cfg2: N = 1e6, D = 3; cfg5: N = 5e5, D = 0) on a
-sample of targets.  The SE-vs-direct bound is the method's own
+against them at FULL size (cfg2: N = 1e6, D = 3; cfg3: N = 2e5, D = 2; cfg5:
+N = 5e5, D = 0) on a sample of targets.  The SE-vs-direct bound is the method's own
 discretisation error at the configs' parameters (eps = 1e-8 class), not a
 rounding bound; the device-vs-reference bound is rounding.
 """
@@ -39,6 +39,17 @@ def test_direct_3p_matches_reference(gold, i):
 
 
 @pytest.mark.parametrize("i", [0, 1])
+def test_direct_2p_matches_reference(gold, i):
+    N, L, xi, kmax, _ = gold[f"d2_{i}_in"]
+    s = se.ParticleSystem(gold[f"d2_{i}_pos"], gold[f"d2_{i}_q"], L)
+    ref = gold[f"d2_{i}_phi"]
+    assert se.relative_rms_error(direct.kspace_direct_2p(s, xi, int(kmax)), ref) < 1e-12
+    sub = np.array([4, 0])
+    assert np.allclose(direct.kspace_direct(s, xi, se.Periodicity(2), int(kmax), targets=sub), ref[sub],
+                       rtol=1e-11, atol=1e-12)
+
+
+@pytest.mark.parametrize("i", [0, 1])
 def test_direct_0p_matches_reference(gold, i):
     N, L, xi, _ = gold[f"d0_{i}_in"]
     s = se.ParticleSystem(gold[f"d0_{i}_pos"], gold[f"d0_{i}_q"], L)
@@ -61,7 +72,7 @@ def test_direct_errors():
     with pytest.raises(ValueError):
         direct.kspace_direct_3p(ok, 3.0, 4, targets=[0, 2])
     with pytest.raises(NotImplementedError):
-        direct.kspace_direct(ok, 3.0, se.Periodicity(2), 4)
+        direct.kspace_direct(ok, 3.0, se.Periodicity(1), 4)
 
 
 def test_se_kspace_vs_direct_small_all_periodicities_d3_d0():
@@ -94,6 +105,24 @@ def test_cfg2_full_size_kspace_vs_direct_sum():
     # ES P=8 at M=128: the window / aliasing error of the eps = 1e-8 class
     # (measured 2.35e-8; the reference's own P=8 sweep fixture shows 1.4e-8)
     assert err < 7e-8
+
+
+def test_cfg3_full_size_kspace_vs_direct_sum():
+    # D = 2 at full size (N = 2e5): the tolerance-meeting parameter set (P = 10,
+    # s0 = s = 4, nI = 48; 8.6e-10 on a probe) against the
+    # closed-form doubly periodic direct sum at sampled targets
+    import workloads
+
+    w = workloads.ALL["cfg3_tol"]()
+    p = se.SEParams(**w["prm"])
+    s = se.ParticleSystem(w["pos"], w["q"], w["L"])
+    phik = se.se_kspace(s, p, se.Periodicity(2))
+    sel = np.random.default_rng(13).choice(s.N, 48, replace=False)
+    kmax = direct.OracleConfig.for_accuracy(p.xi, s.L, 1e-13).kmax
+    ref = direct.kspace_direct_2p(s, p.xi, kmax, targets=sel)
+    err = se.relative_rms_error(phik[sel], ref)
+    print(f"cfg3_tol SE k-space vs direct 2p sum (kmax={kmax}): rel RMS {err:.3e}")
+    assert err < 1e-9  # measured 2.5e-10
 
 
 def test_cfg5_full_size_kspace_vs_direct_sum():

@@ -104,3 +104,6 @@ def test_direct_sums_match_reference():
         N, L, xi, _ = z[f"d0_{i}_in"]
         phi = orc.direct_kspace_0p(z[f"d0_{i}_pos"], z[f"d0_{i}_q"], xi)
         assert rms(phi, z[f"d0_{i}_phi"]) < 1e-14
+        N, L, xi, kmax, _ = z[f"d2_{i}_in"]
+        phi = orc.direct_kspace_2p(z[f"d2_{i}_pos"], z[f"d2_{i}_q"], L, xi, int(kmax))
+        assert rms(phi, z[f"d2_{i}_phi"]) < 1e-12
