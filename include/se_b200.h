@@ -263,6 +263,13 @@ int se_direct_kspace_2p_dev(const double *pos, const double *q, int64_t N, doubl
                             const int64_t *targets, int64_t T, double *phi, void *stream);
 int se_direct_kspace_2p_host(const double *pos, const double *q, int64_t N, double L, double xi, int32_t kmax,
                              const int64_t *targets, int64_t T, double *phi);
+/* oracle.kspace_direct_1p (oracle.py:156-178): singly periodic Fourier sum
+ * (incomplete Bessel K0 per mode, log + E1 zero mode); periodic axis x.
+ * SE_ESINGULAR if two charges share transverse coordinates. */
+int se_direct_kspace_1p_dev(const double *pos, const double *q, int64_t N, double L, double xi, int32_t kmax,
+                            const int64_t *targets, int64_t T, double *phi, void *stream);
+int se_direct_kspace_1p_host(const double *pos, const double *q, int64_t N, double L, double xi, int32_t kmax,
+                             const int64_t *targets, int64_t T, double *phi);
 /* oracle.kspace_direct_0p (oracle.py:181-192): sum_{n != m} q_n erf(xi r)/r
  * + q_m 2 xi / sqrt(pi); SE_ESINGULAR for coincident distinct particles. */
 int se_direct_kspace_0p_dev(const double *pos, const double *q, int64_t N, double xi, const int64_t *targets,

@@ -94,6 +94,10 @@ SIGNATURES = {
                                 ctypes.c_int64, _P, _P],
     "se_direct_kspace_2p_host": [_P, _P, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, _P,
                                  ctypes.c_int64, _P],
+    "se_direct_kspace_1p_dev": [_P, _P, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, _P,
+                                ctypes.c_int64, _P, _P],
+    "se_direct_kspace_1p_host": [_P, _P, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, _P,
+                                 ctypes.c_int64, _P],
     "se_direct_kspace_0p_dev": [_P, _P, ctypes.c_int64, ctypes.c_double, _P, ctypes.c_int64, _P, _P],
     "se_direct_kspace_0p_host": [_P, _P, ctypes.c_int64, ctypes.c_double, _P, ctypes.c_int64, _P],
     "se_self_term_host": [_P, ctypes.c_int64, ctypes.c_double, _P],

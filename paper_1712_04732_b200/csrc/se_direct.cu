@@ -23,6 +23,12 @@
 //    erfcx form, minus (2 sqrt(pi) / L^2) sum_n q_n [e^{-xi^2 z^2}/xi +
 //    sqrt(pi) z erf(xi z)]; one CTA per target, threads over sources, modes
 //    over the half plane (weight 2) with e^{-k^2/4xi^2}, 1/k tabulated.
+//  * D = 1, oracle.py:156-178: (1/L) sum_n q_n 2 sum_{j=1..kmax} cos(k_j x)
+//    K0(a_j, b) - (1/L) sum_{n != m} q_n [gamma + ln b + E1(b)], x = x_m - x_n,
+//    b = xi^2 |transverse distance|^2, a_j = k_j^2/4xi^2, with the incomplete
+//    Bessel K0(a, b) = int_0^inf exp(-a e^u - b e^-u) du (oracle.py:41-55) by
+//    Gauss-Legendre panels in u; the mode sum is moved under the integral
+//    (e^{-a_j e^u} = q^{j^2}, q = e^{-a_1 e^u}: a recurrence per node).
 #include <cstring>
 #include <vector>
 
@@ -241,6 +247,91 @@ __global__ void __launch_bounds__(256) direct2p_kernel(const double *__restrict_
         phi[blockIdx.x] = (M_PI / (L * L)) * 2.0 * ra[0] - (2.0 * sqrt(M_PI) / (L * L)) * rz[0];
 }
 
+// E1(x), x > 0: power series for x <= 1, modified Lentz continued fraction
+// above (oracle.py:58-91 uses the same two regimes).
+__device__ double e1_dev(double x) {
+    if (x <= 1.0) {
+        double total = -0.5772156649015328606 - log(x), term = 1.0;
+        for (int k = 1; k < 60; ++k) {
+            term *= -x / k;
+            const double c = -term / k;
+            total += c;
+            if (fabs(c) < 1e-18 * fabs(total)) break;
+        }
+        return total;
+    }
+    const double tiny = 1e-300;
+    double b = x + 1.0, c = 1.0 / tiny, d = 1.0 / b, f = d;
+    for (int k = 1; k < 300; ++k) {
+        const double an = -(double)k * k;
+        b += 2.0;
+        d = 1.0 / (b + an * d);
+        c = b + an / c;
+        const double delta = c * d;
+        f *= delta;
+        if (fabs(delta - 1.0) < 1e-16) break;
+    }
+    return exp(-x) * f;
+}
+
+struct Node1 {
+    double emu, w, q;  // e^{-u}, weight, e^{-a_1 e^u}
+};
+
+__global__ void __launch_bounds__(256) direct1p_kernel(const double *__restrict__ pos, const double *__restrict__ q,
+                                                       int64_t N, const int64_t *__restrict__ targets, double L,
+                                                       double xi, int kmax, const Node1 *__restrict__ nodes,
+                                                       int nnodes, double *__restrict__ phi, int *__restrict__ flag) {
+    const int64_t m = targets ? targets[blockIdx.x] : (int64_t)blockIdx.x;
+    const double xm = pos[3 * m], ym = pos[3 * m + 1], zm = pos[3 * m + 2];
+    double acc = 0.0, zero = 0.0;
+    int bad = 0;
+    for (int64_t n = threadIdx.x; n < N; n += blockDim.x) {
+        const double x = xm - pos[3 * n], dy = ym - pos[3 * n + 1], dz = zm - pos[3 * n + 2];
+        const double w2 = dy * dy + dz * dz;
+        if (n != m && w2 < 1e-28) {
+            bad = 1;
+            continue;
+        }
+        const double b = xi * xi * w2, qn = q[n];
+        const double c1 = cos(2.0 * M_PI * x / L);
+        double s = 0.0;
+        for (int j = 0; j < nnodes; ++j) {
+            const Node1 nd = nodes[j];
+            const double eb = exp(-b * nd.emu);
+            if (eb == 0.0) continue;
+            // sum_i cos(i theta) q^{i^2}, i = 1..kmax
+            const double qq = nd.q * nd.q;
+            double t = nd.q, p = nd.q * qq;  // q^{i^2}, q^{2i+1}
+            double cm = 1.0, ci = c1, sum = 0.0;
+            for (int i = 1; i <= kmax && t > 1e-30; ++i) {
+                sum = fma(ci, t, sum);
+                t *= p;
+                p *= qq;
+                const double cn = 2.0 * c1 * ci - cm;
+                cm = ci;
+                ci = cn;
+            }
+            s = fma(nd.w * eb, sum, s);
+        }
+        acc = fma(qn, 2.0 * s, acc);
+        if (n != m) zero += qn * (0.5772156649015328606 + log(b) + e1_dev(b));
+    }
+    __shared__ double ra[256], rz[256];
+    ra[threadIdx.x] = acc;
+    rz[threadIdx.x] = zero;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            ra[threadIdx.x] += ra[threadIdx.x + o];
+            rz[threadIdx.x] += rz[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (bad) atomicExch(flag, 1);
+    if (threadIdx.x == 0) phi[blockIdx.x] = (ra[0] - rz[0]) / L;
+}
+
 void check_common(int64_t N, int64_t T, const double *pos) {
     if (N < 0 || T < 0) fail(SE_EINVAL, "negative particle or target count");
     if (N > 0 && !pos) fail(SE_EINVAL, "null positions");
@@ -320,6 +411,61 @@ void direct_2p(const double *pos, const double *q, int64_t N, double L, double x
     SE_CUDA(cudaStreamSynchronize(st));
 }
 
+// Gauss-Legendre nodes on [-1, 1] (Newton on the Legendre recurrence, host)
+static void gauss_legendre(int n, std::vector<double> &x, std::vector<double> &w) {
+    x.resize(n);
+    w.resize(n);
+    for (int i = 0; i < n; ++i) {
+        double z = std::cos(M_PI * (i + 0.75) / (n + 0.5)), dp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = z;
+            for (int j = 2; j <= n; ++j) {
+                const double p2 = ((2 * j - 1) * z * p1 - (j - 1) * p0) / j;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = n * (z * p1 - p0) / (z * z - 1.0);
+            const double dz = p1 / dp;
+            z -= dz;
+            if (std::fabs(dz) < 1e-16) break;
+        }
+        x[i] = z;
+        w[i] = 2.0 / ((1.0 - z * z) * dp * dp);
+    }
+}
+
+void direct_1p(const double *pos, const double *q, int64_t N, double L, double xi, int kmax,
+               const int64_t *targets, int64_t T, double *phi, cudaStream_t st) {
+    check_common(N, T, pos);
+    if (!(L > 0) || !(xi > 0)) fail(SE_EINVAL, "L and xi must be positive");
+    if (kmax < 1 || kmax > 1000) fail(SE_EINVAL, "kmax must lie in [1, 1000]");
+    if (T == 0) return;
+    // u in [0, U]: e^{-a_1 e^U} < e^{-46}; panels of width 1/2, 20 points each
+    const double k1 = 2.0 * M_PI / L, a1 = k1 * k1 / (4.0 * xi * xi);
+    const double U = std::log(46.0 / a1) > 0.5 ? std::log(46.0 / a1) : 0.5;
+    const int npan = (int)std::ceil(U / 0.5);
+    std::vector<double> gx, gw;
+    gauss_legendre(20, gx, gw);
+    std::vector<Node1> nodes;
+    for (int pnl = 0; pnl < npan; ++pnl) {
+        const double lo = U * pnl / npan, hi = U * (pnl + 1) / npan;
+        for (int i = 0; i < 20; ++i) {
+            const double u = 0.5 * (lo + hi) + 0.5 * (hi - lo) * gx[i];
+            nodes.push_back(Node1{std::exp(-u), 0.5 * (hi - lo) * gw[i], std::exp(-a1 * std::exp(u))});
+        }
+    }
+    DevBuf dn(sizeof(Node1) * nodes.size()), flag(sizeof(int));
+    SE_CUDA(cudaMemcpyAsync(dn.p, nodes.data(), sizeof(Node1) * nodes.size(), cudaMemcpyHostToDevice, st));
+    SE_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+    direct1p_kernel<<<(unsigned)T, 256, 0, st>>>(pos, q, N, targets, L, xi, kmax, (const Node1 *)dn.p,
+                                                 (int)nodes.size(), phi, (int *)flag.p);
+    SE_LAUNCH_CHECK();
+    int h = 0;
+    SE_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SE_CUDA(cudaStreamSynchronize(st));
+    if (h) fail(SE_ESINGULAR, "two charges share transverse coordinates; the zero-mode log diverges");
+}
+
 // host buffers -> device, run, phi back
 template <class F>
 void via_device(const double *pos, const double *q, int64_t N, const int64_t *targets, int64_t T, double *phi,
@@ -397,6 +543,24 @@ int se_direct_kspace_2p_host(const double *pos, const double *q, int64_t N, doub
     via_device(pos, q, N, targets, T, phi,
                [&](const double *dp, const double *dq, const int64_t *dt, int64_t nt, double *dphi) {
                    direct_2p(dp, dq, N, L, xi, kmax, targets ? dt : nullptr, nt, dphi, 0);
+               });
+    SE_API_END
+}
+
+int se_direct_kspace_1p_dev(const double *pos, const double *q, int64_t N, double L, double xi, int32_t kmax,
+                            const int64_t *targets, int64_t T, double *phi, void *stream) {
+    SE_API_BEGIN
+    direct_1p(pos, q, N, L, xi, kmax, targets, targets ? T : N, phi, (cudaStream_t)stream);
+    SE_API_END
+}
+
+int se_direct_kspace_1p_host(const double *pos, const double *q, int64_t N, double L, double xi, int32_t kmax,
+                             const int64_t *targets, int64_t T, double *phi) {
+    SE_API_BEGIN
+    check_targets_host(targets, T, N);
+    via_device(pos, q, N, targets, T, phi,
+               [&](const double *dp, const double *dq, const int64_t *dt, int64_t nt, double *dphi) {
+                   direct_1p(dp, dq, N, L, xi, kmax, targets ? dt : nullptr, nt, dphi, 0);
                });
     SE_API_END
 }

@@ -1,21 +1,21 @@
 """Direct Ewald sums on the device (mirror of the evaluators in pmewald.oracle).
 
 The reference ships independently coded, slow evaluators for validating the
-SE method (oracle.py).  Two of them are the natural large-N checks of this
-package's SE path and run here as CUDA kernels of the SE B200 library
-(csrc/se_direct.cu):
+SE method (oracle.py).  Its direct Fourier-space sums for every periodicity
+are the natural large-N checks of this package's SE path and run here as
+CUDA kernels of the SE B200 library (csrc/se_direct.cu):
 
   * kspace_direct_3p  (oracle.py:109-118): the Ewald Fourier sum over all
     integer modes |n_a| <= kmax (structure factors + per-target mode sum);
   * kspace_direct_2p  (oracle.py:120-153): the closed-form doubly periodic
     sum (per-mode erfc form in its overflow-safe erfcx variant + zero mode);
+  * kspace_direct_1p  (oracle.py:156-178): the singly periodic sum
+    (incomplete Bessel K0 by Gauss-Legendre quadrature, log + E1 zero mode);
   * kspace_direct_0p  (oracle.py:181-192): the free-space complement
     sum q erf(xi r)/r plus the self limit.
 
 All accept `targets` (indices into the system) so that a full-size system
-(all N sources) can be checked at a sample of targets.  The singly periodic sum
-(oracle.py:156-178: incomplete Bessel K0 by quadrature) is not provided on
-the device.
+(all N sources) can be checked at a sample of targets.
 """
 
 from __future__ import annotations
@@ -71,6 +71,18 @@ def kspace_direct_2p(system: ParticleSystem, xi: float, kmax: int, targets=None)
     return phi
 
 
+def kspace_direct_1p(system: ParticleSystem, xi: float, kmax: int, targets=None) -> np.ndarray:
+    """Singly periodic Fourier sum (oracle.py:156-178): incomplete Bessel K0
+    per mode (quadrature on the device), log + E1 zero mode; periodic axis x.
+    SingularConfigurationError if two charges share transverse coordinates."""
+    t, T = _targets(system, targets)
+    phi = np.empty(T)
+    _native.call("se_direct_kspace_1p_host", _native.ptr(system.positions), _native.ptr(system.charges),
+                 system.N, float(system.L), float(xi), int(kmax),
+                 _native.ptr(t) if t is not None else None, T, _native.ptr(phi))
+    return phi
+
+
 def kspace_direct_0p(system: ParticleSystem, xi: float, targets=None) -> np.ndarray:
     """sum_{n != m} q_n erf(xi r)/r + q_m 2 xi / sqrt(pi); SingularConfigurationError
     for coincident distinct particles."""
@@ -83,14 +95,14 @@ def kspace_direct_0p(system: ParticleSystem, xi: float, targets=None) -> np.ndar
 
 def kspace_direct(system: ParticleSystem, xi: float, periodicity: Periodicity, kmax: int,
                   targets=None) -> np.ndarray:
-    """Dispatch by periodicity (oracle.py:195-204); D = 1 is not provided on the device."""
+    """Dispatch by periodicity (oracle.py:195-204)."""
     if periodicity.D == 3:
         return kspace_direct_3p(system, xi, kmax, targets)
     if periodicity.D == 2:
         return kspace_direct_2p(system, xi, kmax, targets)
-    if periodicity.D == 0:
-        return kspace_direct_0p(system, xi, targets)
-    raise NotImplementedError("the singly periodic direct sum is not provided on the device")
+    if periodicity.D == 1:
+        return kspace_direct_1p(system, xi, kmax, targets)
+    return kspace_direct_0p(system, xi, targets)
 
 
 def self_limit(q, xi: float) -> np.ndarray:

@@ -195,6 +195,12 @@ def direct_golden():
         out[f"d2_{i}_in"] = np.array([N, L, xi, kmax, 920 + i])
         out[f"d2_{i}_pos"], out[f"d2_{i}_q"] = s.positions, s.charges
         out[f"d2_{i}_phi"] = oracle.kspace_direct_2p(s, xi, kmax)
+    for i, (N, L, xi, eps) in enumerate([(14, 1.0, 6.3, 1e-12), (12, 2.0, 3.0, 1e-12)]):
+        s = system(N, L, 940 + i)
+        kmax = oracle.OracleConfig.for_accuracy(xi, L, eps).kmax
+        out[f"d1_{i}_in"] = np.array([N, L, xi, kmax, 940 + i])
+        out[f"d1_{i}_pos"], out[f"d1_{i}_q"] = s.positions, s.charges
+        out[f"d1_{i}_phi"] = oracle.kspace_direct_1p(s, xi, kmax)
     for i, (N, L, xi) in enumerate([(60, 1.0, 6.3), (50, 3.0, 2.0)]):
         s = system(N, L, 950 + i)
         out[f"d0_{i}_in"] = np.array([N, L, xi, 950 + i])
