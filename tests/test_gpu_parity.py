@@ -494,3 +494,45 @@ def test_realspace_geometry_sweep(D, L_over_rc, N):
     sel = rng.choice(N, min(N, 300), replace=False)
     ref = orc.realspace(pos, q, L, D, xi, rc, targets=sel)
     assert se.relative_rms_error(phi[sel], ref) < 1e-12
+
+
+# ----------------------------------------------- randomized configurations
+
+@pytest.mark.parametrize("case", range(24))
+def test_randomized_configurations_vs_oracle(case):
+    # seeded random (D, window, P incl. odd -- allowed for D = 0, 3 -- and
+    # > 16, M, xi, L, N, clustering): the full device pipeline against the
+    # CPU oracle
+    rng = np.random.default_rng(1000 + case)
+    D = int(rng.integers(0, 4))
+    window = ["bm", "gaussian", "kb"][int(rng.integers(0, 3))]
+    Ps = [4, 6, 8, 10, 12, 14, 18, 20] if D in (1, 2) else [3, 4, 5, 6, 7, 8, 10, 12, 17, 20]
+    P = int(rng.choice(Ps))
+    M = max(int(rng.choice([16, 18, 20, 24, 28])), P + P % 2)
+    L = float(rng.choice([0.7, 1.0, 2.3]))
+    N = int(rng.integers(40, 600))
+    xi = float(rng.uniform(4.0, 9.0)) / L
+    eps = 1e-10
+    rc = math.sqrt(-math.log(eps)) / xi
+    h = L / M
+    d = 3.0 - D
+    if D < 3:
+        s0 = max(1.0 + math.sqrt(d), ((1.0 + math.sqrt(d)) * L + 2.0 * rc) / (L + P * h))
+        R = 0.5 * (se.aft.padded_size(s0, M + P) * h - L + math.sqrt(d) * L)
+    else:
+        s0, R = 1.0, 0.0
+    s_up = max(1.0, math.log(1.0 / eps) / (2 * math.pi)) if D in (1, 2) else 1.0
+    nI = int(rng.integers(1, M // 2 + 1)) if D in (1, 2) else 0
+    prm = se.SEParams(xi=xi, rc=rc, M=M, P=P, window=window, shape=windows.default_shape(window, P),
+                      s0=s0, s=s_up, nI=nI, R=R, eps=eps)
+    s = rand_system(N, L, 2000 + case)
+    if case % 4 == 3:  # a tight cluster
+        pos = s.positions.copy()
+        pos[: N // 3] = np.mod(0.5 * L + rng.normal(scale=0.03 * L, size=(N // 3, 3)), L)
+        pos[pos >= L] = 0.0
+        s = se.ParticleSystem(pos, s.charges, L)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        phi = se.total_potential(s, prm, se.Periodicity(D))
+    ref = orc.total_potential(s.positions, s.charges, L, D, dict(prm.__dict__))
+    assert se.relative_rms_error(phi, ref) < 1e-11, (D, window, P, M, L, N)
