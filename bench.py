@@ -77,7 +77,7 @@ def peaks():
     micro-benchmarks (profiles/peaks_r01.json, tools/peaks.cu)."""
     out = {"hbm_gbs": 6655.0, "hbm_src": "fallback (B200_PROFILING.md)",
            "fp64_tflops": 37.0, "fp64_src": "fallback (datasheet ~37-40 TF/s)",
-           "smem_tbs": None}
+           "smem_tbs": None, "redg_gops": None}
     try:
         m = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         out["hbm_gbs"], out["hbm_src"] = float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
@@ -392,6 +392,40 @@ def run_ours(args):
             kern[k]["onchip_GBps"] = onchip / t / 1e9
             kern[k]["compulsory_GBps"] = (32 * N + 8 * G) / t / 1e9
             kern[k]["updates_per_s"] = N * P3 / t
+    # spreading / gathering measured alone (stage entry points, CUDA events on
+    # the plan's stream around each kernel): the SURVEY 8d bounds -- on-chip
+    # shared-memory RMW traffic vs the measured smem bandwidth, the update rate
+    # vs the measured global fp64 atomic (REDG) rate a direct-to-grid spread
+    # would be bound by, and the compulsory HBM traffic vs the HBM copy rate
+    spread_gather = None
+    if not sharded:
+        grid_d = torch.empty(G, dtype=torch.float64, device=dev)
+        plan.set_profiling(True)
+        for _ in range(5):
+            _native.call("se_spread_dev", plan.handle, _native.ptr(pos_d), _native.ptr(q_d), N, _native.ptr(grid_d))
+            _native.call("se_gather_dev", plan.handle, _native.ptr(grid_d), _native.ptr(pos_d), N,
+                         _native.ptr(phi_d), 0)
+        torch.cuda.synchronize(dev)
+        kt = plan.kernel_times()
+        plan.set_profiling(False)
+        sg = {}
+        for k, onchip_b in (("spread", 16), ("gather", 8)):
+            ms, n = kt.get(k, (0.0, 0))
+            if not n:
+                continue
+            t = ms / n * 1e-3
+            comp = 32 * N + 8 * G + (8 * N if k == "gather" else 0)
+            frac = lambda v, peak: v / peak if peak else None  # noqa: E731
+            sg[k] = {"ms_per_launch": ms / n, "updates_per_s": N * P3 / t,
+                     "onchip_GBps": onchip_b * N * P3 / t / 1e9,
+                     "frac_of_smem_peak": frac(onchip_b * N * P3 / t, (pk["smem_tbs"] or 0) * 1e12),
+                     "compulsory_hbm_GBps": comp / t / 1e9,
+                     "frac_of_hbm": frac(comp / t, pk["hbm_gbs"] * 1e9)}
+            if k == "spread":  # vs a spread that adds every update straight into the grid (REDG)
+                sg[k]["frac_of_redg_peak"] = frac(N * P3 / t, (pk["redg_gops"] or 0) * 1e9)
+        spread_gather = {"updates_per_launch": N * P3, **sg,
+                         "peaks": {"redg_gops": pk["redg_gops"], "smem_tbs": pk["smem_tbs"],
+                                   "hbm_gbs": pk["hbm_gbs"], "source": pk["fp64_src"]}}
     roofline = {"kernel": "realspace_cell_kernel (erfc pair sum)", "bound": "fp64",
                 "achieved": achieved, "peak": pk["fp64_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / pk["fp64_tflops"], "traffic": None,
@@ -412,6 +446,7 @@ def run_ours(args):
                        "parallelism": f"particle-shard x{world} (grid + phi sum-all-reduce)",
                        "l2": "flushed (256 MB write) between timed steps, outside the step events"},
             "e2e": e2e, "roofline": roofline, "kernels": kern,
+            "spread_gather": spread_gather,
             "kernels_note": ("event spans per stage on the stream it runs on; the k-space pipeline "
                              "(spread, kspace, gather, its sort) runs on a side stream concurrently with "
                              "the real-space kernel, so its spans include waiting for SM resources and "
