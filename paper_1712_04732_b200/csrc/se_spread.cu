@@ -176,6 +176,31 @@ __device__ __forceinline__ void for_tile_cells(const SpreadArgs &a, const int *g
 // Per-lane share of the P x P (y, z) footprint: lane handles pairs
 // pi = lane + 32 it; with compile-time P the pair coordinates are computed
 // once per CTA instead of per particle.
+// Tile geometry as a function of P alone (tile_setup's rule: the largest
+// tile edge T whose padded tile + batch staging fit kSmemFirst), so that the
+// compile-time-P kernels also know Tp, pitch and plane at compile time: the
+// stencil loads then use immediate offsets instead of per-load address math.
+constexpr int kBatch = 64;
+constexpr size_t kSmemFirst = 57 * 1024;  // measured: 98 KB 0.78/0.73 ms, 57 KB 0.60/0.45, 46 KB 0.65/0.55 (cfg2)
+constexpr int tile_pitch(int Tp, int P) { return P % 16 == 8 ? Tp + ((8 - Tp % 16) + 16) % 16 : Tp; }
+constexpr size_t tile_bytes(int T, int P) {
+    return sizeof(double) * ((size_t)(T + P - 1) * (T + P - 1) * tile_pitch(T + P - 1, P) + (size_t)kBatch * 3 * P) +
+           sizeof(int) * (4 * kBatch + 3 * (T + P - 1));
+}
+constexpr int tile_T(int P) {
+    constexpr int cand[] = {16, 14, 12, 10, 8, 6, 4, 2, 1};
+    for (int T : cand)
+        if (tile_bytes(T, P) <= kSmemFirst) return T;
+    return 0;
+}
+template <int PC>
+struct TileC {
+    static constexpr int T = PC > 0 ? tile_T(PC) : 0;
+    static constexpr int Tp = T > 0 ? T + PC - 1 : 0;
+    static constexpr int pitch = T > 0 ? tile_pitch(Tp, PC) : 0;
+    static constexpr int plane = Tp * pitch;
+};
+
 template <int PC>
 struct LanePairs {
     static constexpr int NPI = PC > 0 ? (PC * PC + 31) / 32 : 1;
@@ -201,7 +226,9 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
     int ubeg = (int)max((int64_t)un.y, a.rlo), uend = (int)min((int64_t)un.y + un.z, a.rhi);
     if (ubeg >= uend) return;
     extern __shared__ double smem[];
-    const int P = PC > 0 ? PC : a.P, Tp = a.Tp, pitch = a.pitch, plane = Tp * pitch;
+    // compile-time geometry for compile-time P (tile_setup checks it matches)
+    const int P = PC > 0 ? PC : a.P, Tp = TileC<PC>::T > 0 ? TileC<PC>::Tp : a.Tp,
+              pitch = TileC<PC>::T > 0 ? TileC<PC>::pitch : a.pitch, plane = Tp * pitch;
     const int ncell = Tp * plane;
     double *tile = smem;
     double *wts = tile + ncell;
@@ -272,7 +299,9 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
     int ubeg = (int)max((int64_t)un.y, a.rlo), uend = (int)min((int64_t)un.y + un.z, a.rhi);
     if (ubeg >= uend) return;
     extern __shared__ double smem[];
-    const int P = PC > 0 ? PC : a.P, Tp = a.Tp, pitch = a.pitch, plane = Tp * pitch;
+    // compile-time geometry for compile-time P (tile_setup checks it matches)
+    const int P = PC > 0 ? PC : a.P, Tp = TileC<PC>::T > 0 ? TileC<PC>::Tp : a.Tp,
+              pitch = TileC<PC>::T > 0 ? TileC<PC>::pitch : a.pitch, plane = Tp * pitch;
     const int ncell = Tp * plane;
     double *tile = smem;
     double *wts = tile + ncell;
@@ -428,7 +457,6 @@ static const int kUnit = 1024;     // particles per spreading work unit
 static const size_t kSmemCap = 200 * 1024;
 // preferred per-CTA budget: 4 CTAs per SM (the per-particle loop is latency
 // bound, so occupancy beats the smaller halo of larger tiles)
-static size_t kSmemFirst = 57 * 1024;  // measured: 98 KB 0.78/0.73 ms, 57 KB 0.60/0.45, 46 KB 0.65/0.55 (cfg2)
 
 void tile_setup(se_plan *pl) {
     TileGeom &t = pl->tile;
@@ -438,21 +466,17 @@ void tile_setup(se_plan *pl) {
     while (nw > 1 && P % nw) --nw;
     if (nw < 4 && P > 4) nw = P < 16 ? P : 16;  // keep enough warps even if nw does not divide P
     t.nwarps = nw;
-    t.batch = 64;
+    t.batch = kBatch;
     const int cand[] = {16, 14, 12, 10, 8, 6, 4, 2, 1};
     t.T = 0;
     for (size_t pass = 0; pass < 2 && !t.T; ++pass) {
         size_t cap = pass == 0 ? kSmemFirst : kSmemCap;
         for (int T : cand) {
-            int Tp = T + P - 1;
-            int pitch = Tp;
-            if (P % 16 == 8) pitch = Tp + ((8 - Tp % 16) + 16) % 16;
-            size_t bytes = sizeof(double) * ((size_t)Tp * Tp * pitch + (size_t)t.batch * 3 * P) +
-                           sizeof(int) * (4 * t.batch + 3 * Tp);
+            const size_t bytes = tile_bytes(T, P);  // the same rule as TileC (compile-time P)
             if (bytes <= cap) {
                 t.T = T;
-                t.Tp = Tp;
-                t.pitch = pitch;
+                t.Tp = T + P - 1;
+                t.pitch = tile_pitch(t.Tp, P);
                 t.smem = bytes;
                 break;
             }
