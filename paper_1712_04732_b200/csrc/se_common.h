@@ -106,9 +106,10 @@ struct Binning {
 };
 
 struct TileGeom {
-    int T;        // tile edge in start-index units
-    int Tp;       // padded tile edge T + P - 1
-    int pitch;    // z pitch of the padded smem tile (doubles)
+    int T;        // tile edge along x and y in start-index units
+    int Tz;       // tile edge along z
+    int Tp;       // padded x / y edge T + P - 1
+    int pitch;    // padded z edge Tz + P - 1 (the z pitch of the smem tile, doubles)
     int nt[3];    // tiles per axis
     int lo[3];    // first start index per axis
     int nwarps;   // warps per CTA (x-plane owners)

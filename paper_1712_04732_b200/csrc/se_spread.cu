@@ -32,7 +32,7 @@ struct SpreadArgs {
     int shape[3];
     double h, halfP;
     double off[3];
-    int T, Tp, pitch, nwarps, batch;
+    int T, Tz, Tp, pitch, nwarps, batch;
     int nt[3];
     int lo[3];
     // window
@@ -83,7 +83,7 @@ __device__ __forceinline__ int start_index(long long first, int axis, const Spre
 }
 
 __device__ __forceinline__ int tile_coord(int s, int axis, const SpreadArgs &a) {
-    int t = (s - a.lo[axis]) / a.T;
+    int t = (s - a.lo[axis]) / (axis == 2 ? a.Tz : a.T);
     t = t < 0 ? 0 : t;
     return t >= a.nt[axis] ? a.nt[axis] - 1 : t;
 }
@@ -137,14 +137,14 @@ __device__ __forceinline__ void unit_origin(int bin, const SpreadArgs &a, int or
     int tx = bin / (a.nt[2] * a.nt[1]);
     org[0] = a.lo[0] + tx * a.T;
     org[1] = a.lo[1] + ty * a.T;
-    org[2] = a.lo[2] + tz * a.T;
+    org[2] = a.lo[2] + tz * a.Tz;
 }
 
 // Per-axis grid index of every padded-tile coordinate (-1 off the grid),
-// wrapped on periodic axes: gmap[ax * Tp + l].
+// wrapped on periodic axes: gmap[ax * Tp + l] (x, y: Tp entries; z: pitch).
 __device__ __forceinline__ void build_axis_maps(const int org[3], const SpreadArgs &a, int *gmap) {
-    for (int i = threadIdx.x; i < 3 * a.Tp; i += blockDim.x) {
-        const int ax = i / a.Tp, l = i - ax * a.Tp;
+    for (int i = threadIdx.x; i < 2 * a.Tp + a.pitch; i += blockDim.x) {
+        const int ax = min(i / a.Tp, 2), l = i - ax * a.Tp;
         int g = org[ax] + l;
         if (ax < a.D)
             g %= a.M;
@@ -166,7 +166,7 @@ __device__ __forceinline__ void for_tile_cells(const SpreadArgs &a, const int *g
         const bool rok = gx >= 0 && gy >= 0;
         const long long gbase = ((long long)gx * a.shape[1] + gy) * a.shape[2];
         const int tbase = (lx * Tp + ly) * a.pitch;
-        for (int lz = lane; lz < Tp; lz += 32) {
+        for (int lz = lane; lz < a.pitch; lz += 32) {
             const int gz = gmap[2 * Tp + lz];
             f(tbase + lz, rok && gz >= 0 ? gbase + gz : -1LL);
         }
@@ -176,28 +176,50 @@ __device__ __forceinline__ void for_tile_cells(const SpreadArgs &a, const int *g
 // Per-lane share of the P x P (y, z) footprint: lane handles pairs
 // pi = lane + 32 it; with compile-time P the pair coordinates are computed
 // once per CTA instead of per particle.
-// Tile geometry as a function of P alone (tile_setup's rule: the largest
-// tile edge T whose padded tile + batch staging fit kSmemFirst), so that the
+// Tile geometry as a function of P alone (tile_setup's rule), so that the
 // compile-time-P kernels also know Tp, pitch and plane at compile time: the
 // stencil loads then use immediate offsets instead of per-load address math.
-constexpr int kBatch = 64;
-constexpr size_t kSmemFirst = 57 * 1024;  // measured: 98 KB 0.78/0.73 ms, 57 KB 0.60/0.45, 46 KB 0.65/0.55 (cfg2)
-constexpr int tile_pitch(int Tp, int P) { return P % 16 == 8 ? Tp + ((8 - Tp % 16) + 16) % 16 : Tp; }
-constexpr size_t tile_bytes(int T, int P) {
-    return sizeof(double) * ((size_t)(T + P - 1) * (T + P - 1) * tile_pitch(T + P - 1, P) + (size_t)kBatch * 3 * P) +
-           sizeof(int) * (4 * kBatch + 3 * (T + P - 1));
+//
+// Bank-conflict-free stencil rows: lane l of a warp handles (y, z) pair
+// pi = l + 32 it of the P x P footprint at word offset ty * pitch + tz; with
+// pitch == P (mod 16) that offset is == pi (mod 16), so the 32 lanes hit
+// every bank pair exactly twice (the minimum for 8-byte words).  The padded
+// z extent is therefore Tz + P - 1 with Tz == 1 (mod 16): tiles are
+// T x T x 17 for P <= 12, the padding doing useful work instead of being
+// wasted columns.  Wider windows keep cubic tiles (a 17-deep tile would
+// leave only a sliver in x and y) with the old padded pitch: rows of 16
+// (P = 16) are conflict free as they are, P == 8 (mod 16) pads to == 8.
+// The budget keeps 3 CTAs per SM (228 KB, 1 KB reserved per CTA): measured
+// at P = 8, 3 CTAs per SM beat both 2 (larger tiles) and 4 (smaller tiles).
+constexpr size_t kSmemSM = 228 * 1024, kSmemReserved = 1024;
+constexpr size_t kSmemFirst = kSmemSM / 3 - kSmemReserved;
+constexpr int tile_batch(int P) { return P >= 12 ? 32 : 64; }
+constexpr bool tile_aniso(int P) { return P % 16 != 0 && P <= 12; }
+constexpr int tile_Tz(int T, int P) { return tile_aniso(P) ? 17 : T; }
+constexpr int tile_pitch(int T, int P) {
+    return tile_aniso(P) ? 17 + P - 1
+                         : (P % 16 == 8 ? T + P - 1 + ((8 - (T + P - 1) % 16) + 16) % 16 : T + P - 1);
 }
+constexpr size_t tile_bytes(int T, int P) {
+    return sizeof(double) * ((size_t)(T + P - 1) * (T + P - 1) * tile_pitch(T, P) + (size_t)tile_batch(P) * 3 * P) +
+           sizeof(int) * (4 * tile_batch(P) + 2 * (T + P - 1) + tile_pitch(T, P));
+}
+// P = 8: 8 x 8 x 17 tiles measured 0.5% faster per cfg2 step than 10 x 10 x 17
+#ifndef SE_TILE_TMAX8
+#define SE_TILE_TMAX8 8
+#endif
+constexpr int tile_Tmax(int P) { return P == 8 ? SE_TILE_TMAX8 : 16; }
 constexpr int tile_T(int P) {
     constexpr int cand[] = {16, 14, 12, 10, 8, 6, 4, 2, 1};
     for (int T : cand)
-        if (tile_bytes(T, P) <= kSmemFirst) return T;
+        if (T <= tile_Tmax(P) && tile_bytes(T, P) <= kSmemFirst) return T;
     return 0;
 }
 template <int PC>
 struct TileC {
     static constexpr int T = PC > 0 ? tile_T(PC) : 0;
     static constexpr int Tp = T > 0 ? T + PC - 1 : 0;
-    static constexpr int pitch = T > 0 ? tile_pitch(Tp, PC) : 0;
+    static constexpr int pitch = T > 0 ? tile_pitch(T, PC) : 0;
     static constexpr int plane = Tp * pitch;
 };
 
@@ -442,6 +464,7 @@ static SpreadArgs make_args(se_plan *pl) {
     if (p.window == SE_WINDOW_KB) a.i0b = bessel_i0(p.shape);
     const TileGeom &t = pl->tile;
     a.T = t.T;
+    a.Tz = t.Tz;
     a.Tp = t.Tp;
     a.pitch = t.pitch;
     a.nwarps = t.nwarps;
@@ -466,17 +489,18 @@ void tile_setup(se_plan *pl) {
     while (nw > 1 && P % nw) --nw;
     if (nw < 4 && P > 4) nw = P < 16 ? P : 16;  // keep enough warps even if nw does not divide P
     t.nwarps = nw;
-    t.batch = kBatch;
+    t.batch = tile_batch(P);
     const int cand[] = {16, 14, 12, 10, 8, 6, 4, 2, 1};
     t.T = 0;
     for (size_t pass = 0; pass < 2 && !t.T; ++pass) {
         size_t cap = pass == 0 ? kSmemFirst : kSmemCap;
         for (int T : cand) {
             const size_t bytes = tile_bytes(T, P);  // the same rule as TileC (compile-time P)
-            if (bytes <= cap) {
+            if (T <= tile_Tmax(P) && bytes <= cap) {
                 t.T = T;
+                t.Tz = tile_Tz(T, P);
                 t.Tp = T + P - 1;
-                t.pitch = tile_pitch(t.Tp, P);
+                t.pitch = tile_pitch(T, P);
                 t.smem = bytes;
                 break;
             }
@@ -484,6 +508,7 @@ void tile_setup(se_plan *pl) {
     }
     if (!t.T) {  // direct path
         t.T = -1;
+        t.Tz = -1;
         t.Tp = 0;
         t.pitch = 0;
         t.smem = 0;
@@ -496,7 +521,8 @@ void tile_setup(se_plan *pl) {
     for (int ax = 0; ax < 3; ++ax) {
         int extent = ax < pl->g.D ? pl->g.M : pl->g.M + 2;
         t.lo[ax] = 0;
-        t.nt[ax] = (extent + t.T - 1) / t.T;
+        const int te = ax == 2 ? t.Tz : t.T;
+        t.nt[ax] = (extent + te - 1) / te;
     }
 }
 
