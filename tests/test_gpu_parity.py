@@ -179,6 +179,37 @@ def test_spread_gather_adjoint_all_periodicities():
             assert lhs == pytest.approx(rhs, rel=1e-13)
 
 
+@pytest.mark.parametrize("P", list(range(2, 19)) + [20, 24])
+def test_spread_gather_tile_geometry_sweep(P):
+    # every window width against the oracle's stencils: anisotropic 17-deep
+    # tiles (P <= 12), cubic ones above, compile-time and runtime P, tiles
+    # clipped at the free-axis ends and wrapped on periodic axes, a cluster
+    # that splits one tile into several work units
+    rng = np.random.default_rng(300 + P)
+    for D in ((0, 3) if P % 2 else (0, 1, 2, 3)):
+        M = max(P + 2, 38) + (P % 2 if D in (1, 2) else 0)
+        N = 2500
+        pos = rng.random((N, 3))
+        pos[:1200] = np.mod(0.37 + rng.normal(scale=0.01, size=(1200, 3)), 1.0)
+        pos[pos >= 1.0] = 0.0
+        q = rng.uniform(-1, 1, N)
+        window = ("bm", "gaussian", "kb")[P % 3]
+        shape = windows.default_shape(window, P)
+        p = se.SEParams(xi=6.0, rc=0.4, M=M, P=P, window=window, shape=shape, s0=3.0, R=2.0)
+        peri = se.Periodicity(D)
+        grid = sekspace.Grid.build(1.0, p, peri)
+        wspec = windows.WindowSpec(window, P, grid.h, shape)
+        s = se.ParticleSystem(pos, q, 1.0)
+        H = sekspace.spread(s, wspec, grid, peri).values
+        g = orc.geometry(1.0, D, M, P, 3.0, 1.0, 2.0)
+        ref = orc.spread(pos, q, g, window, shape)
+        assert np.max(np.abs(H - ref)) <= 1e-13 * np.max(np.abs(ref)), (P, D)
+        G = rng.normal(size=grid.shape)
+        phi = sekspace.gather(sekspace.GridField(G, grid), s, wspec, peri)
+        rphi = orc.gather(G, pos, g, window, shape)
+        assert np.max(np.abs(phi - rphi)) <= 1e-13 * np.max(np.abs(rphi)), (P, D)
+
+
 def test_spread_on_node_tensor_window_and_count():
     M, P = 16, 6
     p = se.SEParams(xi=5.0, rc=0.4, M=M, P=P, window="bm", shape=15.0, s0=3.0, R=2.0)
