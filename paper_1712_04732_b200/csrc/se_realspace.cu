@@ -11,8 +11,9 @@
 //  * one warp per unit = 16 consecutive targets of a column (a thin z-slab);
 //  * for each neighbour column within +-3 (half shell with Newton's third
 //    law), the z-window that can hold partners, |dz| <= sqrt(rc^2 - gap^2)
-//    around the slab, is found by a warp-cooperative search in the column,
-//    and only that run is streamed (~2.1x the in-cutoff pairs instead of
+//    around the slab, is found by a binary search in the column (one lane per
+//    column, all columns of the half shell at once), and only that run is
+//    streamed (~2.1x the in-cutoff pairs instead of
 //    ~3.7x for 5x5x5 rc/2 cells); periodic z adds the window's wrapped parts
 //    as shifted images;
 //  * sources are staged 32 at a time in the warp's shared workspace with the
@@ -105,15 +106,17 @@ __global__ void cell_keys_hist_kernel(const double *__restrict__ pos, int64_t N,
         if (hist[b]) atomicAdd(&counts[b], hist[b]);
 }
 
-// erfc(x), x >= 0, as exp(-x^2) erfcx(x): erfcx by a degree-14 polynomial in
-// s = A t + B, t = (x - K)/(x + K), and exp by Cody-Waite reduction;
-// coefficients are __constant__ operands (tools/gen_erfc_coeffs.py: fitted
-// for absolute accuracy, max error 7.6e-17 absolute / 7.6e-10 relative on
-// [0, 6] -- the pair term's 1/r rounding is ~1e-16 relative).  The x^2 rounding
-// residual is not carried: it moves exp(-x^2) by <= x^2 2^-53 relative,
-// i.e. <= 4e-17 absolute, below the 1/r rounding of the pair term.
-// Beyond SE_ERFC_XMAX the library erfc is used.
-//
+// Scalar constants of erfc_fast as one constant-bank block (read two per
+// LDCU.128 instead of materialised as 64-bit immediates per use).
+__constant__ double se_erfc_k[6] = {
+    SE_ERFC_A + SE_ERFC_B,                // s = ((A+B) x + K (B-A)) / (x + K)
+    SE_ERFC_K * (SE_ERFC_B - SE_ERFC_A),  //   (K = 4: an immediate)
+    -SE_LOG2E,                            // n = rint(-x^2 log2 e)
+    -SE_LN2_HI,                           // r = -x^2 - n ln2 (Cody-Waite)
+    -SE_LN2_LO,
+    0.375};                               // rsqrt_nr: a 64-bit constant operand, not
+                                          //   two IMAD.MOVs per use
+
 // 1/d and 1/sqrt(d): the MUFU approximations (~2^-22 relative) and one
 // third-order correction each (error O(e^3): ~1 ulp), branch-free; d is a
 // positive normal number here.
@@ -127,18 +130,18 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
     const double e = fma(-d * y, y, 1.0);  // d^-1/2 = y (1 - e)^-1/2 = y (1 + e/2 + 3e^2/8 + ...)
-    return fma(y, e * fma(e, 0.375, 0.5), y);
+    return fma(y, e * fma(e, se_erfc_k[5], 0.5), y);
 }
 
-// Scalar constants of erfc_fast as one constant-bank block (read two per
-// LDCU.128 instead of materialised as 64-bit immediates per use).
-__constant__ double se_erfc_k[5] = {
-    SE_ERFC_A + SE_ERFC_B,                // s = ((A+B) x + K (B-A)) / (x + K)
-    SE_ERFC_K * (SE_ERFC_B - SE_ERFC_A),  //   (K = 4: an immediate)
-    -SE_LOG2E,                            // n = rint(-x^2 log2 e)
-    -SE_LN2_HI,                           // r = -x^2 - n ln2 (Cody-Waite)
-    -SE_LN2_LO};
-
+// erfc(x), x >= 0, as exp(-x^2) erfcx(x): erfcx by a degree-14 polynomial in
+// s = A t + B, t = (x - K)/(x + K), and exp by Cody-Waite reduction;
+// coefficients are __constant__ operands (tools/gen_erfc_coeffs.py: fitted
+// for absolute accuracy, max error 7.6e-17 absolute / 7.6e-10 relative on
+// [0, 6] -- the pair term's 1/r rounding is ~1e-16 relative).  The x^2 rounding
+// residual is not carried: it moves exp(-x^2) by <= x^2 2^-53 relative,
+// i.e. <= 4e-17 absolute, below the 1/r rounding of the pair term.
+// Beyond SE_ERFC_XMAX the library erfc is used.
+//
 // erfc(x) * w.  WIDE: x may exceed SE_ERFC_XMAX (xi rc > 6, i.e. eps < 2e-16).
 // Otherwise the caller guarantees x <= SE_ERFC_XMAX (1 + 1e-4) for every
 // evaluated pair (beyond the cutoff the result is multiplied by w = 0), and
@@ -177,8 +180,9 @@ constexpr int kT = 16;     // targets per warp unit: lane l tests target l % 16 
 
 // Shared-memory workspace of one warp unit (7 KB: 8 blocks x 4 warps per SM).
 struct __align__(16) WarpBuf {
-    double tx[kT], ty[kT], tz[kT], tq[kT];  // the unit's targets (SoA)
-    double sx[32], sy[32], sz[32], sq[32];  // current source batch (SoA: hits read random k)
+    double2 txy[kT], tzq[kT];    // the unit's targets: (x, y), (z, q) -- one LDS.128 each
+    double2 sxy[32], szq[32];    // current source batch, likewise (16-B stride: a warp's
+                                 // random reads cost the minimum 4 wavefronts per LDS.128)
     float4 sf[32];               // the same in fp32 for the prefilter
     double acc[kT][32];          // per-lane private accumulators acc[t][lane]: lane-owned banks
     unsigned short ent[kT * 32];  // compacted hits of a batch: (target << 5) | source
@@ -199,17 +203,21 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 struct Hit {
     double f;   // erfc(xi r)/r, 0 outside the cutoff
     double qt;  // target charge (source-side update with NEWTON)
+    double qs;  // source charge (target-side update)
     int tt, k;
     bool ok;
 };
 
-template <bool MI, bool NEWTON, bool WIDE>
-__device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const WarpBuf &wb, int jb, int tbase,
-                                        int &singular) {
-    Hit h;
+// Geometry of one hit up to the erfc argument: h.f = w (1/r, or 0 outside
+// the cutoff or for an invalid slot), returns x = xi r.
+template <bool MI, bool NEWTON>
+__device__ __forceinline__ double hit_geometry(unsigned en, bool valid, const RealArgs &a, const WarpBuf &wb, int jb,
+                                               int tbase, int &singular, Hit &h) {
     h.tt = (int)(en >> 5);
     h.k = (int)(en & 31u);
-    double dx = wb.tx[h.tt] - wb.sx[h.k], dy = wb.ty[h.tt] - wb.sy[h.k], dz = wb.tz[h.tt] - wb.sz[h.k];
+    const double2 t01 = wb.txy[h.tt], t23 = wb.tzq[h.tt];
+    const double2 s01 = wb.sxy[h.k], s23 = wb.szq[h.k];
+    double dx = t01.x - s01.x, dy = t01.y - s01.y, dz = t23.x - s23.x;
     if (MI) {
         if (a.mode[0] == 2) dx = min_image(dx, a.L);
         if (a.mode[1] == 2) dy = min_image(dy, a.L);
@@ -218,18 +226,31 @@ __device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const Wa
     const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
     // r < 1e-14: the self pair (never compacted with NEWTON) or a coincidence
     const bool zero = r2 < 1e-28;
-    if (NEWTON)
+    double r2s;
+    if (NEWTON) {
+        // any zero distance is a coincidence: the call raises and its
+        // result (here NaN for r = 0) is discarded -- no select needed
         singular |= zero ? 1 : 0;
-    else
+        r2s = r2;
+    } else {
         singular |= (zero && jb + h.k != tbase + h.tt) ? 1 : 0;
-    // a coincident pair is evaluated at r = rc (keeps x in range) and dropped
-    const double r2s = zero ? a.rc2 : r2;
+        r2s = zero ? a.rc2 : r2;  // the self pair: evaluated at r = rc and dropped
+    }
     const double rinv = rsqrt_nr(r2s);
     const double rr = r2s * rinv;
-    h.ok = !zero && rr < a.rc;
-    // evaluated unconditionally (a select, not a branch, on ok)
-    h.f = erfc_fast<WIDE>(a.xi * rr, h.ok ? rinv : 0.0);
-    h.qt = wb.tq[h.tt];
+    h.ok = valid && rr < a.rc && (NEWTON || !zero);
+    h.f = h.ok ? rinv : 0.0;  // a select, not a branch: the erfc runs unconditionally
+    h.qt = t23.y;
+    h.qs = s23.y;
+    return a.xi * rr;
+}
+
+template <bool MI, bool NEWTON, bool WIDE>
+__device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const WarpBuf &wb, int jb, int tbase,
+                                        int &singular) {
+    Hit h;
+    const double x = hit_geometry<MI, NEWTON>(en, true, a, wb, jb, tbase, singular, h);
+    h.f = erfc_fast<WIDE>(x, h.f);
     return h;
 }
 
@@ -238,7 +259,7 @@ __device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const Wa
 template <bool NEWTON>
 __device__ __forceinline__ void apply_hit(const Hit &h, WarpBuf &wb, int lane, double *__restrict__ acc_batch) {
     double *slot = &wb.acc[h.tt][lane];
-    *slot = fma(wb.sq[h.k], h.f, *slot);
+    *slot = fma(h.qs, h.f, *slot);
     if (NEWTON && h.ok) atomicAdd(acc_batch + h.k, h.qt * h.f);
 }
 
@@ -289,10 +310,8 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     if (j < j1) {
         const double4 r = rec[j];
         const double xs = r.x + shx, ys = r.y + shy, zs = r.z + shz;
-        wb.sx[lane] = xs;
-        wb.sy[lane] = ys;
-        wb.sz[lane] = zs;
-        wb.sq[lane] = r.w;
+        wb.sxy[lane] = make_double2(xs, ys);
+        wb.szq[lane] = make_double2(zs, r.w);
         if (MI) {
             wb.sf[lane] = make_float4((float)xs, (float)ys, (float)zs, 0.f);
         } else {
@@ -374,10 +393,11 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
             const bool v2 = lane < rem - 32;
             const unsigned en1 = wb.ent[e0 + lane];
             const unsigned en2 = v2 ? wb.ent[e0 + 32 + lane] : en1;
-            Hit h1 = eval_hit<MI, NEWTON, WIDE>(en1, a, wb, jb, tbase, singular);
-            Hit h2 = eval_hit<MI, NEWTON, WIDE>(en2, a, wb, jb, tbase, singular);
-            h2.ok = h2.ok && v2;
-            h2.f = v2 ? h2.f : 0.0;
+            Hit h1, h2;
+            const double x1 = hit_geometry<MI, NEWTON>(en1, true, a, wb, jb, tbase, singular, h1);
+            const double x2 = hit_geometry<MI, NEWTON>(en2, v2, a, wb, jb, tbase, singular, h2);
+            h1.f = erfc_fast<WIDE>(x1, h1.f);
+            h2.f = erfc_fast<WIDE>(x2, h2.f);
             if (COUNT) {
                 cnt += (h1.ok ? (NEWTON ? 2 : 1) : 0) + (h2.ok ? (NEWTON ? 2 : 1) : 0);
             } else {
@@ -395,31 +415,19 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     __syncwarp();
 }
 
-// First index j in [lo, hi) of a z-run with Q(z_j) >= qt (upper: > qt), or
-// hi: a warp-cooperative 32-ary search (the run is sorted by Q up to one
-// quantum at cell seams; callers widen qt by two quanta).
-__device__ __forceinline__ int zsearch(const double4 *__restrict__ rec, int lo, int hi, int qt, bool upper,
-                                       double qinv, int lane) {
-    auto pred = [&](int p) {
-        if (p >= hi) return true;
-        const int qz = zq(__ldg(&rec[p].z), qinv);
-        return upper ? qz > qt : qz >= qt;
-    };
-    while (hi - lo > 32) {
-        const int step = (hi - lo + 31) >> 5;
-        const unsigned m = __ballot_sync(0xffffffffu, pred(lo + lane * step));
-        if (m == 0) {
-            lo += 31 * step + 1;
-            continue;
-        }
-        const int k = __ffs(m) - 1;
-        if (k == 0) return lo;
-        hi = min(hi, lo + k * step);
-        lo += (k - 1) * step + 1;
+// First index j in [lo, hi) with
+// Q(z_j) >= qt (upper: > qt), or hi, by bisection.
+__device__ __forceinline__ int zbound(const double4 *__restrict__ rec, int lo, int hi, int qt, bool upper,
+                                      double qinv) {
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const int qz = zq(__ldg(&rec[mid].z), qinv);
+        if (upper ? qz > qt : qz >= qt)
+            hi = mid;
+        else
+            lo = mid + 1;
     }
-    if (lo >= hi) return hi;
-    const unsigned m = __ballot_sync(0xffffffffu, pred(lo + lane));
-    return m ? lo + __ffs(m) - 1 : hi;
+    return lo;
 }
 
 // NEWTON: every unordered pair once -- neighbour cells in the half shell
@@ -447,10 +455,8 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
     if (__ballot_sync(0xffffffffu, active) == 0) return;
     const double4 tp = active ? rec[t] : make_double4(0, 0, 0, 0);
     if (lane < kT) {
-        wb.tx[lane] = tp.x;
-        wb.ty[lane] = tp.y;
-        wb.tz[lane] = tp.z;
-        wb.tq[lane] = tp.w;
+        wb.txy[lane] = make_double2(tp.x, tp.y);
+        wb.tzq[lane] = make_double2(tp.z, tp.w);
     }
     for (int i = 0; i < kT; ++i) wb.acc[i][lane] = 0.0;
     // z extent of the unit's targets (a unit is a z-slab of its column)
@@ -475,7 +481,7 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int sl = h ? pt.tb : pt.ta;
-            const double4 q = make_double4(wb.tx[sl], wb.ty[sl], wb.tz[sl], 0.0);
+            const double4 q = make_double4(wb.txy[sl].x, wb.txy[sl].y, wb.tzq[sl].x, 0.0);
             const bool ok = (amask >> sl) & 1u;
             if (MI) {
                 v[h][0] = (float)q.x;
@@ -498,73 +504,83 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
     int singular = 0;
     long long cnt = 0;
 
-    auto axis_range = [&](int c, int mode, int &lo, int &hi) {
-        if (mode == 2) {
-            lo = 0;
-            hi = n - 1;
-        } else if (mode == 1) {
-            lo = c - a.reach;
-            hi = c + a.reach;
-        } else {
-            lo = max(0, c - a.reach);
-            hi = min(n - 1, c + a.reach);
-        }
-    };
-    int xlo, xhi, ylo, yhi;
-    axis_range(cx, a.mode[0], xlo, xhi);
-    axis_range(cy, a.mode[1], ylo, yhi);
-    if (NEWTON) xlo = cx;  // ox >= 0
     auto run = [&](int j0, int j1, double shx, double shy, double shz, int hs) {
         for (int jb = j0; jb < j1; jb += 32)
             pair_batch<MI, COUNT, NEWTON, WIDE>(rec, jb, j1, shx, shy, shz, a, wb, lane, pt, org, un.y, hs, acc_src,
                                                 singular, cnt);
     };
-    for (int ox = xlo; ox <= xhi; ++ox) {
-        int xc = ox;
-        double shx = 0.0;
-        if (a.mode[0] == 1) {
-            if (xc < 0) { xc += n; shx = -a.L; }
-            else if (xc >= n) { xc -= n; shx = a.L; }
-        }
-        const int ylo2 = (NEWTON && ox == cx) ? cy : ylo;  // ox == 0: oy >= 0
-        for (int oy = ylo2; oy <= yhi; ++oy) {
-            int yc = oy;
-            double shy = 0.0;
+    if (MI) {
+        // every column once, the whole column, minimum image in the distance
+        for (int xc = 0; xc < n; ++xc)
+            for (int yc = 0; yc < n; ++yc) {
+                const int cs = starts[xc * n + yc], ce = starts[xc * n + yc + 1];
+                if (cs < ce) run(cs, ce, 0.0, 0.0, 0.0, -1);
+            }
+    } else {
+        // The half shell's columns, one per lane (<= 25 for reach 3): own
+        // row (ox = cx, oy = cy .. cy + R), then rows ox = cx + 1 .. cx + R
+        // (oy = cy - R .. cy + R).  Each lane locates its column's runs by a
+        // scalar binary search, all columns concurrently (the searches were
+        // a chain of dependent L2 loads per column).  Sources with
+        // |z_s - z_t| <= h, h^2 = rc^2 - (lateral gap)^2, for some target can
+        // be within rc (one quantum of slack each side):
+        //   [j0, j1)  in-box window (own column: sources above the unit, j > t)
+        //   [k0, ce)  the window's part below z = 0, as the image shifted by -L
+        //   [cs, k1)  its part above z = L, shifted by +L (periodic z only)
+        const int R = a.reach, nc = (R + 1) + R * (2 * R + 1);
+        int j0 = 0, j1 = 0, k0 = 0, k1 = 0, cs = 0, ce = 0, shc = 0;  // shc: x, y image codes (-1, 0, 1)
+        if (lane < nc) {
+            int ox, oy;
+            if (lane <= R) {
+                ox = cx;
+                oy = cy + lane;
+            } else {
+                const int i = lane - R - 1;
+                ox = cx + 1 + i / (2 * R + 1);
+                oy = cy - R + i % (2 * R + 1);
+            }
+            int xc = ox, yc = oy, sx = 0, sy = 0;
+            bool ok = true;
+            if (a.mode[0] == 1) {
+                if (xc >= n) { xc -= n; sx = 1; }
+            } else {
+                ok = ok && xc < n;
+            }
             if (a.mode[1] == 1) {
-                if (yc < 0) { yc += n; shy = -a.L; }
-                else if (yc >= n) { yc -= n; shy = a.L; }
+                if (yc < 0) { yc += n; sy = -1; }
+                else if (yc >= n) { yc -= n; sy = 1; }
+            } else {
+                ok = ok && yc >= 0 && yc < n;
             }
-            const int cs = starts[xc * n + yc], ce = starts[xc * n + yc + 1];
-            if (cs == ce) continue;
-            if (MI) {  // whole column; minimum image in the distance
-                run(cs, ce, shx, shy, 0.0, -1);
-                continue;
-            }
-            // only sources with |z_s - z_t| <= h, h^2 = rc^2 - (lateral gap)^2,
-            // for some target can be within rc: the column is searched for
-            // that z-window (one quantum of slack each side)
-            const double gx = max(abs(ox - cx) - 1, 0) * a.edge, gy = max(abs(oy - cy) - 1, 0) * a.edge;
+            const double gx = max(ox - cx - 1, 0) * a.edge, gy = max(abs(oy - cy) - 1, 0) * a.edge;
             const double h2 = a.rc2 - gx * gx - gy * gy;
-            if (h2 < 0.0) continue;
-            const double h = sqrt(h2);
-            const double wlo = zmin - h, whi = zmax + h;
-            const bool own = NEWTON && ox == cx && oy == cy;
-            // in-box images: own column -> sources above the unit (j > t)
-            const int j0 = own ? un.y + 1 : zsearch(rec, cs, ce, zq(wlo, a.qinv) - 1, false, a.qinv, lane);
-            const int j1 = zsearch(rec, j0, ce, zq(whi, a.qinv) + 1, true, a.qinv, lane);
-            if (j0 < j1) run(j0, j1, shx, shy, 0.0, own ? un.y : -1);
-            if (a.zper) {
-                // periodic z: the window's parts beyond [0, L) as shifted images
-                // (the own column takes only the images above: half shell)
-                if (!own && wlo < 0.0) {
-                    const int k0 = zsearch(rec, cs, ce, zq(wlo + a.L, a.qinv) - 1, false, a.qinv, lane);
-                    if (k0 < ce) run(k0, ce, shx, shy, -a.L, -1);
+            ok = ok && h2 >= 0.0;
+            if (ok) {
+                cs = starts[xc * n + yc];
+                ce = starts[xc * n + yc + 1];
+                const double h = sqrt(h2);
+                const double wlo = zmin - h, whi = zmax + h;
+                const bool own = lane == 0;
+                j0 = own ? un.y + 1 : zbound(rec, cs, ce, zq(wlo, a.qinv) - 1, false, a.qinv);
+                j1 = zbound(rec, j0, ce, zq(whi, a.qinv) + 1, true, a.qinv);
+                k0 = ce;
+                k1 = cs;
+                if (a.zper) {
+                    if (!own && wlo < 0.0) k0 = zbound(rec, cs, ce, zq(wlo + a.L, a.qinv) - 1, false, a.qinv);
+                    if (whi >= a.L) k1 = zbound(rec, cs, ce, zq(whi - a.L, a.qinv) + 1, true, a.qinv);
                 }
-                if (whi >= a.L) {
-                    const int k1 = zsearch(rec, cs, ce, zq(whi - a.L, a.qinv) + 1, true, a.qinv, lane);
-                    if (cs < k1) run(cs, k1, shx, shy, a.L, -1);
-                }
+                shc = (sx + 1) * 3 + (sy + 1);
             }
+        }
+        for (int c = 0; c < nc; ++c) {
+            const int c0 = __shfl_sync(0xffffffffu, j0, c), c1 = __shfl_sync(0xffffffffu, j1, c);
+            const int ck0 = __shfl_sync(0xffffffffu, k0, c), cce = __shfl_sync(0xffffffffu, ce, c);
+            const int ccs = __shfl_sync(0xffffffffu, cs, c), ck1 = __shfl_sync(0xffffffffu, k1, c);
+            const int code = __shfl_sync(0xffffffffu, shc, c);
+            const double shx = (code / 3 - 1) * a.L, shy = (code % 3 - 1) * a.L;
+            if (c0 < c1) run(c0, c1, shx, shy, 0.0, c == 0 ? un.y : -1);
+            if (ck0 < cce) run(ck0, cce, shx, shy, -a.L, -1);
+            if (ccs < ck1) run(ccs, ck1, shx, shy, a.L, -1);
         }
     }
     if (COUNT) {
