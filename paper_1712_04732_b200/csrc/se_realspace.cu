@@ -195,6 +195,10 @@ struct __align__(16) WarpBuf {
 // Entries and acc rows are indexed by slot.
 __device__ __forceinline__ int tslot(int t) { return t ^ ((t >> 3) << 2); }
 
+// Fire-and-forget L1 prefetch of a record the warp stages later (the staging
+// load otherwise waits a full L2 round trip per batch).
+__device__ __forceinline__ void prefetch_l1(const double4 *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
     for (int o = 1; o < 32; o <<= 1) {
         int y = __shfl_up_sync(0xffffffffu, v, o);
@@ -316,6 +320,7 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     const int j = jb + lane;
     if (j < j1) {
         const double4 r = rec[j];
+        if (j + 32 < j1) prefetch_l1(rec + j + 32);  // the run's next batch
         const double xs = r.x + shx, ys = r.y + shy, zs = r.z + shz;
         wb.sxy[lane] = make_double2(xs, ys);
         wb.szq[lane] = make_double2(zs, r.w);
@@ -585,6 +590,10 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
             const int ck0 = __shfl_sync(0xffffffffu, k0, c), cce = __shfl_sync(0xffffffffu, ce, c);
             const int ccs = __shfl_sync(0xffffffffu, cs, c), ck1 = __shfl_sync(0xffffffffu, k1, c);
             const int code = __shfl_sync(0xffffffffu, shc, c);
+            {   // the next column's first batch
+                const int n0 = __shfl_sync(0xffffffffu, j0, (c + 1) & 31), n1 = __shfl_sync(0xffffffffu, j1, (c + 1) & 31);
+                if (c + 1 < nc && n0 + lane < n1) prefetch_l1(rec + n0 + lane);
+            }
             const double shx = (code / 3 - 1) * a.L, shy = (code % 3 - 1) * a.L;
             if (c0 < c1) run(c0, c1, shx, shy, 0.0, c == 0 ? un.y : -1);
             if (ck0 < cce) run(ck0, cce, shx, shy, -a.L, -1);
