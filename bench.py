@@ -256,6 +256,34 @@ def run_reference(args):
 
 # -------------------------------------------------------------- our pipeline
 
+class _PlanGroup:
+    """Profiling view over the sharded backend's plans (real space on the
+    main stream, the k-space chain on the side stream); `handle` is the
+    real-space plan (pair count)."""
+
+    def __init__(self, plans):
+        self.plans = plans
+        self.handle = plans[0].handle
+
+    def set_profiling(self, on):
+        for p in self.plans:
+            p.set_profiling(on)
+
+    def grid(self):
+        return self.plans[0].grid()
+
+    def launches(self):
+        return sum(p.launches() for p in self.plans)
+
+    def kernel_times(self):
+        out = {}
+        for p in self.plans:
+            for k, (ms, n) in p.kernel_times().items():
+                a = out.get(k, (0.0, 0))
+                out[k] = (a[0] + ms, a[1] + n)
+        return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -289,10 +317,10 @@ def run_ours(args):
 
     if sharded:
         backend = NativeBackend(L, prm, peri, dev)
-        plan = backend.plan
+        plan = _PlanGroup(backend.plans)
 
         def step():
-            return total_potential_sharded(pos_d, q_d, backend)
+            return total_potential_sharded(pos_d, q_d, backend, kspace=args.kspace)
     else:
         plan = sedev.plan(L, prm, peri, dev)
 
@@ -366,7 +394,7 @@ def run_ours(args):
             t0 = time.perf_counter()
             pd = pos_p.to(dev, non_blocking=True)
             qd = q_p.to(dev, non_blocking=True)
-            phi = total_potential_sharded(pd, qd, backend).cpu()
+            phi = total_potential_sharded(pd, qd, backend, kspace=args.kspace).cpu()
             t_e.append(time.perf_counter() - t0)
         te = torch.tensor([statistics.mean(t_e)], dtype=torch.float64, device=dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -443,7 +471,10 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.md 3.1; no public dataset exists for this path)",
             "config": {"workload": DESCR[CFG["workload"]], "N": N, "seed": CFG["seed"],
-                       "parallelism": f"particle-shard x{world} (grid + phi sum-all-reduce)",
+                       "parallelism": (f"particle-shard x{world} (grid + phi sum-all-reduce)"
+                                       if args.kspace == "replicated" or world == 1 else
+                                       f"particle-shard x{world}, slab k-space (grid reduce-scatter, "
+                                       "2 all-to-all, all-gather; phi sum-all-reduce)"),
                        "l2": "flushed (256 MB write) between timed steps, outside the step events"},
             "e2e": e2e, "roofline": roofline, "kernels": kern,
             "spread_gather": spread_gather,
@@ -489,6 +520,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kspace", choices=("replicated", "slab"), default="replicated",
+                    help="multi-GPU k-space stage (torchrun): replicated after a grid all-reduce, or "
+                         "slab-decomposed (D = 3)")
     ap.add_argument("--workload", default="cfg2", choices=sorted(workloads.ALL),
                     help="BASELINE config (default cfg2 = configs[1], the headline)")
     args = ap.parse_args()

@@ -135,6 +135,14 @@ int se_plan_grid(se_plan_t plan, se_grid_t *out);
  * with the same (pos, q, phi, N, stream) replay one graph of the device work
  * (first call eager, second call captured).  0 = always launch eagerly. */
 int se_plan_set_graphs(se_plan_t plan, int on);
+/* Deferred checks (on != 0): the shard entry points (se_*_shard_dev,
+ * se_kspace_apply_dev) only enqueue work -- no host synchronisation for the
+ * device error flags or profiling events -- so one host thread can keep
+ * several streams busy; se_plan_finish synchronises the plan's stream, raises
+ * a pending error (coincident particles -> SE_ESINGULAR) and collects the
+ * profiling events. */
+int se_plan_set_deferred_checks(se_plan_t plan, int on);
+int se_plan_finish(se_plan_t plan);
 /* Number of kernel launches issued by this plan since creation (for the bench). */
 int se_plan_launch_count(se_plan_t plan, int64_t *count);
 /* Warning bits raised by the last total-potential call: bit 0 = the system is
@@ -193,6 +201,26 @@ int se_gather_shard_dev(se_plan_t plan, const double *grid, const double *pos, i
                         int rank, int world, double *phi, int accumulate);
 int se_realspace_shard_dev(se_plan_t plan, const double *pos, const double *q, int64_t N,
                            int rank, int world, double *phi, int add_self);
+
+/* Slab-decomposed k-space stage of D = 3 (aft.py:203-206 + sekspace.py:198-206
+ * + aft.py:237-238 split over `world` ranks).  Rank r owns the
+ * x-slab of nx = M / world planes (block r of the C-order grid, as a
+ * reduce-scatter leaves it); M % world == 0.  Complex buffers are interleaved
+ * fp64 (re, im):
+ *   se_slab_forward_dev: slab (nx, M, M) real -> send (world, nx, nky, nkz)
+ *     complex: 2-D R2C over (y, z), block s = this rank's planes x ky-chunk s;
+ *   (caller: all-to-all of equal blocks -> recv, i.e. (M, nky, nkz) = all kx
+ *     of this rank's ky-chunk)
+ *   se_slab_xpass_dev: in place on recv: x-FFT, Green's-function / window
+ *     multiplier (x 1/M^3), inverse x-FFT;
+ *   (caller: all-to-all back)
+ *   se_slab_inverse_dev: back (world, nx, nky, nkz) -> slab (nx, M, M) real
+ *     (the slab of the k-space-filtered grid; an all-gather gives the grid).
+ * se_slab_geometry returns nx, nky = M / world and nkz = M / 2 + 1. */
+int se_slab_geometry(se_plan_t plan, int world, int64_t *nx, int64_t *nky, int64_t *nkz);
+int se_slab_forward_dev(se_plan_t plan, int world, const double *slab, double *send);
+int se_slab_xpass_dev(se_plan_t plan, int world, int rank, double *recv);
+int se_slab_inverse_dev(se_plan_t plan, int world, const double *back, double *slab);
 
 /* realspace.self_term (realspace.py:183-185): out = -2 xi q / sqrt(pi), on the
  * current CUDA device.  _dev: device pointers on `stream` (cudaStream_t). */

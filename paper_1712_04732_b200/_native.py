@@ -69,6 +69,8 @@ SIGNATURES = {
     "se_plan_d0_geometry": [_P, c_int32_p, c_int32_p, c_double_p],
     "se_plan_set_profiling": [_P, ctypes.c_int],
     "se_plan_set_graphs": [_P, ctypes.c_int],
+    "se_plan_set_deferred_checks": [_P, ctypes.c_int],
+    "se_plan_finish": [_P],
     "se_plan_kernel_times": [_P, c_double_p, c_int64_p],
     "se_realspace_pair_count_dev": [_P, _P, _P, ctypes.c_int64, c_int64_p],
     "se_spread_dev": [_P, _P, _P, ctypes.c_int64, _P],
@@ -78,6 +80,10 @@ SIGNATURES = {
     "se_realspace_dev": [_P, _P, _P, ctypes.c_int64, _P, ctypes.c_int],
     "se_total_potential_dev": [_P, _P, _P, ctypes.c_int64, _P, _P],
     "se_spread_shard_dev": [_P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P],
+    "se_slab_geometry": [_P, ctypes.c_int, c_int64_p, c_int64_p, c_int64_p],
+    "se_slab_forward_dev": [_P, ctypes.c_int, _P, _P],
+    "se_slab_xpass_dev": [_P, ctypes.c_int, ctypes.c_int, _P],
+    "se_slab_inverse_dev": [_P, ctypes.c_int, _P, _P],
     "se_gather_shard_dev": [_P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int],
     "se_realspace_shard_dev": [_P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int],
     "se_total_potential_host": [_P, _P, _P, ctypes.c_int64, _P, _P],

@@ -353,7 +353,7 @@ void plan_release_device(se_plan *pl) {
     for (auto &ev : pl->gfence)
         if (ev) cudaEventDestroy(ev);
     for (cufftHandle h : {pl->fft_fwd, pl->fft_inv, pl->fft_rowJ, pl->fft_rowI, pl->fft_row0, pl->fft_c_fwd,
-                          pl->fft_c_inv, pl->fft_f_fwd, pl->fft_f_inv})
+                          pl->fft_c_inv, pl->fft_f_fwd, pl->fft_f_inv, pl->slab_f2, pl->slab_i2, pl->slab_x})
         if (h) cufftDestroy(h);
     for (Binning *b : {&pl->tbin, &pl->cbin})
         for (DevBuf *d : {&b->keys, &b->keys_sorted, &b->idx, &b->idx_sorted, &b->counts, &b->starts, &b->units,
@@ -417,6 +417,22 @@ int se_plan_set_stream(se_plan_t plan, void *stream) {
     SE_API_BEGIN
     se_plan *pl = checked(plan);
     pl->stream = (cudaStream_t)stream;  // 0 is the legacy default stream
+    SE_API_END
+}
+
+int se_plan_set_deferred_checks(se_plan_t plan, int on) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    pl->defer = on != 0;
+    SE_API_END
+}
+
+int se_plan_finish(se_plan_t plan) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    if (pl->flag.ptr) check_flag(pl);
+    prof_collect(pl);
     SE_API_END
 }
 
@@ -496,7 +512,7 @@ int se_spread_shard_dev(se_plan_t plan, const double *pos, const double *q, int6
     check_shard(rank, world);
     DeviceGuard dg(pl->device);
     spread_run(pl, pos, q, N, grid_out, rank, world);
-    prof_collect(pl);
+    if (!pl->defer) prof_collect(pl);
     SE_API_END
 }
 
@@ -507,7 +523,39 @@ int se_kspace_apply_dev(se_plan_t plan, double *grid, int use_kernel, double *ti
     prof_begin(pl, SE_K_KSPACE);
     kspace_run(pl, grid, use_kernel, timings);
     prof_end(pl, SE_K_KSPACE);
-    prof_collect(pl);
+    if (!pl->defer) prof_collect(pl);
+    SE_API_END
+}
+
+int se_slab_geometry(se_plan_t plan, int world, int64_t *nx, int64_t *nky, int64_t *nkz) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    if (!nx || !nky || !nkz) fail(SE_EINVAL, "null output pointer");
+    slab_geometry(pl, world, nx, nky, nkz);
+    SE_API_END
+}
+
+int se_slab_forward_dev(se_plan_t plan, int world, const double *slab, double *send) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    slab_forward(pl, world, slab, send);
+    SE_API_END
+}
+
+int se_slab_xpass_dev(se_plan_t plan, int world, int rank, double *recv) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    slab_xpass(pl, world, rank, recv);
+    SE_API_END
+}
+
+int se_slab_inverse_dev(se_plan_t plan, int world, const double *back, double *slab) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    slab_inverse(pl, world, back, slab);
     SE_API_END
 }
 
@@ -526,7 +574,7 @@ int se_gather_shard_dev(se_plan_t plan, const double *grid, const double *pos, i
     check_shard(rank, world);
     DeviceGuard dg(pl->device);
     gather_run(pl, grid, pos, N, phi, accumulate, rank, world, true);
-    prof_collect(pl);
+    if (!pl->defer) prof_collect(pl);
     SE_API_END
 }
 
@@ -555,8 +603,10 @@ int se_realspace_shard_dev(se_plan_t plan, const double *pos, const double *q, i
     check_shard(rank, world);
     DeviceGuard dg(pl->device);
     realspace_run(pl, pos, q, N, phi, add_self, rank, world);
-    check_flag(pl);
-    prof_collect(pl);
+    if (!pl->defer) {
+        check_flag(pl);
+        prof_collect(pl);
+    }
     SE_API_END
 }
 

@@ -194,6 +194,12 @@ struct se_plan {
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     se::DevBuf phik;  // phi_F of the overlapped k-space pipeline
+    // slab-decomposed D = 3 k-space stage (per world size)
+    int slab_world = 0;
+    // deferred checks: the shard entry points return without synchronising
+    // (device error flags, profiling events); se_plan_finish does both
+    bool defer = false;
+    cufftHandle slab_f2 = 0, slab_i2 = 0, slab_x = 0;
 };
 
 namespace se {
@@ -237,6 +243,10 @@ void kspace_run(se_plan *pl, double *grid, int use_kernel, double *timings);
 void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi,
                    int add_self, int rank, int world);
 void d0_kernel_prepare(se_plan *pl, double *t_precompute);
+void slab_geometry(se_plan *pl, int world, int64_t *nx, int64_t *nky, int64_t *nkz);
+void slab_forward(se_plan *pl, int world, const double *slab, double *send);
+void slab_xpass(se_plan *pl, int world, int rank, double *recv);
+void slab_inverse(se_plan *pl, int world, const double *back, double *slab);
 void plan_release_device(se_plan *pl);
 
 // binning (se_sort.cu)

@@ -634,4 +634,106 @@ void kspace_run(se_plan *pl, double *grid, int use_kernel, double *timings) {
     }
 }
 
+// --------------------------------------------------- slab-decomposed D = 3
+// The k-space stage of D = 3 over `world` ranks: rank r owns the
+// x-slab of nx = M / world planes (the C-order grid's contiguous block r, as
+// a reduce-scatter leaves it).  Forward: 2-D R2C over (y, z) of the slab's
+// planes, packed into (world, nx, nky, nkz) blocks (block s = this rank's
+// planes x ky-chunk s) for an all-to-all; after it each rank holds all kx
+// for its ky-chunk, (M, nky, nkz): x-FFT, the aft.py:203-206 /
+// sekspace.py:198-206 multiplier, inverse x-FFT in one pass; a second
+// all-to-all and the inverse 2-D C2R return the x-slab.  Forward transforms
+// are unnormalised; the multiplier carries 1/M^3 as in the replicated path.
+
+__global__ void swap01_kernel(const cplx *__restrict__ src, int a, int b, int64_t c, cplx *__restrict__ dst) {
+    // dst (b, a, c) <- src (a, b, c)
+    const int64_t total = (int64_t)a * b * c;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = i % c;
+        const int64_t r = i / c;
+        const int jb = (int)(r % b), ia = (int)(r / b);
+        dst[((int64_t)jb * a + ia) * c + k] = src[i];
+    }
+}
+
+__global__ void scale_slab_kernel(cplx *__restrict__ F, int M, int nky, int ky0, const double *__restrict__ k,
+                                  const double *__restrict__ w, double xi, double norm) {
+    const int nh = M / 2 + 1;
+    const int64_t total = (int64_t)M * nky * nh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int iz = (int)(i % nh);
+        const int64_t r = i / nh;
+        const int iy = ky0 + (int)(r % nky), ix = (int)(r / nky);
+        const double k2 = k[ix] * k[ix] + k[iy] * k[iy] + k[iz] * k[iz];
+        const double W = w[ix] * w[iy] * w[iz];
+        const double fac = k2 > 0.0 ? 4.0 * M_PI * mollify(k2, xi) * (1.0 / k2) / (W * W) * norm : 0.0;
+        const cplx v = F[i];
+        F[i] = make_double2(v.x * fac, v.y * fac);
+    }
+}
+
+void slab_geometry(se_plan *pl, int world, int64_t *nx, int64_t *nky, int64_t *nkz) {
+    if (pl->D != 3) fail(SE_EINVAL, "the slab-decomposed k-space stage covers D = 3");
+    const int M = pl->g.M;
+    if (world < 1 || M % world) fail(SE_EINVAL, "slab decomposition needs M divisible by the number of ranks");
+    *nx = M / world;
+    *nky = M / world;
+    *nkz = M / 2 + 1;
+}
+
+static void slab_ffts(se_plan *pl, int world) {
+    if (pl->slab_world == world) return;
+    for (cufftHandle *h : {&pl->slab_f2, &pl->slab_i2, &pl->slab_x}) {
+        if (*h) cufftDestroy(*h);
+        *h = 0;
+    }
+    const int M = pl->g.M, nx = M / world, nky = M / world, nh = M / 2 + 1;
+    int n2[2] = {M, M}, rin[2] = {M, M}, cout[2] = {M, nh};
+    SE_CUFFT(cufftPlanMany(&pl->slab_f2, 2, n2, rin, 1, M * M, cout, 1, M * nh, CUFFT_D2Z, nx));
+    SE_CUFFT(cufftPlanMany(&pl->slab_i2, 2, n2, cout, 1, M * nh, rin, 1, M * M, CUFFT_Z2D, nx));
+    int n1[1] = {M}, e1[1] = {M};
+    SE_CUFFT(cufftPlanMany(&pl->slab_x, 1, n1, e1, nky * nh, 1, e1, nky * nh, 1, CUFFT_Z2Z, nky * nh));
+    pl->slab_world = world;
+}
+
+void slab_forward(se_plan *pl, int world, const double *slab, double *send) {
+    int64_t nx, nky, nkz;
+    slab_geometry(pl, world, &nx, &nky, &nkz);
+    slab_ffts(pl, world);
+    set_streams(pl, {pl->slab_f2});
+    const int M = pl->g.M;
+    pl->spec.ensure(sizeof(cplx) * (size_t)nx * M * nkz);
+    SE_CUFFT(cufftExecD2Z(pl->slab_f2, const_cast<double *>(slab), pl->spec.as<cplx>()));
+    // (nx, world, nky * nkz) -> (world, nx, nky * nkz)
+    LAUNCH(swap01_kernel, nx * M * nkz, pl->spec.as<cplx>(), (int)nx, world, nky * nkz, reinterpret_cast<cplx *>(send));
+}
+
+void slab_xpass(se_plan *pl, int world, int rank, double *recv) {
+    int64_t nx, nky, nkz;
+    slab_geometry(pl, world, &nx, &nky, &nkz);
+    if (rank < 0 || rank >= world) fail(SE_EINVAL, "rank out of range");
+    ensure_tables(pl);
+    slab_ffts(pl, world);
+    set_streams(pl, {pl->slab_x});
+    const int M = pl->g.M;
+    cplx *F = reinterpret_cast<cplx *>(recv);
+    SE_CUFFT(cufftExecZ2Z(pl->slab_x, F, F, CUFFT_FORWARD));
+    LAUNCH(scale_slab_kernel, (int64_t)M * nky * nkz, F, M, (int)nky, (int)(rank * nky), pl->tM.k.as<double>(),
+           pl->tM.what.as<double>(), pl->p.xi, 1.0 / ((double)M * M * M));
+    SE_CUFFT(cufftExecZ2Z(pl->slab_x, F, F, CUFFT_INVERSE));
+}
+
+void slab_inverse(se_plan *pl, int world, const double *back, double *slab) {
+    int64_t nx, nky, nkz;
+    slab_geometry(pl, world, &nx, &nky, &nkz);
+    slab_ffts(pl, world);
+    set_streams(pl, {pl->slab_i2});
+    const int M = pl->g.M;
+    pl->spec.ensure(sizeof(cplx) * (size_t)nx * M * nkz);
+    // (world, nx, nky * nkz) -> (nx, world, nky * nkz) = (nx, M, nkz)
+    LAUNCH(swap01_kernel, nx * M * nkz, reinterpret_cast<const cplx *>(back), world, (int)nx, nky * nkz,
+           pl->spec.as<cplx>());
+    SE_CUFFT(cufftExecZ2D(pl->slab_i2, pl->spec.as<cplx>(), slab));
+}
+
 }  // namespace se

@@ -76,29 +76,92 @@ class OracleBackend:
         v = self.orc.gather(grid.numpy(), pos.numpy()[own], self.g, self.prm["window"], self.prm["shape"])
         phi[torch.from_numpy(own)] += torch.from_numpy(v)
 
+    # slab-decomposed k-space stage (D = 3), numpy transforms with the
+    # library's buffer layouts: send / recv (world, nx, nky, nkz, re|im)
+    def slab_geometry(self, world):
+        M = self.prm["M"]
+        return M // world, M // world, M // 2 + 1
 
-def _worker(rank, world, port, out_path):
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    sys.path[:0] = [root, os.path.join(root, "oracle")]
-    import se_oracle as orc
-    from paper_1712_04732_b200.distributed import total_potential_sharded
+    def empty_spectrum(self, world):
+        nx, nky, nkz = self.slab_geometry(world)
+        return torch.empty((world, nx, nky, nkz, 2), dtype=torch.float64)
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    @staticmethod
+    def _put(t, c):
+        t.copy_(torch.from_numpy(np.ascontiguousarray(np.stack([c.real, c.imag], -1))))
+
+    @staticmethod
+    def _get(t):
+        a = t.numpy()
+        return a[..., 0] + 1j * a[..., 1]
+
+    def slab_forward(self, slab, world, send):
+        nx, nky, nkz = self.slab_geometry(world)
+        A = np.fft.rfft2(slab.numpy(), axes=(1, 2))  # (nx, M, nkz)
+        self._put(send, A.reshape(nx, world, nky, nkz).transpose(1, 0, 2, 3))
+
+    def slab_xpass(self, recv, rank, world):
+        nx, nky, nkz = self.slab_geometry(world)
+        M = self.prm["M"]
+        g, xi = self.g, self.prm["xi"]
+        k = self.orc.wavenumbers(M, g["h"])
+        wh = self.orc.window_fourier_checked(self.prm["window"], self.prm["shape"], 0.5 * g["P"] * g["h"], k)
+        ky, kz = slice(rank * nky, (rank + 1) * nky), slice(0, nkz)
+        k2 = k[:, None, None] ** 2 + k[None, ky, None] ** 2 + k[None, None, kz] ** 2
+        inv = np.where(k2 > 0, 1.0 / np.where(k2 > 0, k2, 1.0), 0.0)
+        W = wh[:, None, None] * wh[None, ky, None] * wh[None, None, kz]
+        mult = self.orc.FOUR_PI * self.orc._mollify(k2, xi) * inv / W ** 2
+        C = self._get(recv).reshape(M, nky, nkz)
+        G = np.fft.ifft(np.fft.fft(C, axis=0) * mult, axis=0)
+        self._put(recv, G.reshape(world, nx, nky, nkz))
+
+    def slab_inverse(self, back, world, slab):
+        nx, nky, nkz = self.slab_geometry(world)
+        M = self.prm["M"]
+        B = self._get(back).transpose(1, 0, 2, 3).reshape(nx, M, nkz)
+        slab.copy_(torch.from_numpy(np.fft.irfft2(B, s=(M, M), axes=(1, 2))))
+
+
+def _inputs():
     rng = np.random.default_rng(5)
     N, L = 400, 1.0
     pos = rng.random((N, 3)) * L
     q = rng.uniform(-1, 1, N)
     q -= q.mean()
     prm = dict(xi=8.0, rc=0.4, M=24, P=8, window="bm", shape=20.0)
+    return pos, q, L, prm
+
+
+# uneven particle partition for the partitioned-input API
+_SPLIT = 150
+
+
+def _worker(rank, world, port, out_path, mode):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "oracle")]
+    import se_oracle as orc
+    from paper_1712_04732_b200.distributed import total_potential_partitioned, total_potential_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pos, q, L, prm = _inputs()
     be = OracleBackend(orc, pos, q, L, 3, prm)
-    phi = total_potential_sharded(torch.from_numpy(pos), torch.from_numpy(q), be)
+    if mode == "partitioned":
+        lo, hi = (0, _SPLIT) if rank == 0 else (_SPLIT, len(q))
+        phi = total_potential_partitioned(torch.from_numpy(pos[lo:hi].copy()), torch.from_numpy(q[lo:hi].copy()),
+                                          be, kspace="slab")
+    else:
+        phi = total_potential_sharded(torch.from_numpy(pos), torch.from_numpy(q), be, kspace=mode)
     np.save(f"{out_path}.{rank}.npy", phi.numpy())
     dist.destroy_process_group()
 
 
-def test_sharded_orchestration_world2_gloo(tmp_path):
+@pytest.mark.parametrize("mode", ["replicated", "slab", "partitioned"])
+def test_sharded_orchestration_world2_gloo(tmp_path, mode):
+    """replicated: grid all-reduce; slab: reduce-scatter into x-slabs, two
+    all-to-all transposes, all-gather; partitioned: each rank passes its own
+    (uneven) particle subset and gets its own potentials back."""
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, os.path.join(root, "oracle"))
@@ -106,17 +169,30 @@ def test_sharded_orchestration_world2_gloo(tmp_path):
 
     world = 2
     out = str(tmp_path / "phi")
-    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
-    rng = np.random.default_rng(5)
-    N, L = 400, 1.0
-    pos = rng.random((N, 3)) * L
-    q = rng.uniform(-1, 1, N)
-    q -= q.mean()
-    prm = dict(xi=8.0, rc=0.4, M=24, P=8, window="bm", shape=20.0)
+    mp.spawn(_worker, args=(world, _free_port(), out, mode), nprocs=world, join=True)
+    pos, q, L, prm = _inputs()
     ref = orc.total_potential(pos, q, L, 3, prm)
     for r in range(world):
         phi = np.load(f"{out}.{r}.npy")
-        assert orc.relative_rms(phi, ref) < 1e-13
+        want = ref if mode != "partitioned" else (ref[:_SPLIT] if r == 0 else ref[_SPLIT:])
+        assert orc.relative_rms(phi, want) < 1e-13
+
+
+def test_slab_single_process_matches_replicated():
+    """world = 1 (no process group): the slab path aliases its buffers."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "oracle")]
+    import se_oracle as orc
+    from paper_1712_04732_b200.distributed import total_potential_sharded
+
+    pos, q, L, prm = _inputs()
+    be = OracleBackend(orc, pos, q, L, 3, prm)
+    a = total_potential_sharded(torch.from_numpy(pos), torch.from_numpy(q), be, kspace="slab")
+    ref = orc.total_potential(pos, q, L, 3, prm)
+    assert orc.relative_rms(a.numpy(), ref) < 1e-13
+    with pytest.raises(ValueError):
+        total_potential_sharded(torch.from_numpy(pos), torch.from_numpy(q), be, kspace="pencil")
 
 
 def test_shard_bounds_cover_exactly():

@@ -464,10 +464,62 @@ def test_sharded_pipeline_nccl_single_rank():
         dev = torch.device("cuda", 0)
         pos = torch.from_numpy(s.positions).to(dev)
         q = torch.from_numpy(s.charges).to(dev)
-        phi = total_potential_sharded(pos, q, NativeBackend(s.L, p, se.Periodicity(3), dev))
-        assert se.relative_rms_error(phi.cpu().numpy(), full) < 1e-13
+        be = NativeBackend(s.L, p, se.Periodicity(3), dev)
+        for mode in ("replicated", "slab"):
+            phi = total_potential_sharded(pos, q, be, kspace=mode)
+            assert se.relative_rms_error(phi.cpu().numpy(), full) < 1e-13, mode
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_slab_kspace_stages_virtual_ranks(world):
+    # the slab-decomposed D = 3 k-space stage for `world` ranks, driven in one
+    # process: each virtual rank's forward / x-pass / inverse run on the device
+    # and the two all-to-all transposes are done by indexing (send block s of
+    # rank r -> recv block r of rank s).  The assembled grid must equal the
+    # replicated stage (se_kspace_apply_dev) on the same spread grid.
+    from paper_1712_04732_b200.distributed import NativeBackend
+
+    s = rand_system(6000, 2.0, 47)
+    p = se.SEParams(xi=6.0, rc=0.5, M=32, P=8, window="bm", shape=20.0, eps=1e-8)
+    dev = torch.device("cuda", 0)
+    pos = torch.from_numpy(s.positions).to(dev)
+    q = torch.from_numpy(s.charges).to(dev)
+    be = NativeBackend(s.L, p, se.Periodicity(3), dev)
+    grid = be.empty_grid()
+    be.spread_shard(pos, q, 0, 1, grid)
+    ref = grid.clone()
+    be.kspace_apply(ref)
+    nx, nky, nkz = be.slab_geometry(world)
+    assert (nx, nky, nkz) == (32 // world, 32 // world, 17)
+    send = [be.empty_spectrum(world) for _ in range(world)]
+    for r in range(world):
+        be.slab_forward(grid[r * nx:(r + 1) * nx].contiguous(), world, send[r])
+    recv = [torch.stack([send[src][r] for src in range(world)]) for r in range(world)]
+    for r in range(world):
+        be.slab_xpass(recv[r], r, world)
+    back = [torch.stack([recv[src][r] for src in range(world)]) for r in range(world)]
+    out = torch.empty_like(grid)
+    for r in range(world):
+        slab = torch.empty((nx,) + tuple(grid.shape[1:]), dtype=torch.float64, device=dev)
+        be.slab_inverse(back[r], world, slab)
+        out[r * nx:(r + 1) * nx] = slab
+    assert torch.max(torch.abs(out - ref)).item() <= 1e-13 * torch.max(torch.abs(ref)).item()
+
+
+def test_slab_kspace_rejections():
+    from paper_1712_04732_b200.distributed import NativeBackend
+
+    dev = torch.device("cuda", 0)
+    p = se.SEParams(xi=6.0, rc=0.5, M=24, P=8, window="bm", shape=20.0, eps=1e-8)
+    be = NativeBackend(2.0, p, se.Periodicity(3), dev)
+    with pytest.raises(ValueError):
+        be.slab_geometry(5)  # 24 % 5 != 0
+    p2 = se.SEParams(xi=6.0, rc=0.5, M=24, P=8, window="bm", shape=20.0, eps=1e-8, R=3.0)
+    be2 = NativeBackend(2.0, p2, se.Periodicity(2), dev)
+    with pytest.raises(ValueError):
+        be2.slab_geometry(2)  # D = 2
 
 
 def test_cuda_graph_replay_matches_eager_and_tracks_inputs():
