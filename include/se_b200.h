@@ -202,6 +202,18 @@ int se_gather_shard_dev(se_plan_t plan, const double *grid, const double *pos, i
 int se_realspace_shard_dev(se_plan_t plan, const double *pos, const double *q, int64_t N,
                            int rank, int world, double *phi, int add_self);
 
+/* Electric field E = -grad phi at every particle, D = 3 (forces F = q E; the
+ * reference stops at potentials: SPEC.md:16 notes the force integration "has
+ * to be performed three times").  E is (N, 3) in caller
+ * order: the real-space pair field q_s (erfc(xi r)/r + 2 xi/sqrt(pi)
+ * exp(-xi^2 r^2)) (x_t - x_s)/r^2 over the same pair set as
+ * real_space_sum, plus the Fourier field gathered from the spectrally
+ * differentiated grid (-i k times the scaled spectrum, one inverse transform
+ * and one gather per component).  No self term (the self-interaction is a
+ * constant).  Errors as se_total_potential_*. */
+int se_total_field_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E);
+int se_total_field_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E);
+
 /* Slab-decomposed k-space stage of D = 3 (aft.py:203-206 + sekspace.py:198-206
  * + aft.py:237-238 split over `world` ranks).  Rank r owns the
  * x-slab of nx = M / world planes (block r of the C-order grid, as a

@@ -614,3 +614,114 @@ def relative_rms(phi, ref):
     phi = np.asarray(phi, dtype=complex)
     ref = np.asarray(ref, dtype=complex)
     return float(np.sqrt(np.mean(np.abs(phi - ref) ** 2)) / np.sqrt(np.mean(np.abs(ref) ** 2)))
+
+
+# ------------------------------------------------------------ field (forces)
+# Beyond the reference, which stops at potentials (SURVEY 8f
+# item 4).  Pinned by central differences of the reference's own
+# real_space_sum (realspace.py:168-180) and oracle.kspace_direct_3p
+# (oracle.py:109-118): tests/golden/make_golden.py -> field.npz.
+
+def realspace_field(pos, q, L, D, xi, rc, targets=None):
+    """E_R(x_t) = sum q_s (erfc(xi r)/r + 2 xi/sqrt(pi) e^{-xi^2 r^2}) d / r^2,
+    d = x_t - x_s over the same pair set as realspace(): minimum image when
+    rc <= L/2 on the periodic axes, explicit images otherwise.  Brute force
+    over all sources (test sizes)."""
+    N = len(q)
+    tsel = np.arange(N) if targets is None else np.asarray(targets)
+    per = np.array([a < D for a in range(3)])
+    c = 2.0 * xi / math.sqrt(math.pi)
+
+    def block(xt, xs, same=None):
+        d = xt[:, None, :] - xs[None, :, :]
+        r = np.sqrt(np.sum(d * d, axis=2))
+        zero = r < 1e-14
+        if same is not None and np.any(zero & ~same):
+            raise SingularConfigurationError_("coincident distinct particles")
+        use = (r < rc) & ~zero
+        rs = np.where(use, r, 1.0)
+        g = np.where(use, (_erfc(xi * rs) / rs + c * np.exp(-(xi * rs) ** 2)) / rs ** 2, 0.0) * q[None, :]
+        return np.einsum("ts,tsa->ta", g, d)
+
+    out = np.zeros((len(tsel), 3))
+    for i0 in range(0, len(tsel), 256):
+        ti = tsel[i0:i0 + 256]
+        same = ti[:, None] == np.arange(N)[None, :]
+        if D >= 1 and rc > L / 2 + 1e-12:
+            layers = int(np.floor((rc + L / 2) / L)) + 1
+            rng = [np.arange(-layers, layers + 1) if per[a] else np.array([0]) for a in range(3)]
+            for a in rng[0]:
+                for b in rng[1]:
+                    for cc in rng[2]:
+                        sh = np.array([a, b, cc], float) * L
+                        out[i0:i0 + 256] += block(pos[ti], pos - sh, same if (a == b == cc == 0) else None)
+        else:
+            d = pos[ti][:, None, :] - pos[None, :, :]
+            d -= per[None, None, :] * L * np.rint(d / L)
+            out[i0:i0 + 256] += _field_from_disp(d, q, xi, rc, c, same)
+    return out
+
+
+def _field_from_disp(d, q, xi, rc, c, same):
+    r = np.sqrt(np.sum(d * d, axis=2))
+    zero = r < 1e-14
+    if np.any(zero & ~same):
+        raise SingularConfigurationError_("coincident distinct particles")
+    use = (r < rc) & ~zero
+    rs = np.where(use, r, 1.0)
+    g = np.where(use, (_erfc(xi * rs) / rs + c * np.exp(-(xi * rs) ** 2)) / rs ** 2, 0.0) * q[None, :]
+    return np.einsum("ts,tsa->ta", g, d)
+
+
+def kspace_field_d3(pos, q, L, prm, targets=None):
+    """E_F = gather(IFFT(-i k_a Phi)), Phi the scaled spectrum of kspace_d3
+    (aft.py:203-206 + sekspace.py:198-206); the Nyquist index of the
+    differentiated axis is zeroed (real output)."""
+    g = geometry(L, 3, prm["M"], prm["P"])
+    kind, shape, xi = prm["window"], prm["shape"], prm["xi"]
+    H = spread(pos, q, g, kind, shape)
+    M, w = g["M"], 0.5 * g["P"] * g["h"]
+    k = wavenumbers(M, g["h"])
+    wh = window_fourier_checked(kind, shape, w, k)
+    k2 = k[:, None, None] ** 2 + k[None, :, None] ** 2 + k[None, None, :] ** 2
+    inv = np.zeros_like(k2)
+    inv[k2 > 0] = 1.0 / k2[k2 > 0]
+    W = wh[:, None, None] * wh[None, :, None] * wh[None, None, :]
+    F = np.fft.fftn(H) * (FOUR_PI * _mollify(k2, xi) * inv / W ** 2)
+    kd = k.copy()
+    kd[M // 2] = 0.0
+    tpos = pos if targets is None else pos[np.asarray(targets)]
+    out = np.zeros((len(tpos), 3))
+    for a in range(3):
+        shp = [1, 1, 1]
+        shp[a] = M
+        Ea = np.fft.ifftn(-1j * kd.reshape(shp) * F).real
+        out[:, a] = gather(Ea, tpos, g, kind, shape)
+    return out
+
+
+def total_field(pos, q, L, prm):
+    """E = E_R + E_F (D = 3)."""
+    return realspace_field(pos, q, L, 3, prm["xi"], prm["rc"]) + kspace_field_d3(pos, q, L, prm)
+
+
+def direct_field_3p(pos, q, L, xi, kmax, targets=None):
+    """-grad of direct_kspace_3p at the targets: (4 pi / L^3) sum_k
+    e^{-k^2/4xi^2}/k^2 k Im(e^{i k.x_m} S_k)."""
+    pos = np.asarray(pos, float)
+    tg = np.arange(len(pos)) if targets is None else np.asarray(targets)
+    n = np.arange(-kmax, kmax + 1)
+    c = 2.0 * np.pi / L
+    ex, ey, ez = (np.exp(-1j * c * np.outer(pos[:, a], n)) for a in range(3))
+    out = np.zeros((len(tg), 3))
+    for i1, n1 in enumerate(n):
+        S = np.einsum("n,nb,nc->bc", q * ex[:, i1], ey, ez)
+        k2 = c * c * (n1 * n1 + n[:, None] ** 2 + n[None, :] ** 2)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            coef = np.where(k2 > 0, np.exp(-k2 / (4.0 * xi * xi)) / k2, 0.0)
+        E = np.einsum("t,tb,tc->tbc", np.conj(ex[tg, i1]), np.conj(ey[tg]), np.conj(ez[tg]))
+        im = np.imag(E * S[None]) * coef[None]
+        out[:, 0] += c * n1 * im.sum(axis=(1, 2))
+        out[:, 1] += c * np.einsum("tbc,b->t", im, n.astype(float))
+        out[:, 2] += c * np.einsum("tbc,c->t", im, n.astype(float))
+    return out * (FOUR_PI / L ** 3)

@@ -14,7 +14,9 @@ from . import core, params, realspace, sekspace
 _PUBLIC = {
     core: ("ConfigurationError", "ParticleSystem", "Periodicity", "SEParams",
            "SingularConfigurationError", "energy", "generate_random_system", "load_particles",
-           "relative_rms_error", "save_particles", "total_potential"),
+           "relative_rms_error", "save_particles", "total_potential",
+           # beyond the reference: E = -grad phi and F = q E, D = 3
+           "total_field", "forces"),
     params: ("auto_params",),
     realspace: ("real_space_sum", "self_term"),
     sekspace: ("se_kspace",),

@@ -348,6 +348,9 @@ void plan_release_device(se_plan *pl) {
     if (pl->fork_ev) cudaEventDestroy(pl->fork_ev);
     if (pl->join_ev) cudaEventDestroy(pl->join_ev);
     pl->phik.release();
+    pl->fgrid.release();
+    pl->fphi.release();
+    pl->io_E.release();
     if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
     pl->gexec = nullptr;
     for (auto &ev : pl->gfence)
@@ -616,6 +619,60 @@ int se_total_potential_dev(se_plan_t plan, const double *pos, const double *q, i
     se_plan *pl = checked(plan);
     DeviceGuard dg(pl->device);
     total_pipeline(pl, pos, q, N, phi, timings);
+    SE_API_END
+}
+
+__global__ void field_combine_kernel(const double *__restrict__ ek, int64_t N, double *__restrict__ E) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    E[3 * i] += ek[i];
+    E[3 * i + 1] += ek[N + i];
+    E[3 * i + 2] += ek[2 * N + i];
+}
+
+// E = E_R + E_F at every particle (D = 3): the real-space field kernel, then
+// spread -> scaled spectrum -> three differentiated inverse transforms ->
+// three gathers, summed into E (N x 3, caller order).
+void field_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *E) {
+    if (pl->D != 3) fail(SE_EINVAL, "the electric field (forces) covers D = 3");
+    check_system(pl, pos, q, N, true);
+    realspace_field_run(pl, pos, q, N, E, 0, 1);
+    if (N <= 0) return;
+    const size_t G = grid_points(pl);
+    pl->grid_dev.ensure(sizeof(double) * G);
+    pl->fgrid.ensure(sizeof(double) * 3 * G);
+    pl->fphi.ensure(sizeof(double) * 3 * (size_t)N);
+    double *grid = pl->grid_dev.as<double>();
+    spread_run(pl, pos, q, N, grid, 0, 1);
+    prof_begin(pl, SE_K_KSPACE);
+    kspace_field_run(pl, grid, pl->fgrid.as<double>());
+    prof_end(pl, SE_K_KSPACE);
+    for (int a = 0; a < 3; ++a)
+        gather_run(pl, pl->fgrid.as<double>() + a * G, pos, N, pl->fphi.as<double>() + a * N, 0, 0, 1, false);
+    field_combine_kernel<<<(unsigned)((N + 255) / 256), 256, 0, pl->stream>>>(pl->fphi.as<double>(), N, E);
+    SE_LAUNCH_CHECK();
+    pl->launches += 1;
+    check_flag(pl);
+    prof_collect(pl);
+}
+
+int se_total_field_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    field_pipeline(pl, pos, q, N, E);
+    SE_API_END
+}
+
+int se_total_field_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    const double *dp = stage_in(pl, pl->io_pos, pos, 3 * (size_t)N);
+    const double *dq = stage_in(pl, pl->io_q, q, (size_t)N);
+    pl->io_E.ensure(sizeof(double) * 3 * (N ? N : 1));
+    field_pipeline(pl, dp, dq, N, pl->io_E.as<double>());
+    stage_out(pl, E, pl->io_E.ptr, sizeof(double) * 3 * N);
     SE_API_END
 }
 

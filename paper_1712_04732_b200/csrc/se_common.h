@@ -194,6 +194,7 @@ struct se_plan {
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     se::DevBuf phik;  // phi_F of the overlapped k-space pipeline
+    se::DevBuf fgrid, fphi, io_E;  // field: three filtered grids, three gathered components, host staging
     // slab-decomposed D = 3 k-space stage (per world size)
     int slab_world = 0;
     // deferred checks: the shard entry points return without synchronising
@@ -242,7 +243,10 @@ void gather_run(se_plan *pl, const double *grid, const double *pos, int64_t N, d
 void kspace_run(se_plan *pl, double *grid, int use_kernel, double *timings);
 void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi,
                    int add_self, int rank, int world);
+void realspace_field_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *E,
+                         int rank, int world);
 void d0_kernel_prepare(se_plan *pl, double *t_precompute);
+void kspace_field_run(se_plan *pl, double *grid, double *g3);
 void slab_geometry(se_plan *pl, int world, int64_t *nx, int64_t *nky, int64_t *nkz);
 void slab_forward(se_plan *pl, int world, const double *slab, double *send);
 void slab_xpass(se_plan *pl, int world, int rank, double *recv);

@@ -736,4 +736,43 @@ void slab_inverse(se_plan *pl, int world, const double *back, double *slab) {
     SE_CUFFT(cufftExecZ2D(pl->slab_i2, pl->spec.as<cplx>(), slab));
 }
 
+// ------------------------------------------------------ field (D = 3, ik)
+// E_F = -grad phi_F by spectral differentiation of the filtered grid: the
+// gather is a convolution with the window, so grad commutes with it and
+// E_F,a = gather(IFFT(-i k_a Phi)), Phi the scaled spectrum (three inverse
+// transforms, three gathers; no window derivative -- the ES window's is
+// singular at the support edge).  The Nyquist plane of the differentiated
+// axis is zeroed (real output).
+__global__ void grad_d3_kernel(const cplx *__restrict__ F, cplx *__restrict__ G, int M, const double *__restrict__ k,
+                               int axis) {
+    const int nh = M / 2 + 1;
+    const int64_t total = (int64_t)M * M * nh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int iz = (int)(i % nh);
+        const int64_t r = i / nh;
+        const int iy = (int)(r % M), ix = (int)(r / M);
+        const int id = axis == 0 ? ix : (axis == 1 ? iy : iz);
+        const double kk = id == M / 2 ? 0.0 : k[id];
+        const cplx v = F[i];
+        G[i] = make_double2(kk * v.y, -kk * v.x);  // -i k (re + i im)
+    }
+}
+
+void kspace_field_run(se_plan *pl, double *grid, double *g3) {
+    if (pl->D != 3) fail(SE_EINVAL, "the electric field (forces) covers D = 3");
+    ensure_tables(pl);
+    make_ffts(pl);
+    set_streams(pl, {pl->fft_fwd, pl->fft_inv});
+    const int M = pl->g.M;
+    const size_t G = (size_t)M * M * M, S = (size_t)M * M * (M / 2 + 1);
+    pl->spec2.ensure(sizeof(cplx) * S);
+    SE_CUFFT(cufftExecD2Z(pl->fft_fwd, grid, pl->spec.as<cplx>()));
+    LAUNCH(scale_d3_kernel, (int64_t)S, pl->spec.as<cplx>(), M, pl->tM.k.as<double>(), pl->tM.what.as<double>(),
+           pl->p.xi, 1.0 / ((double)M * M * M));
+    for (int a = 0; a < 3; ++a) {
+        LAUNCH(grad_d3_kernel, (int64_t)S, pl->spec.as<cplx>(), pl->spec2.as<cplx>(), M, pl->tM.k.as<double>(), a);
+        SE_CUFFT(cufftExecZ2D(pl->fft_inv, pl->spec2.as<cplx>(), g3 + a * G));
+    }
+}
+
 }  // namespace se

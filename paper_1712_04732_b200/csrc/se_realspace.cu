@@ -44,6 +44,8 @@ struct RealArgs {
     int reach;        // neighbour columns within +-reach (column edge >= rc / reach)
 };
 
+constexpr double kTwoOverSqrtPi = 1.1283791670955126;  // field mode: c = 2 xi / sqrt(pi)
+
 // columns of edge >= rc/reach: neighbours within +-reach columns; reach 3
 // (fewer candidates) unless columns would be short (small N: every visited
 // column costs at least one batch, so fewer, longer columns win)
@@ -170,6 +172,31 @@ __device__ __forceinline__ double erfc_fast(double x, double w) {
     return p * (e * w);
 }
 
+// Field mode: the two factors separately, erfcx(x) (as p) and exp(-x^2) (as
+// e): E_R needs erfc(x)/r + (2 xi / sqrt(pi)) exp(-x^2) = e (p / r + c).
+template <bool WIDE>
+__device__ __forceinline__ void erfc_parts(double x, double &p, double &e) {
+    if (WIDE) {
+        if (x > SE_ERFC_XMAX) {
+            p = erfcx(x);
+            e = exp(-x * x);
+            return;
+        }
+    }
+    const double s = fma(x, se_erfc_k[0], se_erfc_k[1]) * rcp_nr(x + SE_ERFC_K);
+    p = se_erfcx_c[SE_ERFC_NE];
+#pragma unroll
+    for (int i = SE_ERFC_NE - 1; i >= 0; --i) p = fma(p, s, se_erfcx_c[i]);
+    const double u = x * x;
+    const double n = rint(u * se_erfc_k[2]);
+    const double r = fma(n, se_erfc_k[4], fma(n, se_erfc_k[3], -u));
+    e = se_exp_c[SE_EXP_NX];
+#pragma unroll
+    for (int i = SE_EXP_NX - 1; i >= 2; --i) e = fma(e, r, se_exp_c[i]);
+    e = fma(fma(e, r, SE_EXP_C1), r, SE_EXP_C0);
+    e = __hiloint2double(__double2hiint(e) + (int)n * (1 << 20), __double2loint(e));
+}
+
 __device__ __forceinline__ double min_image(double d, double L) { return d - L * rint(d / L); }
 __device__ __forceinline__ float min_image_f(float d, float L, float invL) { return d - L * rintf(d * invL); }
 
@@ -178,15 +205,19 @@ constexpr int kWarps = 1;  // warps (units) per block: one, so that the WarpBuf 
 constexpr int kMinBlocks = 27;  // 27 x (7 KB + 1 KB reserved) of shared memory per SM
 constexpr int kT = 16;     // targets per warp unit: lane l tests target l % 16 against half of a 32-source batch
 
-// Shared-memory workspace of one warp unit (7 KB: 8 blocks x 4 warps per SM).
-struct __align__(16) WarpBuf {
+// Shared-memory workspace of one warp unit (7 KB; 15 KB in field mode, FLD:
+// three accumulator components).
+template <bool FLD>
+struct __align__(16) WarpBufT {
     double2 txy[kT], tzq[kT];    // the unit's targets: (x, y), (z, q) -- one LDS.128 each
     double2 sxy[32], szq[32];    // current source batch, likewise (16-B stride: a warp's
                                  // random reads cost the minimum 4 wavefronts per LDS.128)
     float4 sf[32];               // the same in fp32 for the prefilter
-    double acc[kT][32];          // per-lane private accumulators acc[t][lane]: lane-owned banks
+    double acc[FLD ? 3 : 1][kT][32];  // per-lane private accumulators acc[c][t][lane]: lane-owned banks
     unsigned short ent[kT * 32];  // compacted hits of a batch: (target slot << 5) | source
 };
+// field mode: 13 CTAs x (15 KB + 1 KB reserved) per SM
+constexpr int kMinBlocksField = 13;
 
 // Shared-memory slot of unit target t: targets t and t + 8 (one prefilter
 // lane's pair) land in different bank quads of txy / tzq (slot t ^ 4 for
@@ -215,14 +246,15 @@ struct Hit {
     double f;   // erfc(xi r)/r, 0 outside the cutoff
     double qt;  // target charge (source-side update with NEWTON)
     double qs;  // source charge (target-side update)
+    double dx, dy, dz;  // x_t - x_s (field mode)
     int tt, k;
     bool ok;
 };
 
 // Geometry of one hit up to the erfc argument: h.f = w (1/r, or 0 outside
 // the cutoff or for an invalid slot), returns x = xi r.
-template <bool MI, bool NEWTON>
-__device__ __forceinline__ double hit_geometry(unsigned en, bool valid, const RealArgs &a, const WarpBuf &wb, int jb,
+template <bool MI, bool NEWTON, bool FLD, class WB>
+__device__ __forceinline__ double hit_geometry(unsigned en, bool valid, const RealArgs &a, const WB &wb, int jb,
                                                int tbase, int &singular, Hit &h) {
     h.tt = (int)(en >> 5);
     h.k = (int)(en & 31u);
@@ -253,23 +285,60 @@ __device__ __forceinline__ double hit_geometry(unsigned en, bool valid, const Re
     h.f = h.ok ? rinv : 0.0;  // a select, not a branch: the erfc runs unconditionally
     h.qt = t23.y;
     h.qs = s23.y;
+    if (FLD) {
+        h.dx = dx;
+        h.dy = dy;
+        h.dz = dz;
+    }
     return a.xi * rr;
 }
 
-template <bool MI, bool NEWTON, bool WIDE>
-__device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const WarpBuf &wb, int jb, int tbase,
+// Potential mode: h.f = erfc(x) w.  Field mode (FLD): h.f = g with
+// E_t += q_s g (x_t - x_s), g = (erfc(x)/r + c exp(-x^2)) / r^2 =
+// e w^2 (p w + c), c = 2 xi / sqrt(pi) (w = 1/r, 0 outside the cutoff).
+template <bool WIDE, bool FLD>
+__device__ __forceinline__ void hit_value(double x, const RealArgs &a, Hit &h) {
+    if (FLD) {
+        double p, e;
+        erfc_parts<WIDE>(x, p, e);
+        const double w = h.f;
+        h.f = e * (w * w) * fma(p, w, a.xi * kTwoOverSqrtPi);
+    } else {
+        h.f = erfc_fast<WIDE>(x, h.f);
+    }
+}
+
+template <bool MI, bool NEWTON, bool WIDE, bool FLD, class WB>
+__device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const WB &wb, int jb, int tbase,
                                         int &singular) {
     Hit h;
-    const double x = hit_geometry<MI, NEWTON>(en, true, a, wb, jb, tbase, singular, h);
-    h.f = erfc_fast<WIDE>(x, h.f);
+    const double x = hit_geometry<MI, NEWTON, FLD>(en, true, a, wb, jb, tbase, singular, h);
+    hit_value<WIDE, FLD>(x, a, h);
     return h;
 }
 
 // Target side into the lane's private slot; with NEWTON the source side
 // q_t f goes to the source's global accumulator (REDG).
-template <bool NEWTON>
-__device__ __forceinline__ void apply_hit(const Hit &h, WarpBuf &wb, int lane, double *__restrict__ acc_batch) {
-    double *slot = &wb.acc[h.tt][lane];
+// Field mode: three components on both sides (the source side with the
+// opposite sign), acc_batch in (3 j + c) layout.
+template <bool NEWTON, bool FLD>
+__device__ __forceinline__ void apply_hit(const Hit &h, WarpBufT<FLD> &wb, int lane, double *__restrict__ acc_batch) {
+    if (FLD) {
+        const double gs = h.qs * h.f;
+        double *s0 = &wb.acc[0][h.tt][lane], *s1 = &wb.acc[FLD ? 1 : 0][h.tt][lane],
+               *s2 = &wb.acc[FLD ? 2 : 0][h.tt][lane];
+        *s0 = fma(gs, h.dx, *s0);
+        *s1 = fma(gs, h.dy, *s1);
+        *s2 = fma(gs, h.dz, *s2);
+        if (NEWTON && h.ok) {
+            const double gt = -h.qt * h.f;
+            atomicAdd(acc_batch + 3 * h.k, gt * h.dx);
+            atomicAdd(acc_batch + 3 * h.k + 1, gt * h.dy);
+            atomicAdd(acc_batch + 3 * h.k + 2, gt * h.dz);
+        }
+        return;
+    }
+    double *slot = &wb.acc[0][h.tt][lane];
     *slot = fma(h.qs, h.f, *slot);
     if (NEWTON && h.ok) atomicAdd(acc_batch + h.k, h.qt * h.f);
 }
@@ -312,9 +381,9 @@ struct PreTargets {
 //     sources of the target's own column count only if j > t;
 //  2. warp prefix scan of the hit counts and compaction of the hits;
 //  3. the list is evaluated 64 hits at a time (two per lane) on full warps.
-template <bool MI, bool COUNT, bool NEWTON, bool WIDE>
+template <bool MI, bool COUNT, bool NEWTON, bool WIDE, bool FLD>
 __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int jb, int j1, double shx, double shy,
-                                           double shz, const RealArgs &a, WarpBuf &wb, int lane,
+                                           double shz, const RealArgs &a, WarpBufT<FLD> &wb, int lane,
                                            const PreTargets &pt, const double3 org, int tbase, int hs,
                                            double *__restrict__ acc_src, int &singular, long long &cnt) {
     const int j = jb + lane;
@@ -397,7 +466,7 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
             if (hit & (1u << b)) *dst++ = (unsigned short)(((b & 1) ? tagb : taga) + (b >> 1));
     }
     __syncwarp();
-    double *__restrict__ acc_batch = acc_src + jb;  // source-side sums of this batch
+    double *__restrict__ acc_batch = acc_src + (FLD ? 3 : 1) * jb;  // source-side sums of this batch
     for (int e0 = 0; e0 < total; e0 += 64) {
         const int rem = total - e0;
         if (rem > 32) {
@@ -407,22 +476,22 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
             const unsigned en1 = wb.ent[e0 + lane];
             const unsigned en2 = v2 ? wb.ent[e0 + 32 + lane] : en1;
             Hit h1, h2;
-            const double x1 = hit_geometry<MI, NEWTON>(en1, true, a, wb, jb, tbase, singular, h1);
-            const double x2 = hit_geometry<MI, NEWTON>(en2, v2, a, wb, jb, tbase, singular, h2);
-            h1.f = erfc_fast<WIDE>(x1, h1.f);
-            h2.f = erfc_fast<WIDE>(x2, h2.f);
+            const double x1 = hit_geometry<MI, NEWTON, FLD>(en1, true, a, wb, jb, tbase, singular, h1);
+            const double x2 = hit_geometry<MI, NEWTON, FLD>(en2, v2, a, wb, jb, tbase, singular, h2);
+            hit_value<WIDE, FLD>(x1, a, h1);
+            hit_value<WIDE, FLD>(x2, a, h2);
             if (COUNT) {
                 cnt += (h1.ok ? (NEWTON ? 2 : 1) : 0) + (h2.ok ? (NEWTON ? 2 : 1) : 0);
             } else {
-                apply_hit<NEWTON>(h1, wb, lane, acc_batch);
-                apply_hit<NEWTON>(h2, wb, lane, acc_batch);
+                apply_hit<NEWTON, FLD>(h1, wb, lane, acc_batch);
+                apply_hit<NEWTON, FLD>(h2, wb, lane, acc_batch);
             }
         } else if (lane < rem) {
-            const Hit h = eval_hit<MI, NEWTON, WIDE>(wb.ent[e0 + lane], a, wb, jb, tbase, singular);
+            const Hit h = eval_hit<MI, NEWTON, WIDE, FLD>(wb.ent[e0 + lane], a, wb, jb, tbase, singular);
             if (COUNT)
                 cnt += h.ok ? (NEWTON ? 2 : 1) : 0;
             else
-                apply_hit<NEWTON>(h, wb, lane, acc_batch);
+                apply_hit<NEWTON, FLD>(h, wb, lane, acc_batch);
         }
     }
     __syncwarp();
@@ -448,14 +517,14 @@ __device__ __forceinline__ int zbound(const double4 *__restrict__ rec, int lo, i
 // partial sums of both sides go to acc_src (sorted order, zeroed before) and
 // a finishing kernel scatters them.  Otherwise the full column neighbourhood
 // and direct writes of phi (minimum-image mode for < 5 cells per axis).
-template <bool MI, bool COUNT, bool NEWTON, bool WIDE>
-__global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel(
+template <bool MI, bool COUNT, bool NEWTON, bool WIDE, bool FLD>
+__global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlocks) realspace_cell_kernel(
     const double4 *__restrict__ rec, const int *__restrict__ sidx, const int *__restrict__ starts,
     const int4 *__restrict__ units, const int *__restrict__ nunits, RealArgs a, double *__restrict__ phi,
     double *__restrict__ acc_src, int *__restrict__ flag, unsigned long long *__restrict__ npairs) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpBuf &wb = reinterpret_cast<WarpBuf *>(smem_raw)[warp];
+    WarpBufT<FLD> &wb = reinterpret_cast<WarpBufT<FLD> *>(smem_raw)[warp];
     const int u = blockIdx.x * kWarps + warp;
     if (u >= *nunits) return;
     const int4 un = units[u];
@@ -471,7 +540,9 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
         wb.txy[tslot(lane)] = make_double2(tp.x, tp.y);
         wb.tzq[tslot(lane)] = make_double2(tp.z, tp.w);
     }
-    for (int i = 0; i < kT; ++i) wb.acc[i][lane] = 0.0;
+#pragma unroll
+    for (int c = 0; c < (FLD ? 3 : 1); ++c)
+        for (int i = 0; i < kT; ++i) wb.acc[c][i][lane] = 0.0;
     // z extent of the unit's targets (a unit is a z-slab of its column)
     double zmin = active ? tp.z : 1e300, zmax = active ? tp.z : -1e300;
     for (int o = 16; o > 0; o >>= 1) {
@@ -519,7 +590,7 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
 
     auto run = [&](int j0, int j1, double shx, double shy, double shz, int hs) {
         for (int jb = j0; jb < j1; jb += 32)
-            pair_batch<MI, COUNT, NEWTON, WIDE>(rec, jb, j1, shx, shy, shz, a, wb, lane, pt, org, un.y, hs, acc_src,
+            pair_batch<MI, COUNT, NEWTON, WIDE, FLD>(rec, jb, j1, shx, shy, shz, a, wb, lane, pt, org, un.y, hs, acc_src,
                                                 singular, cnt);
     };
     if (MI) {
@@ -609,15 +680,35 @@ __global__ void __launch_bounds__(32 * kWarps, kMinBlocks) realspace_cell_kernel
     if (__any_sync(0xffffffffu, singular) && lane == 0) atomicExch(flag, 1);
     __syncwarp();
     if (active && lane < kT) {
-        double v = 0.0;
-        for (int i = 0; i < 32; ++i) v += wb.acc[tslot(tl)][(tl + i) & 31];
-        if (NEWTON) {
-            atomicAdd(acc_src + t, v);
-        } else {
-            if (a.add_self) v += (-2.0 * a.xi * tp.w) / a.sqrtpi;
-            phi[sidx[t]] = v;
+#pragma unroll
+        for (int c = 0; c < (FLD ? 3 : 1); ++c) {
+            double v = 0.0;
+            for (int i = 0; i < 32; ++i) v += wb.acc[c][tslot(tl)][(tl + i) & 31];
+            if (FLD) {
+                // field: no self term (the Ewald self-interaction is a constant)
+                if (NEWTON)
+                    atomicAdd(acc_src + 3 * t + c, v);
+                else
+                    phi[3 * (int64_t)sidx[t] + c] = v;
+            } else if (NEWTON) {
+                atomicAdd(acc_src + t, v);
+            } else {
+                if (a.add_self) v += (-2.0 * a.xi * tp.w) / a.sqrtpi;
+                phi[sidx[t]] = v;
+            }
         }
     }
+}
+
+// NEWTON finish, field mode: E[orig] = accumulated (3 components)
+__global__ void realspace_finish_field_kernel(const double *__restrict__ acc, const int *__restrict__ sidx, int64_t N,
+                                              double *__restrict__ E) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int64_t o = 3 * (int64_t)sidx[i];
+    E[o] = acc[3 * i];
+    E[o + 1] = acc[3 * i + 1];
+    E[o + 2] = acc[3 * i + 2];
 }
 
 // NEWTON finish: phi[orig] = accumulated pair sums (+ the self term of owned targets)
@@ -631,6 +722,7 @@ __global__ void realspace_finish_kernel(const double *__restrict__ acc, const do
 }
 
 // rc > L/2 with periodic axes: explicit images (realspace.py:138-165)
+template <bool FLD>
 __global__ void realspace_image_kernel(const double *__restrict__ pos, const double *__restrict__ q, int64_t N,
                                        int64_t rlo, int64_t rhi, RealArgs a, int D, int layers,
                                        double *__restrict__ phi, int *__restrict__ flag) {
@@ -640,7 +732,7 @@ __global__ void realspace_image_kernel(const double *__restrict__ pos, const dou
     if (!own) return;
     double xt = pos[3 * t], yt = pos[3 * t + 1], zt = pos[3 * t + 2];
     int lx = D >= 1 ? layers : 0, ly = D >= 2 ? layers : 0, lz = D >= 3 ? layers : 0;
-    double acc = 0.0;
+    double acc = 0.0, ex = 0.0, ey = 0.0, ez = 0.0;
     int err = 0;
     for (int ax = -lx; ax <= lx; ++ax)
         for (int ay = -ly; ay <= ly; ++ay)
@@ -658,11 +750,26 @@ __global__ void realspace_image_kernel(const double *__restrict__ pos, const dou
                         else if (s != t) err = err ? err : 1;
                         continue;
                     }
-                    if (r < a.rc) img += q[s] * (erfc(a.xi * r) / r);
+                    if (r < a.rc) {
+                        if (FLD) {
+                            const double g = q[s] * (erfc(a.xi * r) / r + kTwoOverSqrtPi * a.xi * exp(-a.xi * a.xi * r * r)) / (r * r);
+                            ex += g * dx;
+                            ey += g * dy;
+                            ez += g * dz;
+                        } else {
+                            img += q[s] * (erfc(a.xi * r) / r);
+                        }
+                    }
                 }
                 acc += img;
             }
     if (err) atomicMax(flag, err);
+    if (FLD) {
+        phi[3 * t] = ex;
+        phi[3 * t + 1] = ey;
+        phi[3 * t + 2] = ez;
+        return;
+    }
     double v = acc;
     if (a.add_self) v += (-2.0 * a.xi * q[t]) / a.sqrtpi;
     phi[t] = v;
@@ -724,7 +831,7 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     prof_end(pl, SE_K_SORT);
 }
 
-template <bool COUNT>
+template <bool COUNT, bool FLD = false>
 static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, unsigned long long *npairs) {
     const CellGeom &c = pl->cell;
     int nbins = c.n * c.n;
@@ -732,12 +839,13 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
     const bool mi = c.mode[0] == 2 || c.mode[1] == 2 || c.mode[2] == 2;
     unsigned blocks = (unsigned)((maxu + kWarps - 1) / kWarps);
     cudaStream_t st = pl->stream;
-    const size_t smem = sizeof(WarpBuf) * kWarps;
+    const size_t smem = sizeof(WarpBufT<FLD>) * kWarps;
+    const int nc = FLD ? 3 : 1;
     double *acc = nullptr;
     if (!mi) {
-        pl->racc.ensure(sizeof(double) * N);
+        pl->racc.ensure(sizeof(double) * nc * N);
         acc = pl->racc.as<double>();
-        SE_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * N, st));
+        SE_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * nc * N, st));
     }
     auto args = [&](auto kern) {
         SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -749,29 +857,38 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
     // narrow kernels: x = xi r <= xi rc (1 + 2e-5) for every prefiltered pair
     const bool wide = a.xi * a.rc * (1.0 + 1e-4) > SE_ERFC_XMAX;
     if (mi)
-        args(wide ? realspace_cell_kernel<true, COUNT, false, true> : realspace_cell_kernel<true, COUNT, false, false>);
+        args(wide ? realspace_cell_kernel<true, COUNT, false, true, FLD>
+                  : realspace_cell_kernel<true, COUNT, false, false, FLD>);
     else
-        args(wide ? realspace_cell_kernel<false, COUNT, true, true> : realspace_cell_kernel<false, COUNT, true, false>);
+        args(wide ? realspace_cell_kernel<false, COUNT, true, true, FLD>
+                  : realspace_cell_kernel<false, COUNT, true, false, FLD>);
     SE_LAUNCH_CHECK();
     pl->launches += 1;
     if (!mi && !COUNT) {
-        realspace_finish_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(acc, pl->cbin.rec.as<double4>(),
-                                                                           pl->cbin.idx_sorted.as<int>(), N, a, phi);
+        if (FLD)
+            realspace_finish_field_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(
+                acc, pl->cbin.idx_sorted.as<int>(), N, phi);
+        else
+            realspace_finish_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(acc, pl->cbin.rec.as<double4>(),
+                                                                               pl->cbin.idx_sorted.as<int>(), N, a,
+                                                                               phi);
         SE_LAUNCH_CHECK();
         pl->launches += 1;
     }
     if (!COUNT) prof_end(pl, SE_K_REALSPACE);
 }
 
-void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, int add_self, int rank,
-                   int world) {
+template <bool FLD>
+static void realspace_impl(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, int add_self,
+                           int rank, int world) {
     const double L = pl->L, rc = pl->p.rc, xi = pl->p.xi;
     const int D = pl->D;
+    const int nc = FLD ? 3 : 1;
     if (!(xi > 0) || !(rc > 0)) fail(SE_EINVAL, "xi and rc must be positive");
     cudaStream_t st = pl->stream;
     pl->flag.ensure(sizeof(int) * 4);
     SE_CUDA(cudaMemsetAsync(pl->flag.ptr, 0, sizeof(int) * 4, st));
-    if (world > 1) SE_CUDA(cudaMemsetAsync(phi, 0, sizeof(double) * (N > 0 ? N : 1), st));
+    if (world > 1) SE_CUDA(cudaMemsetAsync(phi, 0, sizeof(double) * nc * (N > 0 ? N : 1), st));
     if (N <= 0) return;
     RealArgs a{};
     a.L = L;
@@ -786,15 +903,29 @@ void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, d
     if (D >= 1 && rc > L / 2 + 1e-12) {
         int layers = (int)std::floor((rc + L / 2) / L) + 1;
         prof_begin(pl, SE_K_REALSPACE);
-        realspace_image_kernel<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(pos, q, N, a.rlo, a.rhi, a, D, layers, phi,
-                                                                           pl->flag.as<int>());
+        realspace_image_kernel<FLD><<<(unsigned)((N + 127) / 128), 128, 0, st>>>(pos, q, N, a.rlo, a.rhi, a, D, layers,
+                                                                                phi, pl->flag.as<int>());
         SE_LAUNCH_CHECK();
         prof_end(pl, SE_K_REALSPACE);
         pl->launches += 1;
     } else {
         cell_bin(pl, pos, q, N, a);
-        launch_cell<false>(pl, N, a, phi, nullptr);
+        launch_cell<false, FLD>(pl, N, a, phi, nullptr);
     }
+}
+
+void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, int add_self, int rank,
+                   int world) {
+    realspace_impl<false>(pl, pos, q, N, phi, add_self, rank, world);
+}
+
+// Real-space part of the electric field E_R = -grad phi_R at every particle
+// (N x 3, caller order): sum over in-cutoff pairs of
+// q_s (erfc(xi r)/r + (2 xi/sqrt(pi)) exp(-xi^2 r^2)) (x_t - x_s) / r^2,
+// the same pair set, cell path and Newton symmetry as realspace_run.
+void realspace_field_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *E, int rank,
+                         int world) {
+    realspace_impl<true>(pl, pos, q, N, E, 0, rank, world);
 }
 
 void realspace_pair_count(se_plan *pl, const double *pos, const double *q, int64_t N, long long *pairs) {

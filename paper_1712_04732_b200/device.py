@@ -47,6 +47,23 @@ def total_potential(positions: torch.Tensor, charges: torch.Tensor, L: float, pa
     return out
 
 
+def total_field(positions: torch.Tensor, charges: torch.Tensor, L: float, params: SEParams,
+                periodicity: Periodicity, out: torch.Tensor | None = None) -> torch.Tensor:
+    """core.total_field on device tensors: E (N, 3), D = 3."""
+    N = charges.shape[0]
+    _check(positions, (N, 3), "positions")
+    _check(charges, (N,), "charges")
+    if periodicity.D != 3:
+        raise ValueError("the electric field (forces) covers D = 3")
+    params.validate(L, periodicity)
+    pl = plan(L, params, periodicity, positions.device)
+    if out is None:
+        out = torch.empty((N, 3), dtype=torch.float64, device=positions.device)
+    _native.call("se_total_field_dev", pl.handle, _native.ptr(positions), _native.ptr(charges), N,
+                 _native.ptr(out))
+    return out
+
+
 def kspace_potential(positions, charges, L, params, periodicity, use_kernel=None, out=None, timings=None):
     """sekspace.se_kspace on device tensors."""
     N = charges.shape[0]

@@ -1,0 +1,123 @@
+"""Electric field / forces (D = 3) on the device against the field oracle
+(pinned to the reference by central differences, tests/test_field_cpu.py)
+and against the direct Ewald field."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import se_oracle as orc  # noqa: E402
+
+import paper_1712_04732_b200 as se  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+G = np.load(os.path.join(ROOT, "tests", "golden", "field.npz"))
+
+
+def _rel(a, b):
+    return float(np.sqrt(np.mean((a - b) ** 2)) / np.sqrt(np.mean(b ** 2)))
+
+
+def _system(N, L, seed):
+    rng = np.random.default_rng(seed)
+    pos = rng.random((N, 3)) * L
+    q = rng.uniform(-1, 1, N)
+    q -= q.mean()
+    return pos, q
+
+
+def _prm_dict(p):
+    return dict(xi=p.xi, rc=p.rc, M=p.M, P=p.P, window=p.window, shape=p.shape)
+
+
+def test_field_matches_oracle_and_reference_differences():
+    # small box: few columns -> the minimum-image kernel
+    pos, q, L = G["pos"], G["q"], float(G["L"])
+    p = se.SEParams(xi=float(G["xi"]), rc=float(G["rc"]), M=32, P=16, window="gaussian",
+                    shape=float(np.sqrt(16 * np.pi)), eps=1e-12)
+    s = se.ParticleSystem(pos, q, L)
+    E = se.total_field(s, p, se.Periodicity(3))
+    ref = orc.total_field(pos, q, L, _prm_dict(p))
+    assert _rel(E, ref) < 1e-12
+    # against the reference's own potentials (real space + direct Fourier sum)
+    assert _rel(E, G["E_real_fd"] + G["E_kspace_direct_fd"]) < 1e-7
+    F = se.forces(s, p, se.Periodicity(3))  # a second evaluation: fp64 atomics reorder the last bits
+    assert _rel(F, q[:, None] * E) < 1e-14
+
+
+@pytest.mark.parametrize("window,P,shape", [("bm", 8, 20.0), ("gaussian", 12, float(np.sqrt(12 * np.pi))),
+                                            ("kb", 10, 25.0)])
+def test_field_newton_path_vs_oracle(window, P, shape):
+    # enough columns for the half-shell (Newton) kernel; all three windows
+    pos, q = _system(20000, 2.0, 61)
+    p = se.SEParams(xi=7.0, rc=0.55, M=40, P=P, window=window, shape=shape, eps=1e-8)
+    E = se.total_field(se.ParticleSystem(pos, q, 2.0), p, se.Periodicity(3))
+    sel = np.random.default_rng(1).choice(len(q), 300, replace=False)
+    er = orc.realspace_field(pos, q, 2.0, 3, p.xi, p.rc, targets=sel)
+    ek = orc.kspace_field_d3(pos, q, 2.0, _prm_dict(p))[sel]
+    assert _rel(E[sel], er + ek) < 1e-12
+
+
+def test_field_image_path_and_wide_erfc():
+    # rc > L/2: explicit images; xi rc > 6: the library-erfc kernel variant
+    pos, q = _system(200, 1.0, 62)
+    for xi, rc in ((5.0, 0.7), (14.0, 0.45)):
+        p = se.SEParams(xi=xi, rc=rc, M=32, P=12, window="bm", shape=30.0, eps=1e-8)
+        E = se.total_field(se.ParticleSystem(pos, q, 1.0), p, se.Periodicity(3))
+        ref = orc.total_field(pos, q, 1.0, _prm_dict(p))
+        assert _rel(E, ref) < 1e-12, (xi, rc)
+
+
+def test_field_device_api_and_rejections():
+    import torch
+
+    from paper_1712_04732_b200 import device as sedev
+
+    pos, q = _system(3000, 1.5, 63)
+    p = se.SEParams(xi=8.0, rc=0.45, M=32, P=8, window="bm", shape=20.0, eps=1e-8)
+    host = se.total_field(se.ParticleSystem(pos, q, 1.5), p, se.Periodicity(3))
+    dev = sedev.total_field(torch.from_numpy(pos).cuda(), torch.from_numpy(q).cuda(), 1.5, p,
+                            se.Periodicity(3)).cpu().numpy()
+    assert _rel(dev, host) < 1e-14
+    with pytest.raises(ValueError):
+        se.total_field(se.ParticleSystem(pos, q, 1.5), p, se.Periodicity(2))
+    with pytest.raises(ValueError):  # non-neutral periodic system
+        se.total_field(se.ParticleSystem(pos, q + 1.0, 1.5), p, se.Periodicity(3))
+
+
+def test_field_full_size_cfg2_momentum_and_differences():
+    # cfg2 at full size: Newton's third law holds pairwise in real space and
+    # the ik-differentiated Fourier field conserves momentum exactly, so
+    # sum q E = 0 to rounding; E = -grad phi against central differences of
+    # the device potential at a few particles (SE discretisation ~1e-6)
+    rng = np.random.default_rng(2)
+    N, L = 1_000_000, 10.0
+    pos = rng.random((N, 3)) * L
+    q = rng.uniform(-1, 1, N)
+    q -= q.mean()
+    p = se.SEParams(xi=4.2919, rc=1.0, M=128, P=8, window="bm", shape=20.0, eps=1e-8)
+    s = se.ParticleSystem(pos, q, L)
+    E = se.total_field(s, p, se.Periodicity(3))
+    F = q[:, None] * E
+    assert np.abs(F.sum(0)).max() < 1e-10 * np.abs(F).sum(0).max()
+    sel = np.random.default_rng(3).choice(N, 200, replace=False)
+    # sampled parity against the oracle at full size (the oracle spreads all
+    # 1e6 charges in numpy: ~15 s)
+    er = orc.realspace_field(pos, q, L, 3, p.xi, p.rc, targets=sel)
+    ek = orc.kspace_field_d3(pos, q, L, _prm_dict(p), targets=sel)
+    assert _rel(E[sel], er + ek) < 1e-11
+    d = 1e-4
+    for m in sel[:3]:
+        for a in range(3):
+            p1, p2 = pos.copy(), pos.copy()
+            p1[m, a] += d
+            p2[m, a] -= d
+            f1 = se.total_potential(se.ParticleSystem(p1, q, L), p, se.Periodicity(3))[m]
+            f2 = se.total_potential(se.ParticleSystem(p2, q, L), p, se.Periodicity(3))[m]
+            fd = -(f1 - f2) / (2 * d)
+            assert abs(fd - E[m, a]) < 1e-4 * np.abs(E[m]).max(), (m, a, fd, E[m, a])
