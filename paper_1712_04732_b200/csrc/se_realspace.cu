@@ -806,9 +806,14 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     a.zper = c.mode[2] == 1;
     int nbins = c.n * c.n;
     {
+        // z quantum L / 2^kb <= rc / 256: the windows' one-quantum slack and
+        // the index order inside a quantum cost nothing measurable, and the
+        // key stays short (cfg2: 10 + 12 bits, three radix passes, not four)
         int cb = 1;
         while ((1LL << cb) < (long long)nbins) ++cb;
-        a.kb = 32 - cb < 20 ? 32 - cb : 20;
+        int kz = 8;
+        while (kz < 20 && (double)(1 << kz) < 256.0 * L / rc) ++kz;
+        a.kb = std::min(32 - cb, kz);
         a.qinv = (double)(1 << a.kb) / L;
     }
     for (int ax = 0; ax < 3; ++ax) a.mode[ax] = c.mode[ax];
