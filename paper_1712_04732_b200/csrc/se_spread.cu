@@ -134,8 +134,10 @@ __global__ void tile_keys_hist_kernel(const double *__restrict__ pos, int64_t N,
 }
 
 // Stage the 3P window factors of a batch of particles.  wts layout:
-// [p][axis][t]; loc: [p][4] = local start (x,y,z) within the padded tile and
-// the sorted index.  FOLDQ multiplies the x factors by the charge.  PC > 0
+// [p][axis][t]; loc: [p][4] = the local start (x, y, z) within the padded
+// tile as bytes 0..2 of loc[p][0] (one broadcast LDS.32 for the consumers
+// instead of three; each axis task writes its own byte), loc[p][3] = the
+// sorted index.  FOLDQ multiplies the x factors by the charge.  PC > 0
 // is the window support P as a compile-time constant (0: runtime a.P).
 template <int WIN, bool FOLDQ, int PC>
 __device__ __forceinline__ void stage_batch(const double4 *__restrict__ rec, int s0, int nb, const int org[3],
@@ -156,7 +158,7 @@ __device__ __forceinline__ void stage_batch(const double4 *__restrict__ rec, int
             if (FOLDQ && ax == 0) v = __dmul_rn(r.w, v);
             wo[t] = v;
         }
-        loc[p * 4 + ax] = start_index(f, ax, a) - org[ax];
+        reinterpret_cast<unsigned char *>(loc + p * 4)[ax] = (unsigned char)(start_index(f, ax, a) - org[ax]);
         if (ax == 0) loc[p * 4 + 3] = s0 + p;
     }
 }
@@ -301,7 +303,8 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
         stage_batch<WIN, true, PC>(rec, b0, nb, org, a, wts, loc);
         __syncthreads();
         for (int p = 0; p < nb; ++p) {
-            const int lx0 = loc[p * 4], ly0 = loc[p * 4 + 1], lz0 = loc[p * 4 + 2];
+            const int pk = loc[p * 4];
+            const int lx0 = pk & 0xff, ly0 = (pk >> 8) & 0xff, lz0 = (pk >> 16) & 0xff;
             const double *wx = wts + p * 3 * P, *wy = wx + P, *wz = wy + P;
             if (PC > 0) {
                 // nwarps == P: this warp owns exactly one x-plane of the particle
@@ -374,7 +377,8 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
         stage_batch<WIN, false, PC>(rec, b0, nb, org, a, wts, loc);
         __syncthreads();
         for (int p = warp; p < nb; p += nw) {
-            const int lx0 = loc[p * 4], ly0 = loc[p * 4 + 1], lz0 = loc[p * 4 + 2];
+            const int pk = loc[p * 4];
+            const int lx0 = pk & 0xff, ly0 = (pk >> 8) & 0xff, lz0 = (pk >> 16) & 0xff;
             const double *wx = wts + p * 3 * P, *wy = wx + P, *wz = wy + P;
             double acc = 0.0;
             if (PC > 0) {
