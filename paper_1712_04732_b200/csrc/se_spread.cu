@@ -376,7 +376,8 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
         __syncthreads();
         stage_batch<WIN, false, PC>(rec, b0, nb, org, a, wts, loc);
         __syncthreads();
-        for (int p = warp; p < nb; p += nw) {
+        // this lane's share of particle p's P^3 sum
+        auto partial = [&](int p) -> double {
             const int pk = loc[p * 4];
             const int lx0 = pk & 0xff, ly0 = (pk >> 8) & 0xff, lz0 = (pk >> 16) & 0xff;
             const double *wx = wts + p * 3 * P, *wy = wx + P, *wz = wy + P;
@@ -402,13 +403,31 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
                     acc = fma(__dmul_rn(wy[ty], wz[tz]), s, acc);
                 }
             }
+            return acc;
+        };
+        auto store = [&](int p, double acc) {
+            const int orig = sidx[loc[p * 4 + 3]];
+            const double v = acc * h3;
+            phi[orig] = accumulate ? phi[orig] + v : v;
+        };
+        // two particles per pass with one reduce-scatter: after the xor-16
+        // exchange lanes 0-15 hold particle p's pair sums, lanes 16-31 those
+        // of p + nw (5 shuffles for two particles instead of 10)
+        int p = warp;
+        for (; p + nw < nb; p += 2 * nw) {
+            const double a0 = partial(p), a1 = partial(p + nw);
+            const bool hi = (lane & 16) != 0;
+            double v = hi ? a1 : a0;
+            v += __shfl_xor_sync(0xffffffffu, hi ? a0 : a1, 16);
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if ((lane & 15) == 0) store(hi ? p + nw : p, v);
+        }
+        if (p < nb) {
+            double acc = partial(p);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) {
-                int orig = sidx[loc[p * 4 + 3]];
-                double v = acc * h3;
-                phi[orig] = accumulate ? phi[orig] + v : v;
-            }
+            if (lane == 0) store(p, acc);
         }
     }
 }
