@@ -525,7 +525,9 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpBufT<FLD> &wb = reinterpret_cast<WarpBufT<FLD> *>(smem_raw)[warp];
-    const int u = blockIdx.x * kWarps + warp;
+    // units from the one holding this shard's first target (nunits[1]; 0 for
+    // one rank): a rank launches only about its share of the units
+    const int u = nunits[1] + blockIdx.x * kWarps + warp;
     if (u >= *nunits) return;
     const int4 un = units[u];
     const int n = a.n;
@@ -777,6 +779,9 @@ __global__ void realspace_image_kernel(const double *__restrict__ pos, const dou
 
 // targets per work unit: kT, or half of it for small systems (latency bound:
 // more, shorter units keep more warps in flight)
+// (by the total particle count: for a shard of a large system the 16-target
+// units stay faster -- 8-target units measured 2.27 vs 1.96 ms per cfg2 rank
+// at 8 ranks)
 static int real_unit(int64_t N) { return N < 50000 ? kT / 2 : kT; }
 
 // columns of edge >= rc/reach and the particle binning by (column, z)
@@ -819,7 +824,8 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     for (int ax = 0; ax < 3; ++ax) a.mode[ax] = c.mode[ax];
     cudaStream_t st = pl->stream;
     prof_begin(pl, SE_K_SORT);
-    binning_reserve(pl->cbin, N, nbins, real_unit(N), a.kb);
+    const int unit = real_unit(N);
+    binning_reserve(pl->cbin, N, nbins, unit, a.kb);
     SE_CUDA(cudaMemsetAsync(pl->cbin.counts.ptr, 0, sizeof(int) * (nbins + 1), st));
     if (nbins <= kHistSmem) {
         int64_t blocks = (N + 4095) / 4096;  // ~16 particles per thread
@@ -832,7 +838,7 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     }
     SE_LAUNCH_CHECK();
     pl->launches += 1;
-    binning_sort(pl, pl->cbin, pos, q, N, nbins, real_unit(N), a.kb);
+    binning_sort(pl, pl->cbin, pos, q, N, nbins, unit, a.kb, a.rlo);
     prof_end(pl, SE_K_SORT);
 }
 
@@ -840,7 +846,11 @@ template <bool COUNT, bool FLD = false>
 static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, unsigned long long *npairs) {
     const CellGeom &c = pl->cell;
     int nbins = c.n * c.n;
-    int64_t maxu = binning_max_units(pl->cbin, N, nbins, real_unit(N));
+    const int unit = real_unit(N);
+    int64_t maxu = binning_max_units(pl->cbin, N, nbins, unit);
+    // a shard [rlo, rhi) spans at most its targets / unit + one partial unit
+    // per column + 1 units from nunits[1] on
+    if (a.rhi - a.rlo < N) maxu = std::min<int64_t>(maxu, (a.rhi - a.rlo) / unit + nbins + 2);
     const bool mi = c.mode[0] == 2 || c.mode[1] == 2 || c.mode[2] == 2;
     unsigned blocks = (unsigned)((maxu + kWarps - 1) / kWarps);
     cudaStream_t st = pl->stream;

@@ -28,9 +28,11 @@ __global__ void gather_records_kernel(const double *__restrict__ pos, const doub
 // One CTA: exclusive scans of bin counts and of per-bin unit counts, then the
 // unit list.  nbins is at most a few 1e5 (tiles or cells), so a single CTA
 // with a serial per-thread pass is a few microseconds.
+// nunits[0] = number of units; nunits[1] = the unit holding sorted position
+// rlo (the first unit of a rank's shard; the unit count if rlo >= N).
 __global__ void __launch_bounds__(1024) build_units_kernel(const int *__restrict__ counts, int nbins, int chunk,
                                                            int *__restrict__ starts, int4 *__restrict__ units,
-                                                           int *__restrict__ nunits) {
+                                                           int *__restrict__ nunits, int64_t rlo) {
     typedef cub::BlockScan<long long, 1024> Scan;
     __shared__ typename Scan::TempStorage tmp;
     const int per = (nbins + 1023) / 1024;
@@ -49,13 +51,16 @@ __global__ void __launch_bounds__(1024) build_units_kernel(const int *__restrict
         int c = counts[b];
         starts[b] = (int)cpos;
         for (int s = 0; s < c; s += chunk) {
-            units[upos++] = make_int4(b, (int)cpos + s, min(chunk, c - s), 0);
+            const int len = min(chunk, c - s);
+            if (rlo >= cpos + s && rlo < cpos + s + len) nunits[1] = (int)upos;
+            units[upos++] = make_int4(b, (int)cpos + s, len, 0);
         }
         cpos += c;
     }
     if (threadIdx.x == 1023) {
         starts[nbins] = (int)cpos;
         *nunits = (int)upos;
+        if (rlo >= cpos) nunits[1] = (int)upos;
     }
 }
 
@@ -97,7 +102,7 @@ void binning_reserve(Binning &b, int64_t N, int nbins, int chunk, int extra_bits
 
 // Keys must already be in b.keys and the histogram in b.counts.
 void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, int64_t N, int nbins, int chunk,
-                  int extra_bits) {
+                  int extra_bits, int64_t rlo) {
     cudaStream_t st = pl->stream;
     if (N > 0) {
         size_t bytes = b.cub_bytes;
@@ -111,7 +116,7 @@ void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, i
         pl->launches += 1;
     }
     build_units_kernel<<<1, 1024, 0, st>>>(b.counts.as<int>(), nbins, chunk, b.starts.as<int>(),
-                                           b.units.as<int4>(), b.nunits.as<int>());
+                                           b.units.as<int4>(), b.nunits.as<int>(), rlo);
     SE_LAUNCH_CHECK();
     pl->launches += 1;
 }
