@@ -39,7 +39,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native
-from .core import Periodicity, SEParams
+from .core import Periodicity, SEParams, SingularConfigurationError
 
 
 class NativeBackend:
@@ -196,9 +196,28 @@ def total_potential_sharded(pos, q, backend, group=None, kspace: str = "replicat
         phi.add_(phik)
     if init and reduce_phi:
         dist.all_reduce(phi, op=dist.ReduceOp.SUM, group=group)
-    if hasattr(backend, "finish"):
-        backend.finish()
+    _finish(backend, phi, group, init and world > 1)
     return phi
+
+
+def _finish(backend, like, group, multi):
+    """Deferred device checks of this call, agreed over the ranks: a rank
+    whose shard found coincident particles (realspace.py:118-122) raises
+    SingularConfigurationError, and so does every other rank (instead of
+    entering the next collective alone)."""
+    err = None
+    if hasattr(backend, "finish"):
+        try:
+            backend.finish()
+        except SingularConfigurationError as e:
+            err = e
+    if multi:
+        flag = torch.tensor([1.0 if err is not None else 0.0], dtype=torch.float64, device=like.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+        if err is None and flag.item() > 0:
+            err = SingularConfigurationError("coincident distinct particles (detected on another rank)")
+    if err is not None:
+        raise err
 
 
 def total_potential_partitioned(pos_local, q_local, backend, group=None, kspace: str = "replicated"):

@@ -202,3 +202,41 @@ def test_shard_bounds_cover_exactly():
             spans = [shard_bounds(N, r, world) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == N
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def _worker_error(rank, world, port, out_path):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "oracle")]
+    import se_oracle as orc
+    from paper_1712_04732_b200.core import SingularConfigurationError
+    from paper_1712_04732_b200.distributed import total_potential_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pos, q, L, prm = _inputs()
+
+    class Failing(OracleBackend):
+        # a deferred device error found by rank 0's shard only
+        def finish(self):
+            if rank == 0:
+                raise SingularConfigurationError("coincident distinct particles")
+
+    try:
+        total_potential_sharded(torch.from_numpy(pos), torch.from_numpy(q), Failing(orc, pos, q, L, 3, prm))
+        outcome = "returned"
+    except SingularConfigurationError:
+        outcome = "raised"
+    # the ranks are still in step: one more collective completes
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    open(f"{out_path}.{rank}", "w").write(f"{outcome} {int(t.item())}")
+    dist.destroy_process_group()
+
+
+def test_deferred_error_raised_on_every_rank(tmp_path):
+    world = 2
+    out = str(tmp_path / "err")
+    mp.spawn(_worker_error, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        assert open(f"{out}.{r}").read() == "raised 2"
