@@ -121,3 +121,28 @@ def test_field_full_size_cfg2_momentum_and_differences():
             f2 = se.total_potential(se.ParticleSystem(p2, q, L), p, se.Periodicity(3))[m]
             fd = -(f1 - f2) / (2 * d)
             assert abs(fd - E[m, a]) < 1e-4 * np.abs(E[m]).max(), (m, a, fd, E[m, a])
+
+
+def test_field_randomized_configurations():
+    # seeded random D = 3 configurations across the kernel variants (minimum
+    # image / Newton / image path / wide erfc), windows and supports
+    rng = np.random.default_rng(2024)
+    worst = 0.0
+    for case in range(12):
+        N = int(rng.integers(40, 1500))
+        L = float(rng.uniform(0.8, 3.0))
+        M = int(rng.choice([16, 24, 32, 40]))
+        P = int(rng.choice([4, 6, 8, 10, 12]))
+        P = min(P, M)
+        window = str(rng.choice(["gaussian", "bm", "kb"]))
+        shape = {"gaussian": float(np.sqrt(np.pi * P)), "bm": 2.5 * P, "kb": 2.5 * P}[window]
+        rc = float(rng.uniform(0.15, 0.7)) * L
+        xi = float(rng.uniform(2.5, 7.5)) / rc
+        pos, q = _system(N, L, 1000 + case)
+        p = se.SEParams(xi=xi, rc=rc, M=M, P=P, window=window, shape=shape, eps=1e-8)
+        E = se.total_field(se.ParticleSystem(pos, q, L), p, se.Periodicity(3))
+        ref = orc.total_field(pos, q, L, _prm_dict(p))
+        err = _rel(E, ref)
+        worst = max(worst, err)
+        assert err < 1e-11, (case, N, L, M, P, window, rc, xi, err)
+    print(f"randomized field cases: worst relative RMS {worst:.2e}")
