@@ -1,5 +1,6 @@
 // Micro-benchmarks for the roofline denominators MEASURED_PEAKS.json lacks:
-// fp64 FMA throughput, shared-memory bandwidth (64-bit LDS/STS), native
+// fp64 FMA throughput, fp64 tensor-core MMA (DMMA) throughput,
+// shared-memory bandwidth (64-bit LDS/STS), native
 // fp64 global reductions (REDG.E.ADD.F64) into an L2-resident array, and an
 // fp64 copy (HBM) as a cross-check.  Prints one JSON object.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o peaks tools/peaks.cu
@@ -28,6 +29,24 @@ __global__ void dfma_kernel(double *out, int iters, double a, double b) {
     double s = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) s += x[j];
+    if (s == 12345.678) out[0] = s;
+}
+
+// fp64 tensor-core MMA (mma.sync.m8n8k4.f64, DMMA): 4 independent
+// accumulator tiles per warp, 2 * 8 * 8 * 4 = 512 flop per instruction
+__global__ void dmma_kernel(double *out, int iters, double a0, double b0) {
+    double a = a0 + threadIdx.x * 1e-12, b = b0;
+    double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(c[j][0]), "+d"(c[j][1])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s += c[j][0] + c[j][1];
     if (s == 12345.678) out[0] = s;
 }
 
@@ -90,6 +109,10 @@ int main() {
     float ms = time_ms([&] { dfma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7); }, 5);
     double flops = 2.0 * 8 * iters * (double)blocks * threads;
     double fp64_tflops = flops / (ms * 1e-3) / 1e12;
+    // fp64 tensor-core MMA
+    int diters = 4096;
+    ms = time_ms([&] { dmma_kernel<<<sms * 8, 256>>>(out, diters, 1e-3, 1e-3); }, 5);
+    double dmma_tflops = 512.0 * 4 * diters * (sms * 8 * 256 / 32.0) / (ms * 1e-3) / 1e12;
     // shared memory: one LDS.64 + one STS.64 per thread-iteration
     int siters = 1 << 14;
     ms = time_ms([&] { smem_kernel<<<sms * 4, 512>>>(out, siters); }, 5);
@@ -114,10 +137,10 @@ int main() {
     double hbm = 2.0 * cn * 16 / (ms * 1e-3) / 1e9;
     cudaDeviceProp prop;
     cudaGetDeviceProperties(&prop, 0);
-    printf("{\"gpu\": \"%s\", \"sms\": %d, \"fp64_fma_tflops\": %.2f, \"smem_tbs\": %.2f, "
+    printf("{\"gpu\": \"%s\", \"sms\": %d, \"fp64_fma_tflops\": %.2f, \"fp64_dmma_tflops\": %.2f, \"smem_tbs\": %.2f, "
            "\"redg_f64_gops\": %.2f, \"copy_hbm_gbs\": %.1f, "
            "\"how\": \"dfma 8 chains x %d iters x %d blocks x 256; smem LDS.64+STS.64 per iter; "
            "REDG.F64 to a 16 MB array, 8 x 256 thr per SM; float2x2 copy of 1 GiB; best of 5, CUDA events\"}\n",
-           prop.name, sms, fp64_tflops, smem_tbs, red_g, hbm, iters, blocks);
+           prop.name, sms, fp64_tflops, dmma_tflops, smem_tbs, red_g, hbm, iters, blocks);
     return 0;
 }
