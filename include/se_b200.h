@@ -213,6 +213,10 @@ int se_realspace_shard_dev(se_plan_t plan, const double *pos, const double *q, i
  * constant).  Errors as se_total_potential_*. */
 int se_total_field_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E);
 int se_total_field_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E);
+/* The two parts separately (host pointers): the real-space pair field (any
+ * D; the same pair set as real_space_sum) and the Fourier field (D = 3). */
+int se_realspace_field_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E);
+int se_kspace_field_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E);
 
 /* Slab-decomposed k-space stage of D = 3 (aft.py:203-206 + sekspace.py:198-206
  * + aft.py:237-238 split over `world` ranks).  Rank r owns the

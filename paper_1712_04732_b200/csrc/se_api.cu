@@ -633,10 +633,11 @@ __global__ void field_combine_kernel(const double *__restrict__ ek, int64_t N, d
 // E = E_R + E_F at every particle (D = 3): the real-space field kernel, then
 // spread -> scaled spectrum -> three differentiated inverse transforms ->
 // three gathers, summed into E (N x 3, caller order).
-void field_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *E) {
+// Fourier part of the field (D = 3): spread -> scaled spectrum -> three
+// differentiated inverse transforms -> three gathers; E = E_F (accumulate
+// 0) or E += E_F.
+void kspace_field_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *E, int accumulate) {
     if (pl->D != 3) fail(SE_EINVAL, "the electric field (forces) covers D = 3");
-    check_system(pl, pos, q, N, true);
-    realspace_field_run(pl, pos, q, N, E, 0, 1);
     if (N <= 0) return;
     const size_t G = grid_points(pl);
     pl->grid_dev.ensure(sizeof(double) * G);
@@ -649,11 +650,44 @@ void field_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, 
     prof_end(pl, SE_K_KSPACE);
     for (int a = 0; a < 3; ++a)
         gather_run(pl, pl->fgrid.as<double>() + a * G, pos, N, pl->fphi.as<double>() + a * N, 0, 0, 1, false);
+    if (!accumulate) SE_CUDA(cudaMemsetAsync(E, 0, sizeof(double) * 3 * N, pl->stream));
     field_combine_kernel<<<(unsigned)((N + 255) / 256), 256, 0, pl->stream>>>(pl->fphi.as<double>(), N, E);
     SE_LAUNCH_CHECK();
     pl->launches += 1;
+}
+
+void field_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *E) {
+    if (pl->D != 3) fail(SE_EINVAL, "the electric field (forces) covers D = 3");
+    check_system(pl, pos, q, N, true);
+    realspace_field_run(pl, pos, q, N, E, 0, 1);
+    kspace_field_pipeline(pl, pos, q, N, E, 1);
     check_flag(pl);
     prof_collect(pl);
+}
+
+int se_realspace_field_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    const double *dp = stage_in(pl, pl->io_pos, pos, 3 * (size_t)N);
+    const double *dq = stage_in(pl, pl->io_q, q, (size_t)N);
+    pl->io_E.ensure(sizeof(double) * 3 * (N ? N : 1));
+    realspace_field_run(pl, dp, dq, N, pl->io_E.as<double>(), 0, 1);
+    check_flag(pl);
+    stage_out(pl, E, pl->io_E.ptr, sizeof(double) * 3 * N);
+    SE_API_END
+}
+
+int se_kspace_field_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    const double *dp = stage_in(pl, pl->io_pos, pos, 3 * (size_t)N);
+    const double *dq = stage_in(pl, pl->io_q, q, (size_t)N);
+    pl->io_E.ensure(sizeof(double) * 3 * (N ? N : 1));
+    kspace_field_pipeline(pl, dp, dq, N, pl->io_E.as<double>(), 0);
+    stage_out(pl, E, pl->io_E.ptr, sizeof(double) * 3 * N);
+    SE_API_END
 }
 
 int se_total_field_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E) {

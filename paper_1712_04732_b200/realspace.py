@@ -66,6 +66,20 @@ def real_space_sum(system: ParticleSystem, xi: float, rc: float, periodicity: Pe
     return phi
 
 
+def real_space_field(system: ParticleSystem, xi: float, rc: float, periodicity: Periodicity,
+                     threads: int = 1) -> np.ndarray:
+    """Real-space part of E = -grad phi, (N, 3): sum over the pairs / images
+    of real_space_sum of q_n (erfc(xi r)/r + 2 xi/sqrt(pi) e^{-xi^2 r^2})
+    (x_m - x_n)/r^2.  Beyond the reference (forces)."""
+    if xi <= 0 or rc <= 0:
+        raise ValueError("xi and rc must be positive")
+    plan = _native.plan_for(periodicity.D, system.L, _real_params(xi, rc))
+    E = np.empty((system.N, 3))
+    _native.call("se_realspace_field_host", plan.handle, _native.ptr(system.positions),
+                 _native.ptr(system.charges), system.N, _native.ptr(E))
+    return E
+
+
 def self_term(q, xi: float) -> np.ndarray:
     """-2 xi q / sqrt(pi) (realspace.py:183-185)."""
     qa = np.ascontiguousarray(np.asarray(q, dtype=float))

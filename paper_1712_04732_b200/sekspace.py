@@ -226,6 +226,22 @@ def se_kspace(system: ParticleSystem, params: SEParams, periodicity: Periodicity
     return phi
 
 
+def se_kspace_field(system: ParticleSystem, params: SEParams, periodicity: Periodicity,
+                    threads: int = 1) -> np.ndarray:
+    """Fourier part of E = -grad phi at every source, (N, 3), D = 3: the
+    scaled spectrum of se_kspace times -i k per axis, three inverse
+    transforms and three gathers.  Beyond the reference (forces, SURVEY 8f
+    item 4)."""
+    if periodicity.D != 3:
+        raise ValueError("the electric field (forces) covers D = 3")
+    params.validate(system.L, periodicity)
+    plan = _native.plan_for(periodicity.D, system.L, params)
+    E = np.empty((system.N, 3))
+    _native.call("se_kspace_field_host", plan.handle, _native.ptr(system.positions),
+                 _native.ptr(system.charges), system.N, _native.ptr(E))
+    return E
+
+
 def global_upsampled_kspace(system: ParticleSystem, params: SEParams,
                             periodicity: Periodicity) -> np.ndarray:
     """Validation path with every free axis padded at s0 (sekspace.py:392-435).

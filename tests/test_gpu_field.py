@@ -146,3 +146,21 @@ def test_field_randomized_configurations():
         worst = max(worst, err)
         assert err < 1e-11, (case, N, L, M, P, window, rc, xi, err)
     print(f"randomized field cases: worst relative RMS {worst:.2e}")
+
+
+def test_field_stages_match_oracle_parts_all_periodicities():
+    # the two parts separately: real-space pair field for every D (image path
+    # included), Fourier field for D = 3; their sum is total_field
+    pos, q = _system(1500, 1.2, 64)
+    s = se.ParticleSystem(pos, q, 1.2)
+    for D in (0, 1, 2, 3):
+        for rc in (0.35, 0.7):
+            Er = se.realspace.real_space_field(s, 7.0 / rc, rc, se.Periodicity(D))
+            ref = orc.realspace_field(pos, q, 1.2, D, 7.0 / rc, rc)
+            assert _rel(Er, ref) < 1e-13, (D, rc)
+    p = se.SEParams(xi=12.0, rc=0.45, M=32, P=8, window="bm", shape=20.0, eps=1e-8)
+    Ek = se.sekspace.se_kspace_field(s, p, se.Periodicity(3))
+    assert _rel(Ek, orc.kspace_field_d3(pos, q, 1.2, _prm_dict(p))) < 1e-12
+    Et = se.total_field(s, p, se.Periodicity(3))
+    Er = se.realspace.real_space_field(s, p.xi, p.rc, se.Periodicity(3))
+    assert _rel(Et, Er + Ek) < 1e-14
