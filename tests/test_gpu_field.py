@@ -164,3 +164,15 @@ def test_field_stages_match_oracle_parts_all_periodicities():
     Et = se.total_field(s, p, se.Periodicity(3))
     Er = se.realspace.real_space_field(s, p.xi, p.rc, se.Periodicity(3))
     assert _rel(Et, Er + Ek) < 1e-14
+
+
+def test_field_empty_and_zero_charge_systems():
+    p = se.SEParams(xi=8.0, rc=0.4, M=24, P=8, window="bm", shape=20.0, eps=1e-8)
+    E = se.total_field(se.ParticleSystem(np.zeros((0, 3)), np.zeros(0), 1.0), p, se.Periodicity(3))
+    assert E.shape == (0, 3)
+    pos, _ = _system(300, 1.0, 65)
+    E0 = se.total_field(se.ParticleSystem(pos, np.zeros(300), 1.0), p, se.Periodicity(3))
+    assert E0.shape == (300, 3) and np.all(E0 == 0.0)
+    Er = se.realspace.real_space_field(se.ParticleSystem(np.zeros((0, 3)), np.zeros(0), 1.0), 8.0, 0.4,
+                                       se.Periodicity(1))
+    assert Er.shape == (0, 3)
