@@ -619,3 +619,30 @@ def test_randomized_configurations_vs_oracle(case):
         phi = se.total_potential(s, prm, se.Periodicity(D))
     ref = orc.total_potential(s.positions, s.charges, L, D, dict(prm.__dict__))
     assert se.relative_rms_error(phi, ref) < 1e-11, (D, window, P, M, L, N)
+
+
+@pytest.mark.parametrize("D", [0, 1, 2, 3])
+def test_realspace_rank_shards_sum_to_full(D):
+    # rank shards of the real-space path (contiguous ranges of the column
+    # order, Newton source sides included, only the shard's units launched):
+    # for any rank count their sum must equal the one-rank result
+    from paper_1712_04732_b200.distributed import NativeBackend
+
+    s = rand_system(120000, 4.0, 71 + D)
+    p = se.SEParams(xi=6.0, rc=0.5, M=32, P=8, window="bm", shape=20.0, eps=1e-8,
+                    R=0.0 if D == 3 else 9.0, s0=1.0 if D == 3 else 3.5)
+    dev = torch.device("cuda", 0)
+    pos = torch.from_numpy(s.positions).to(dev)
+    q = torch.from_numpy(s.charges).to(dev)
+    be = NativeBackend(s.L, p, se.Periodicity(D), dev)
+    full = be.empty_phi(len(s.charges))
+    be.realspace_shard(pos, q, 0, 1, full)
+    be.finish()
+    for world in (2, 3, 8):
+        tot = torch.zeros_like(full)
+        for r in range(world):
+            ph = be.empty_phi(len(s.charges))
+            be.realspace_shard(pos, q, r, world, ph)
+            be.finish()
+            tot += ph
+        assert se.relative_rms_error(tot.cpu().numpy(), full.cpu().numpy()) < 1e-13, (D, world)
