@@ -166,6 +166,15 @@ int se_realspace_pair_count_dev(se_plan_t plan, const double *pos, const double 
 /* Truncated-kernel geometry the plan uses for D = 0 (sekspace.py:266-279). */
 int se_plan_d0_geometry(se_plan_t plan, int32_t *nconv, int32_t *g0, double *R);
 
+/* ParticleSystem / check_neutrality validation on device arrays (core.py:65-77,
+ * 180-191): SE_EINVAL if a coordinate lies outside [0, L); with neutrality
+ * != 0 (and q non-null) also SE_EINVAL for a non-neutral periodic system
+ * (D = 0: warning bit 0, see se_plan_warnings).  The _dev stage entry points
+ * run the box check themselves; the shard entry points do so unless
+ * deferred checks are on, in which case the caller checks once per call
+ * (paper_1712_04732_b200.distributed does). */
+int se_check_system_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, int neutrality);
+
 /* sekspace.spread (sekspace.py:130-156): grid = sum_n q_n w (x) w (x) w.
  * grid_out holds prod(Grid.shape) float64 and is overwritten. */
 int se_spread_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *grid_out);

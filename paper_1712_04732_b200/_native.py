@@ -73,6 +73,7 @@ SIGNATURES = {
     "se_plan_finish": [_P],
     "se_plan_kernel_times": [_P, c_double_p, c_int64_p],
     "se_realspace_pair_count_dev": [_P, _P, _P, ctypes.c_int64, c_int64_p],
+    "se_check_system_dev": [_P, _P, _P, ctypes.c_int64, ctypes.c_int],
     "se_spread_dev": [_P, _P, _P, ctypes.c_int64, _P],
     "se_kspace_apply_dev": [_P, _P, ctypes.c_int, _P],
     "se_gather_dev": [_P, _P, _P, ctypes.c_int64, _P, ctypes.c_int],
@@ -234,15 +235,34 @@ class Plan:
             self.handle = None
 
 
-_PLANS: dict = {}
+# A plan owns mutable device buffers and a stream binding, so it is not
+# shared between host threads (one plan per host thread):
+# the cache is per thread, and bounded -- a sweep over L / xi / rc / M
+# evicts the least recently used plans (their device buffers and cuFFT
+# plans are released when the Plan object is collected).
+PLAN_CACHE_LIMIT = int(os.environ.get("SE_B200_PLAN_CACHE", "8"))
+_tls = threading.local()
+
+
+def _plan_cache():
+    c = getattr(_tls, "plans", None)
+    if c is None:
+        from collections import OrderedDict
+        c = _tls.plans = OrderedDict()
+    return c
 
 
 def plan_for(D, L, params, device: int = 0) -> Plan:
     key = (int(D), float(L), params_key(params), int(device))
-    pl = _PLANS.get(key)
+    cache = _plan_cache()
+    pl = cache.get(key)
     if pl is None:
         pl = Plan(D, L, params, device)
-        _PLANS[key] = pl
+        cache[key] = pl
+        while len(cache) > max(1, PLAN_CACHE_LIMIT):
+            cache.popitem(last=False)
+    else:
+        cache.move_to_end(key)
     return pl
 
 
@@ -252,7 +272,8 @@ def params_key(p):
 
 
 def clear_plans():
-    _PLANS.clear()
+    """Drop this thread's cached plans (device memory is freed with them)."""
+    _plan_cache().clear()
 
 
 def timings_buffer():

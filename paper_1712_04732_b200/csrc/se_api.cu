@@ -46,9 +46,11 @@ __global__ void check_kernel(const double *__restrict__ pos, const double *__res
                              double *__restrict__ out) {
     double s = 0.0, a = 0.0, bad = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-        double qi = q[i];
-        s += qi;
-        a += fabs(qi);
+        if (q) {
+            const double qi = q[i];
+            s += qi;
+            a += fabs(qi);
+        }
         for (int ax = 0; ax < 3; ++ax) {
             double x = pos[3 * i + ax];
             if (!(x >= 0.0 && x < L)) bad += 1.0;
@@ -500,10 +502,19 @@ int se_plan_warnings(se_plan_t plan, int *flags) {
     SE_API_END
 }
 
+int se_check_system_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, int neutrality) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    check_system(pl, pos, q, N, neutrality != 0 && q != nullptr);
+    SE_API_END
+}
+
 int se_spread_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *grid_out) {
     SE_API_BEGIN
     se_plan *pl = checked(plan);
     DeviceGuard dg(pl->device);
+    check_system(pl, pos, nullptr, N, false);
     spread_run(pl, pos, q, N, grid_out, 0, 1);
     SE_API_END
 }
@@ -514,6 +525,7 @@ int se_spread_shard_dev(se_plan_t plan, const double *pos, const double *q, int6
     se_plan *pl = checked(plan);
     check_shard(rank, world);
     DeviceGuard dg(pl->device);
+    if (!pl->defer) check_system(pl, pos, nullptr, N, false);
     spread_run(pl, pos, q, N, grid_out, rank, world);
     if (!pl->defer) prof_collect(pl);
     SE_API_END
@@ -566,6 +578,7 @@ int se_gather_dev(se_plan_t plan, const double *grid, const double *pos, int64_t
     SE_API_BEGIN
     se_plan *pl = checked(plan);
     DeviceGuard dg(pl->device);
+    check_system(pl, pos, nullptr, N, false);
     gather_run(pl, grid, pos, N, phi, accumulate, 0, 1, true);
     SE_API_END
 }
@@ -576,6 +589,7 @@ int se_gather_shard_dev(se_plan_t plan, const double *grid, const double *pos, i
     se_plan *pl = checked(plan);
     check_shard(rank, world);
     DeviceGuard dg(pl->device);
+    if (!pl->defer) check_system(pl, pos, nullptr, N, false);
     gather_run(pl, grid, pos, N, phi, accumulate, rank, world, true);
     if (!pl->defer) prof_collect(pl);
     SE_API_END
@@ -586,6 +600,7 @@ int se_kspace_potential_dev(se_plan_t plan, const double *pos, const double *q, 
     SE_API_BEGIN
     se_plan *pl = checked(plan);
     DeviceGuard dg(pl->device);
+    check_system(pl, pos, nullptr, N, false);
     kspace_pipeline(pl, pos, q, N, phi, use_kernel, timings, 0, 0, 1);
     SE_API_END
 }
@@ -594,6 +609,7 @@ int se_realspace_dev(se_plan_t plan, const double *pos, const double *q, int64_t
     SE_API_BEGIN
     se_plan *pl = checked(plan);
     DeviceGuard dg(pl->device);
+    check_system(pl, pos, nullptr, N, false);
     realspace_run(pl, pos, q, N, phi, add_self, 0, 1);
     check_flag(pl);
     SE_API_END
@@ -605,6 +621,7 @@ int se_realspace_shard_dev(se_plan_t plan, const double *pos, const double *q, i
     se_plan *pl = checked(plan);
     check_shard(rank, world);
     DeviceGuard dg(pl->device);
+    if (!pl->defer) check_system(pl, pos, nullptr, N, false);
     realspace_run(pl, pos, q, N, phi, add_self, rank, world);
     if (!pl->defer) {
         check_flag(pl);

@@ -254,7 +254,7 @@ void slab_inverse(se_plan *pl, int world, const double *back, double *slab);
 void plan_release_device(se_plan *pl);
 
 // binning (se_sort.cu)
-void binning_reserve(Binning &b, int64_t N, int nbins, int chunk, int extra_bits = 0);
+void binning_reserve(se_plan *pl, Binning &b, int64_t N, int nbins, int chunk, int extra_bits = 0);
 void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, int64_t N, int nbins, int chunk,
                   int extra_bits = 0, int64_t rlo = 0);
 int64_t binning_max_units(const Binning &b, int64_t N, int nbins, int chunk);

@@ -69,7 +69,10 @@ __device__ __forceinline__ unsigned column_key(const double *__restrict__ pos, i
     int c[2];
 #pragma unroll
     for (int ax = 0; ax < 2; ++ax) {
-        int ci = (int)(pos[3 * i + ax] / a.edge);
+        // clamped on both sides: the C ABI rejects coordinates outside
+        // [0, L), this only keeps an unchecked caller's keys in range
+        int ci = (int)floor(pos[3 * i + ax] / a.edge);
+        ci = ci < 0 ? 0 : ci;
         c[ax] = ci < a.n - 1 ? ci : a.n - 1;
     }
     colid = (unsigned)(c[0] * a.n + c[1]);
@@ -825,7 +828,7 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     cudaStream_t st = pl->stream;
     prof_begin(pl, SE_K_SORT);
     const int unit = real_unit(N);
-    binning_reserve(pl->cbin, N, nbins, unit, a.kb);
+    binning_reserve(pl, pl->cbin, N, nbins, unit, a.kb);
     SE_CUDA(cudaMemsetAsync(pl->cbin.counts.ptr, 0, sizeof(int) * (nbins + 1), st));
     if (nbins <= kHistSmem) {
         int64_t blocks = (N + 4095) / 4096;  // ~16 particles per thread

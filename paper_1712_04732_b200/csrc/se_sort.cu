@@ -74,7 +74,7 @@ static int bits_for(int nbins) {
     return b;
 }
 
-void binning_reserve(Binning &b, int64_t N, int nbins, int chunk, int extra_bits) {
+void binning_reserve(se_plan *pl, Binning &b, int64_t N, int nbins, int chunk, int extra_bits) {
     int64_t cap = N < 1 ? 1 : N;
     bool grow = cap > b.capacity;
     b.keys.ensure(sizeof(unsigned) * cap);
@@ -83,7 +83,8 @@ void binning_reserve(Binning &b, int64_t N, int nbins, int chunk, int extra_bits
     b.rec.ensure(sizeof(double4) * cap);
     if (grow) {
         b.idx.ensure(sizeof(int) * cap);
-        iota_kernel<<<(unsigned)((cap + 255) / 256), 256>>>(b.idx.as<int>(), cap);
+        // on the plan's stream: the sort that reads idx is ordered after it
+        iota_kernel<<<(unsigned)((cap + 255) / 256), 256, 0, pl->stream>>>(b.idx.as<int>(), cap);
         SE_LAUNCH_CHECK();
         b.capacity = cap;
     }

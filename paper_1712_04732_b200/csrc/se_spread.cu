@@ -583,7 +583,7 @@ static void bin_tiles(se_plan *pl, const double *pos, const double *q, int64_t N
     tile_setup(pl);
     TileGeom &t = pl->tile;
     int nbins = t.nt[0] * t.nt[1] * t.nt[2];
-    binning_reserve(pl->tbin, N, nbins, kUnit);
+    binning_reserve(pl, pl->tbin, N, nbins, kUnit);
     prof_begin(pl, SE_K_SORT);
     SE_CUDA(cudaMemsetAsync(pl->tbin.counts.ptr, 0, sizeof(int) * (nbins + 1), pl->stream));
     SpreadArgs a = make_args(pl);

@@ -81,6 +81,17 @@ class NativeBackend:
         _native.call(name, self.plan_k.handle, *args)
         cur.wait_stream(self.kstream)
 
+    def bind_stream(self):
+        """Order the real-space plan on the caller's current stream (the
+        orchestration's joins are against the stream current at call time)."""
+        self.plan.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def check_system(self, pos, q, neutrality=True):
+        """Box [0, L) and neutrality checks (core.py:65-77, 180-191) on the
+        device inputs, once per call (the shard entry points run deferred)."""
+        _native.call("se_check_system_dev", self.plan.handle, _native.ptr(pos), _native.ptr(q), q.shape[0],
+                     int(bool(neutrality)))
+
     def finish(self):
         """Synchronise both plans; raise a deferred device error."""
         for p in self.plans:
@@ -143,6 +154,10 @@ def total_potential_sharded(pos, q, backend, group=None, kspace: str = "replicat
     world = dist.get_world_size(group) if init else 1
     N = q.shape[0]
     multi = init and world > 1
+    if hasattr(backend, "bind_stream"):
+        backend.bind_stream()
+    if hasattr(backend, "check_system"):
+        _agreed(lambda: backend.check_system(pos, q), q, group, multi)
     # the k-space chain on the backend's side stream (if it has one),
     # concurrent with the real-space shard on the current stream; buffers
     # are allocated here, on the current stream, and the final join orders
@@ -200,24 +215,36 @@ def total_potential_sharded(pos, q, backend, group=None, kspace: str = "replicat
     return phi
 
 
+def _agreed(fn, like, group, multi):
+    """Run fn() on every rank and agree on failure: a rank whose call raised
+    re-raises its own exception, every other rank raises the same class
+    (so no rank enters the next collective alone).  Any exception counts:
+    a deferred CUDA / cuFFT error as much as SingularConfigurationError."""
+    err = None
+    try:
+        fn()
+    except Exception as e:  # noqa: BLE001 -- re-raised below on every rank
+        err = e
+    if multi:
+        code = 0.0 if err is None else (2.0 if isinstance(err, SingularConfigurationError) else
+                                        3.0 if isinstance(err, ValueError) else 1.0)
+        flag = torch.tensor([code], dtype=torch.float64, device=like.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+        c = flag.item()
+        if err is None and c > 0:
+            err = {2.0: SingularConfigurationError("coincident distinct particles (detected on another rank)"),
+                   3.0: ValueError("invalid input (detected on another rank)")}.get(
+                       c, RuntimeError("device error on another rank"))
+    if err is not None:
+        raise err
+
+
 def _finish(backend, like, group, multi):
     """Deferred device checks of this call, agreed over the ranks: a rank
     whose shard found coincident particles (realspace.py:118-122) raises
     SingularConfigurationError, and so does every other rank (instead of
     entering the next collective alone)."""
-    err = None
-    if hasattr(backend, "finish"):
-        try:
-            backend.finish()
-        except SingularConfigurationError as e:
-            err = e
-    if multi:
-        flag = torch.tensor([1.0 if err is not None else 0.0], dtype=torch.float64, device=like.device)
-        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
-        if err is None and flag.item() > 0:
-            err = SingularConfigurationError("coincident distinct particles (detected on another rank)")
-    if err is not None:
-        raise err
+    _agreed(backend.finish if hasattr(backend, "finish") else (lambda: None), like, group, multi)
 
 
 def total_potential_partitioned(pos_local, q_local, backend, group=None, kspace: str = "replicated"):

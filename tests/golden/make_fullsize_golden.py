@@ -38,7 +38,8 @@ import workloads  # noqa: E402
 from pmewald import core, realspace, sekspace  # noqa: E402
 from pmewald.core import ParticleSystem, Periodicity, SEParams  # noqa: E402
 
-SAMPLE = {"cfg1": 2000, "cfg2": 20000, "cfg3": 20000, "cfg3_tol": 20000, "cfg4": 20000}
+SAMPLE = {"cfg1": 2000, "cfg1_tol": 2000, "cfg2": 20000, "cfg2_tol": 20000, "cfg3": 20000, "cfg3_tol": 20000,
+          "cfg4": 20000, "cfg4_tol": 20000, "cfg5": 20000}
 
 
 def run(name, threads):

@@ -20,7 +20,8 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 
 pytestmark = pytest.mark.gpu
 
-CASES = [c for c in ("cfg1", "cfg3", "cfg3_tol", "cfg4", "cfg2") if os.path.exists(os.path.join(GOLD, f"full_{c}.npz"))]
+CASES = [c for c in ("cfg1", "cfg1_tol", "cfg3", "cfg3_tol", "cfg4", "cfg4_tol", "cfg5", "cfg2", "cfg2_tol")
+         if os.path.exists(os.path.join(GOLD, f"full_{c}.npz"))]
 
 
 @pytest.mark.parametrize("name", CASES)
