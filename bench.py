@@ -367,7 +367,7 @@ def measure(name, args, dev, world, rank, sharded, steps, warmup, extras=True):
 
     import paper_1712_04732_b200 as se
     from paper_1712_04732_b200 import device as sedev
-    from paper_1712_04732_b200.distributed import NativeBackend, total_potential_sharded
+    from paper_1712_04732_b200.distributed import NativeBackend, total_potential_domain, total_potential_sharded
 
     load_workload(name)
     local = dev.index
@@ -383,12 +383,20 @@ def measure(name, args, dev, world, rank, sharded, steps, warmup, extras=True):
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
+    lo, hi = N * rank // world, N * (rank + 1) // world
     if sharded:
         backend = NativeBackend(L, prm, peri, dev)
         plan = _PlanGroup(backend.plans)
+        if args.mode == "domain":
+            # particles partitioned over the ranks: rank r passes the r-th
+            # contiguous chunk of the (spatially random) input order
+            pos_r, q_r = pos_d[lo:hi].contiguous(), q_d[lo:hi].contiguous()
 
-        def step():
-            return total_potential_sharded(pos_d, q_d, backend, kspace=args.kspace)
+            def step():
+                return total_potential_domain(pos_r, q_r, backend)
+        else:
+            def step():
+                return total_potential_sharded(pos_d, q_d, backend, kspace=args.kspace)
     else:
         plan = sedev.plan(L, prm, peri, dev)
 
@@ -451,19 +459,27 @@ def measure(name, args, dev, world, rank, sharded, steps, warmup, extras=True):
                "api": "paper_1712_04732_b200.total_potential (se_total_potential_host)"}
     else:
         t_e = []
+        domain = args.mode == "domain"
+        pos_pr, q_pr = (pos_p[lo:hi].pin_memory(), q_p[lo:hi].pin_memory()) if domain else (pos_p, q_p)
         for _ in range(max(1, steps)):
             torch.cuda.synchronize(dev)
             dist.barrier()
             t0 = time.perf_counter()
-            pd = pos_p.to(dev, non_blocking=True)
-            qd = q_p.to(dev, non_blocking=True)
-            phi_h = total_potential_sharded(pd, qd, backend, kspace=args.kspace).cpu().numpy()
+            pd = pos_pr.to(dev, non_blocking=True)
+            qd = q_pr.to(dev, non_blocking=True)
+            if domain:
+                phi_h = total_potential_domain(pd, qd, backend).cpu().numpy()
+            else:
+                phi_h = total_potential_sharded(pd, qd, backend, kspace=args.kspace).cpu().numpy()
             t_e.append(time.perf_counter() - t0)
         te = torch.tensor([statistics.mean(t_e)], dtype=torch.float64, device=dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        nb = (hi - lo) if domain else N
         e2e = {"value": N / float(te.item()), "unit": "particles/s",
-               "h2d_bytes_per_step": pos_h.nbytes + q_h.nbytes, "d2h_bytes_per_step": N * 8,
-               "api": "paper_1712_04732_b200.distributed.total_potential_sharded"}
+               "h2d_bytes_per_step": 32 * nb, "d2h_bytes_per_step": 8 * nb,
+               "h2d_note": "per rank (its own particles)" if domain else "per rank (replicated inputs)",
+               "api": ("paper_1712_04732_b200.distributed.total_potential_domain" if domain else
+                       "paper_1712_04732_b200.distributed.total_potential_sharded")}
     out = {"name": name, "N": N, "ms_per_step": ms_per_step, "value": value, "e2e": e2e, "ktimes": ktimes,
            "launches": launches, "t_wall": t_wall, "clocks": clk.summary(), "pairs": pairs, "plan": plan,
            "pos_d": pos_d, "q_d": q_d, "phi_d": phi_d, "prm": prm, "peri": peri, "phi_h": phi_h}
@@ -582,10 +598,15 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.md 3.1; no public dataset exists for this path)",
             "config": {"workload": DESCR[CFG["workload"]], "N": N, "seed": CFG["seed"],
-                       "parallelism": (f"particle-shard x{world} (grid + phi sum-all-reduce)"
-                                       if args.kspace == "replicated" or world == 1 else
-                                       f"particle-shard x{world}, slab k-space (grid reduce-scatter, "
-                                       "2 all-to-all, all-gather; phi sum-all-reduce)"),
+                       "parallelism": ("single GPU (fused pipeline, CUDA graph)" if world == 1 and not
+                                       ("RANK" in os.environ) else
+                                       (f"domain decomposition x{world}: particles partitioned (contiguous "
+                                        "chunks of the random input order), migrated to x-slabs of "
+                                        "real-space columns, +x halo with Newton sums returned, touched "
+                                        "grid planes to the k-space slab owners, slab FFT with two "
+                                        "all-to-all transposes (D = 3)" if args.mode == "domain" else
+                                        f"particle-shard x{world} with replicated inputs, {args.kspace} "
+                                        "k-space")),
                        "l2": "flushed (256 MB write) between timed steps, outside the step events"},
             "e2e": m["e2e"], "roofline": roofline, "kernels": kern,
             "spread_gather": spread_gather,
@@ -657,6 +678,9 @@ def main():
     ap.add_argument("--kspace", choices=("replicated", "slab"), default="replicated",
                     help="multi-GPU k-space stage (torchrun): replicated after a grid all-reduce, or "
                          "slab-decomposed (D = 3)")
+    ap.add_argument("--mode", choices=("domain", "sharded"), default="domain",
+                    help="multi-GPU decomposition (torchrun): domain (partitioned particles) or sharded "
+                         "(replicated inputs)")
     ap.add_argument("--workload", default="cfg2", choices=sorted(workloads.ALL),
                     help="BASELINE config (default cfg2 = configs[1], the headline)")
     args = ap.parse_args()

@@ -211,6 +211,23 @@ int se_gather_shard_dev(se_plan_t plan, const double *grid, const double *pos, i
 int se_realspace_shard_dev(se_plan_t plan, const double *pos, const double *q, int64_t N,
                            int rank, int world, double *phi, int add_self);
 
+/* Domain-decomposed real space (particles partitioned over ranks by x-slabs
+ * of columns; paper_1712_04732_b200.distributed.total_potential_domain).
+ * The column grid is ncols x ncols columns in (x, y) of edge L / ncols >=
+ * rc / 3, identical on every rank; this rank owns the columns with
+ * cx in [col_lo, col_hi).  The local set is pos/q[0, n_own) = the own
+ * particles (exactly those in the own columns, column index floor(x / edge)
+ * clamped to [0, ncols - 1]) followed by pos/q[n_own, n_local) = the halo:
+ * every particle of the ceil(rc ncols / L) columns beyond col_hi (+x side,
+ * wrapping on a periodic x).  Each unordered in-cutoff pair with an own end
+ * is evaluated once over all ranks (half shell towards +x, Newton's third
+ * law).  phi[0, n_own) = the real-space potentials of the own particles
+ * (+ self term if add_self), phi[n_own, n_local) = the source-side partial
+ * sums of the halo particles, which the caller returns to their owners.
+ * Needs rc <= L / 2 and >= 2 reach + 1 columns per periodic axis. */
+int se_realspace_domain_dev(se_plan_t plan, const double *pos, const double *q, int64_t n_local, int64_t n_own,
+                            int ncols, int col_lo, int col_hi, double *phi, int add_self);
+
 /* Electric field E = -grad phi at every particle, D = 3 (forces F = q E; the
  * reference stops at potentials: SPEC.md:16 notes the force integration "has
  * to be performed three times").  E is (N, 3) in caller

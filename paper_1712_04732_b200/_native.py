@@ -80,6 +80,8 @@ SIGNATURES = {
     "se_kspace_potential_dev": [_P, _P, _P, ctypes.c_int64, _P, ctypes.c_int, _P],
     "se_realspace_dev": [_P, _P, _P, ctypes.c_int64, _P, ctypes.c_int],
     "se_total_potential_dev": [_P, _P, _P, ctypes.c_int64, _P, _P],
+    "se_realspace_domain_dev": [_P, _P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                _P, ctypes.c_int],
     "se_spread_shard_dev": [_P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P],
     "se_total_field_dev": [_P, _P, _P, ctypes.c_int64, _P],
     "se_total_field_host": [_P, _P, _P, ctypes.c_int64, _P],

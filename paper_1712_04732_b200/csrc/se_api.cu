@@ -630,6 +630,20 @@ int se_realspace_shard_dev(se_plan_t plan, const double *pos, const double *q, i
     SE_API_END
 }
 
+int se_realspace_domain_dev(se_plan_t plan, const double *pos, const double *q, int64_t n_local, int64_t n_own,
+                            int ncols, int col_lo, int col_hi, double *phi, int add_self) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    if (!pl->defer) check_system(pl, pos, nullptr, n_local, false);
+    realspace_domain_run(pl, pos, q, n_local, n_own, ncols, col_lo, col_hi, phi, add_self);
+    if (!pl->defer) {
+        check_flag(pl);
+        prof_collect(pl);
+    }
+    SE_API_END
+}
+
 int se_total_potential_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *phi,
                            double *timings) {
     SE_API_BEGIN

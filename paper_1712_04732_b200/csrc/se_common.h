@@ -123,6 +123,15 @@ struct CellGeom {
     int mode[3];  // 0: free (clip), 1: periodic wrap +-2, 2: periodic, all cells + min image
 };
 
+// Domain-decomposed real space (se_realspace_domain_dev): the column grid
+// is fixed by the caller (the same on every rank), targets are the
+// particles of the columns with cx in [col_lo, col_hi), the rest of the
+// local set is +x halo (sources only); ncols = 0: the usual single-set sum.
+struct DomainSpec {
+    int ncols = 0, col_lo = 0, col_hi = 0;
+    int64_t n_own = -1;  // caller-order particles [0, n_own) are the own ones
+};
+
 struct se_plan_impl;
 
 }  // namespace se
@@ -142,6 +151,7 @@ struct se_plan {
     se::Binning tbin;  // tile binning for spread / gather
     // real space
     se::CellGeom cell{};
+    se::DomainSpec dom{};
     se::Binning cbin;  // cell binning for the real-space sum
     se::DevBuf flag;   // device error flags (int)
 
@@ -243,6 +253,8 @@ void gather_run(se_plan *pl, const double *grid, const double *pos, int64_t N, d
 void kspace_run(se_plan *pl, double *grid, int use_kernel, double *timings);
 void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi,
                    int add_self, int rank, int world);
+void realspace_domain_run(se_plan *pl, const double *pos, const double *q, int64_t n_local, int64_t n_own, int ncols,
+                          int col_lo, int col_hi, double *phi, int add_self);
 void realspace_field_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *E,
                          int rank, int world);
 void d0_kernel_prepare(se_plan *pl, double *t_precompute);
@@ -256,7 +268,7 @@ void plan_release_device(se_plan *pl);
 // binning (se_sort.cu)
 void binning_reserve(se_plan *pl, Binning &b, int64_t N, int nbins, int chunk, int extra_bits = 0);
 void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, int64_t N, int nbins, int chunk,
-                  int extra_bits = 0, int64_t rlo = 0);
+                  int extra_bits = 0, int64_t rlo = 0, int ubin_lo = 0, int ubin_hi = -1);
 int64_t binning_max_units(const Binning &b, int64_t N, int nbins, int chunk);
 
 // shared device helpers ---------------------------------------------------

@@ -42,6 +42,9 @@ struct RealArgs {
     double qinv;      // z quantum^-1 = 2^kb / L: Q(z) = floor(z qinv), monotone along a column
     int zper;         // z periodic (D = 3)
     int reach;        // neighbour columns within +-reach (column edge >= rc / reach)
+    int dense_min;    // prefilter hits per full batch (of kT x 32) from which the batch is
+                      // evaluated densely (all pairs, no compaction); > kT * 32: never
+    int64_t n_own;    // domain mode: caller-order particles [0, n_own) get the self term; -1: off
 };
 
 constexpr double kTwoOverSqrtPi = 1.1283791670955126;  // field mode: c = 2 xi / sqrt(pi)
@@ -116,9 +119,9 @@ __global__ void cell_keys_hist_kernel(const double *__restrict__ pos, int64_t N,
 __constant__ double se_erfc_k[6] = {
     SE_ERFC_A + SE_ERFC_B,                // s = ((A+B) x + K (B-A)) / (x + K)
     SE_ERFC_K * (SE_ERFC_B - SE_ERFC_A),  //   (K = 4: an immediate)
-    -SE_LOG2E,                            // n = rint(-x^2 log2 e)
-    -SE_LN2_HI,                           // r = -x^2 - n ln2 (Cody-Waite)
-    -SE_LN2_LO,
+    -SE_LOG2E,                            // n = rint(-x^2 log2 e) by the 1.5 2^52 shifter
+    -SE_LN2_HI,                           // r = -x^2 - n ln2 (one rounded ln2, see exp_neg)
+    6755399441055744.0,                   // 1.5 2^52
     0.375};                               // rsqrt_nr: a 64-bit constant operand, not
                                           //   two IMAD.MOVs per use
 
@@ -138,14 +141,38 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
     return fma(y, e * fma(e, se_erfc_k[5], 0.5), y);
 }
 
+// exp(-u) for 0 <= u <= ~40 as e 2^n: returns the reduced factor e in
+// [2^-1/2, 2^1/2] and n (<= 0).  n = rint(-u log2 e) by the 1.5 2^52
+// shifter (one DFMA and one DADD; n is the low word -- no FRND / F2I), and
+// r = -u - n ln2 with ONE rounded ln2 (one DFMA instead of the two of a
+// Cody-Waite split): the ln2 rounding moves r by |n| 2^-53 ln2, a relative
+// error of exp(-u) of at most 1.1e-16 u, i.e. an absolute error of
+// erfc(x) = exp(-u) erfcx(x) below 1.1e-16 u erfc(sqrt u) <= 1.7e-17 --
+// under the erfcx fit's own 7.6e-17.
+__device__ __forceinline__ double exp_neg(double u, int &n) {
+    const double t = fma(u, se_erfc_k[2], se_erfc_k[4]);
+    n = __double2loint(t);
+    const double nf = t - se_erfc_k[4];
+    const double r = fma(nf, se_erfc_k[3], -u);
+    double e = se_exp_c[SE_EXP_NX];
+#pragma unroll
+    for (int i = SE_EXP_NX - 1; i >= 2; --i) e = fma(e, r, se_exp_c[i]);
+    return fma(fma(e, r, SE_EXP_C1), r, SE_EXP_C0);  // literals (1.0): no constant-bank operands
+}
+
+// e 2^n by an exponent add (n in [-60, 0] and e ~ 1: e 2^n stays normal)
+__device__ __forceinline__ double scale2(double e, int n) {
+    return __hiloint2double(__double2hiint(e) + n * (1 << 20), __double2loint(e));
+}
+
 // erfc(x), x >= 0, as exp(-x^2) erfcx(x): erfcx by a degree-14 polynomial in
-// s = A t + B, t = (x - K)/(x + K), and exp by Cody-Waite reduction;
-// coefficients are __constant__ operands (tools/gen_erfc_coeffs.py: fitted
-// for absolute accuracy, max error 7.6e-17 absolute / 7.6e-10 relative on
-// [0, 6] -- the pair term's 1/r rounding is ~1e-16 relative).  The x^2 rounding
-// residual is not carried: it moves exp(-x^2) by <= x^2 2^-53 relative,
-// i.e. <= 4e-17 absolute, below the 1/r rounding of the pair term.
-// Beyond SE_ERFC_XMAX the library erfc is used.
+// s = A t + B, t = (x - K)/(x + K), and exp by exp_neg; coefficients are
+// __constant__ operands (tools/gen_erfc_coeffs.py: fitted for absolute
+// accuracy, max error 7.6e-17 absolute / 7.6e-10 relative on [0, 6] -- the
+// pair term's 1/r rounding is ~1e-16 relative).  The x^2 rounding residual
+// is not carried: it moves exp(-x^2) by <= x^2 2^-53 relative, i.e. <= 4e-17
+// absolute, below the 1/r rounding of the pair term.  Beyond SE_ERFC_XMAX
+// the library erfc is used.
 //
 // erfc(x) * w.  WIDE: x may exceed SE_ERFC_XMAX (xi rc > 6, i.e. eps < 2e-16).
 // Otherwise the caller guarantees x <= SE_ERFC_XMAX (1 + 1e-4) for every
@@ -163,16 +190,9 @@ __device__ __forceinline__ double erfc_fast(double x, double w) {
     double p = se_erfcx_c[SE_ERFC_NE];
 #pragma unroll
     for (int i = SE_ERFC_NE - 1; i >= 0; --i) p = fma(p, s, se_erfcx_c[i]);
-    const double u = x * x;
-    const double n = rint(u * se_erfc_k[2]);
-    const double r = fma(n, se_erfc_k[4], fma(n, se_erfc_k[3], -u));
-    double e = se_exp_c[SE_EXP_NX];
-#pragma unroll
-    for (int i = SE_EXP_NX - 1; i >= 2; --i) e = fma(e, r, se_exp_c[i]);
-    e = fma(fma(e, r, SE_EXP_C1), r, SE_EXP_C0);  // literals (1.0): no constant-bank operands
-    // e * 2^n by an exponent add (n in [-27, 0]: e 2^n stays normal)
-    e = __hiloint2double(__double2hiint(e) + (int)n * (1 << 20), __double2loint(e));
-    return p * (e * w);
+    int n;
+    const double e = exp_neg(x * x, n);
+    return p * (scale2(e, n) * w);
 }
 
 // Field mode: the two factors separately, erfcx(x) (as p) and exp(-x^2) (as
@@ -190,14 +210,8 @@ __device__ __forceinline__ void erfc_parts(double x, double &p, double &e) {
     p = se_erfcx_c[SE_ERFC_NE];
 #pragma unroll
     for (int i = SE_ERFC_NE - 1; i >= 0; --i) p = fma(p, s, se_erfcx_c[i]);
-    const double u = x * x;
-    const double n = rint(u * se_erfc_k[2]);
-    const double r = fma(n, se_erfc_k[4], fma(n, se_erfc_k[3], -u));
-    e = se_exp_c[SE_EXP_NX];
-#pragma unroll
-    for (int i = SE_EXP_NX - 1; i >= 2; --i) e = fma(e, r, se_exp_c[i]);
-    e = fma(fma(e, r, SE_EXP_C1), r, SE_EXP_C0);
-    e = __hiloint2double(__double2hiint(e) + (int)n * (1 << 20), __double2loint(e));
+    int n;
+    e = scale2(exp_neg(x * x, n), n);
 }
 
 __device__ __forceinline__ double min_image(double d, double L) { return d - L * rint(d / L); }
@@ -207,6 +221,7 @@ constexpr int kWarps = 1;  // warps (units) per block: one, so that the WarpBuf 
                            // block-uniform (shared addresses fold into [R + UR + imm])
 constexpr int kMinBlocks = 27;  // 27 x (7 KB + 1 KB reserved) of shared memory per SM
 constexpr int kT = 16;     // targets per warp unit: lane l tests target l % 16 against half of a 32-source batch
+constexpr int kDenseMin = 410;  // ~0.8 kT x 32: dense evaluation of a batch from this many prefilter hits
 
 // Shared-memory workspace of one warp unit (7 KB; 15 KB in field mode, FLD:
 // three accumulator components).
@@ -371,8 +386,50 @@ __device__ __forceinline__ unsigned long long f2add(unsigned long long a, float 
 // absolute fp32 positions.  An absent target never passes.
 struct PreTargets {
     unsigned long long x, y, z, w;
-    int ta, tb;  // unit-relative target slots (pa, pa + 8)
+    int ta, tb;       // unit-relative target slots (pa, pa + 8)
+    unsigned amask;   // bit t: unit target t is active (bits 16..31 repeat 0..15)
 };
+
+// Dense evaluation of a batch whose prefilter hit nearly every (target,
+// source) slot (most batches in the middle of a column window): no
+// compaction.  Lane l keeps source l of the batch in registers (staged by
+// itself) and, in step s = 0..kT-1, pairs it with unit target (l + s) mod kT
+// -- every (target, source) slot exactly once, the 32 lanes of a step on 32
+// different sources and kT targets (two lanes per target, different
+// acc columns).  The target side goes to the lane-owned slot acc[t][l]; the
+// source side accumulates in a register and leaves with ONE REDG per source
+// and batch (instead of one per pair).  Pairs outside the cutoff, excluded
+// own-column pairs (j <= t), inactive targets and lanes past the run's end
+// are evaluated at r = rc and multiplied by 0.  Newton (half-shell) path only.
+template <bool WIDE, class WB>
+__device__ __forceinline__ void dense_batch(WB &wb, int lane, int j, int m, double xs, double ys, double zs, double qs,
+                                            const RealArgs &a, unsigned amask, int tbase, int hs,
+                                            double *__restrict__ acc_s, int &singular) {
+    const bool sval = lane < m;
+    double accs = 0.0;
+#pragma unroll 2
+    for (int st = 0; st < kT; ++st) {
+        const int tu = (lane + st) & (kT - 1);
+        const int sl = tslot(tu);
+        const double2 t01 = wb.txy[sl], t23 = wb.tzq[sl];
+        const bool v = sval && ((amask >> tu) & 1u) && (hs < 0 || j > tbase + tu);
+        const double dx = t01.x - xs, dy = t01.y - ys, dz = t23.x - zs;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        const bool zero = r2 < 1e-28;
+        singular |= (v && zero) ? 1 : 0;
+        const bool in = v && r2 < a.rc2 && !zero;  // a.rc2 = rc^2 (1 + 1e-12): never drops a pair
+        const double r2s = in ? r2 : a.rc2;        // a safe argument for every other slot
+        const double rinv = rsqrt_nr(r2s);
+        const double rr = r2s * rinv;
+        const double w = (in && rr < a.rc) ? rinv : 0.0;
+        const double f = erfc_fast<WIDE>(a.xi * rr, w);
+        double *slot = &wb.acc[0][sl][lane];
+        *slot = fma(qs, f, *slot);
+        accs = fma(t23.y, f, accs);
+    }
+    if (sval) atomicAdd(acc_s + lane, accs);
+    __syncwarp();
+}
 
 // One batch of <= 32 candidate sources [jb, jb+m) of a neighbour-cell run:
 //  1. fp32 prefilter of all 16 x m (target, source) pairs: lane l tests
@@ -390,10 +447,16 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
                                            const PreTargets &pt, const double3 org, int tbase, int hs,
                                            double *__restrict__ acc_src, int &singular, long long &cnt) {
     const int j = jb + lane;
+    // the lane's own source stays in registers for the dense path (zero
+    // past the end of the run: finite, never evaluated)
+    double xs = 0.0, ys = 0.0, zs = 0.0, qs = 0.0;
     if (j < j1) {
         const double4 r = rec[j];
         if (j + 32 < j1) prefetch_l1(rec + j + 32);  // the run's next batch
-        const double xs = r.x + shx, ys = r.y + shy, zs = r.z + shz;
+        xs = r.x + shx;
+        ys = r.y + shy;
+        zs = r.z + shz;
+        qs = r.w;
         wb.sxy[lane] = make_double2(xs, ys);
         wb.szq[lane] = make_double2(zs, r.w);
         if (MI) {
@@ -456,6 +519,10 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
         hit &= ~(spread(excl(tbase + pt.ta)) | (spread(excl(tbase + pt.tb)) << 1));
     }
     const int c = __popc(hit);
+    if (!COUNT && !FLD && NEWTON && __reduce_add_sync(0xffffffffu, (unsigned)c) >= (unsigned)a.dense_min) {
+        dense_batch<WIDE>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, hs, acc_src + jb, singular);
+        return;
+    }
     const int incl = warp_incl_scan(c, lane);
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     int pos = incl - c;
@@ -564,6 +631,7 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
         const double Rt = 1.4143 * a.edge + (zmax - zmin), Rs = Rt + 1.01 * a.rc;
         const float bound = (float)(a.rc2 + 4e-7 * (Rt + Rs) * (Rt + Rs));
         const unsigned amask = __ballot_sync(0xffffffffu, active);
+        pt.amask = amask;
         pt.ta = lane & 7;
         pt.tb = pt.ta + 8;
         float v[2][4];
@@ -722,8 +790,9 @@ __global__ void realspace_finish_kernel(const double *__restrict__ acc, const do
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= N) return;
     double v = acc[i];
-    if (a.add_self && i >= a.rlo && i < a.rhi) v += (-2.0 * a.xi * rec[i].w) / a.sqrtpi;
-    phi[sidx[i]] = v;
+    const int o = sidx[i];
+    if (a.add_self && (a.n_own >= 0 ? o < a.n_own : (i >= a.rlo && i < a.rhi))) v += (-2.0 * a.xi * rec[i].w) / a.sqrtpi;
+    phi[o] = v;
 }
 
 // rc > L/2 with periodic axes: explicit images (realspace.py:138-165)
@@ -780,6 +849,16 @@ __global__ void realspace_image_kernel(const double *__restrict__ pos, const dou
     phi[t] = v;
 }
 
+// Prefilter hits (of kT x 32 slots) from which a batch is evaluated densely
+// (dense_batch).  SE_B200_DENSE_MIN overrides it (A/B runs; > 512 disables).
+static int dense_threshold() {
+    static const int v = [] {
+        const char *e = std::getenv("SE_B200_DENSE_MIN");
+        return e ? std::atoi(e) : kDenseMin;
+    }();
+    return v;
+}
+
 // targets per work unit: kT, or half of it for small systems (latency bound:
 // more, shorter units keep more warps in flight)
 // (by the total particle count: for a shard of a large system the 16-target
@@ -795,11 +874,20 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     // columns (cx, cy) of edge >= rc/reach in x, y; z is not binned but sorted
     int reach = kReachMax;
     long long nn = 1;
-    for (;; --reach) {
-        nn = (long long)std::floor(reach * L / rc);
-        if (nn < 1) nn = 1;
-        if (nn > 1024) nn = 1024;
-        if (reach == 2 || (double)N / ((double)nn * nn) >= kShortColumn) break;
+    if (pl->dom.ncols > 0) {
+        // domain mode: the caller's column grid (identical on every rank)
+        nn = pl->dom.ncols;
+        reach = (int)std::ceil(rc * (double)nn / L - 1e-12);
+        if (reach < 1) reach = 1;
+        if (reach > kReachMax || nn > 1024)
+            fail(SE_EINVAL, "domain column grid: columns must be at least rc / 3 wide and at most 1024 per axis");
+    } else {
+        for (;; --reach) {
+            nn = (long long)std::floor(reach * L / rc);
+            if (nn < 1) nn = 1;
+            if (nn > 1024) nn = 1024;
+            if (reach == 2 || (double)N / ((double)nn * nn) >= kShortColumn) break;
+        }
     }
     a.reach = reach;
     c.n = (int)nn;
@@ -808,6 +896,8 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     // else all columns with the minimum image (then z too, if periodic)
     for (int ax = 0; ax < 2; ++ax) c.mode[ax] = ax < pl->D ? (c.n >= 2 * reach + 1 ? 1 : 2) : 0;
     const bool mi = c.mode[0] == 2 || c.mode[1] == 2;
+    if (pl->dom.ncols > 0 && mi)
+        fail(SE_EINVAL, "domain mode needs at least 2 reach + 1 columns per periodic axis (no minimum-image mode)");
     c.mode[2] = pl->D == 3 ? (mi ? 2 : 1) : 0;
     a.n = c.n;
     a.edge = c.edge;
@@ -841,7 +931,10 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     }
     SE_LAUNCH_CHECK();
     pl->launches += 1;
-    binning_sort(pl, pl->cbin, pos, q, N, nbins, unit, a.kb, a.rlo);
+    if (pl->dom.ncols > 0)  // units (targets) only in the own columns cx in [col_lo, col_hi)
+        binning_sort(pl, pl->cbin, pos, q, N, nbins, unit, a.kb, -1, pl->dom.col_lo * c.n, pl->dom.col_hi * c.n);
+    else
+        binning_sort(pl, pl->cbin, pos, q, N, nbins, unit, a.kb, a.rlo);
     prof_end(pl, SE_K_SORT);
 }
 
@@ -913,6 +1006,8 @@ static void realspace_impl(se_plan *pl, const double *pos, const double *q, int6
     a.xi = xi;
     a.rc = rc;
     a.rc2 = rc * rc * (1.0 + 1e-12);  // prefilter only; the exact test is r < rc
+    a.dense_min = dense_threshold();
+    a.n_own = pl->dom.ncols > 0 ? pl->dom.n_own : -1;
     a.add_self = add_self;
     a.sqrtpi = std::sqrt(M_PI);
     a.rlo = N * rank / world;
@@ -937,6 +1032,29 @@ void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, d
     realspace_impl<false>(pl, pos, q, N, phi, add_self, rank, world);
 }
 
+// Domain-decomposed real space: the local set = own particles (caller order
+// [0, n_own), all in the columns cx in [col_lo, col_hi) of the ncols x ncols
+// column grid) + halo particles (the columns up to `reach` beyond col_hi,
+// +x side, periodic wrap on a periodic x).  Every unordered pair with one
+// end in the own columns is evaluated once here or on the rank owning the
+// other end (the half shell points to +x): phi[own] = the pair sums of the
+// own particles (+ self term), phi[halo] = the Newton source-side sums of
+// the halo particles, to be returned to their owners and added there.
+void realspace_domain_run(se_plan *pl, const double *pos, const double *q, int64_t n_local, int64_t n_own, int ncols,
+                          int col_lo, int col_hi, double *phi, int add_self) {
+    if (pl->D >= 1 && pl->p.rc > pl->L / 2 + 1e-12) fail(SE_EINVAL, "domain mode covers the cell path (rc <= L/2)");
+    if (ncols < 1 || col_lo < 0 || col_hi > ncols || col_lo > col_hi || n_own < 0 || n_own > n_local)
+        fail(SE_EINVAL, "invalid domain (ncols, col_lo, col_hi, n_own)");
+    pl->dom = DomainSpec{ncols, col_lo, col_hi, n_own};
+    try {
+        realspace_impl<false>(pl, pos, q, n_local, phi, add_self, 0, 1);
+    } catch (...) {
+        pl->dom = DomainSpec{};
+        throw;
+    }
+    pl->dom = DomainSpec{};
+}
+
 // Real-space part of the electric field E_R = -grad phi_R at every particle
 // (N x 3, caller order): sum over in-cutoff pairs of
 // q_s (erfc(xi r)/r + (2 xi/sqrt(pi)) exp(-xi^2 r^2)) (x_t - x_s) / r^2,
@@ -956,6 +1074,8 @@ void realspace_pair_count(se_plan *pl, const double *pos, const double *q, int64
     a.xi = pl->p.xi;
     a.rc = rc;
     a.rc2 = rc * rc * (1.0 + 1e-12);
+    a.dense_min = kT * 32 + 1;  // counting: the compaction path counts exactly
+    a.n_own = -1;
     a.sqrtpi = std::sqrt(M_PI);
     a.rlo = 0;
     a.rhi = N;

@@ -30,9 +30,11 @@ __global__ void gather_records_kernel(const double *__restrict__ pos, const doub
 // with a serial per-thread pass is a few microseconds.
 // nunits[0] = number of units; nunits[1] = the unit holding sorted position
 // rlo (the first unit of a rank's shard; the unit count if rlo >= N).
+// Units are emitted only for bins in [ulo, uhi) (all bins: [0, nbins)); a
+// restricted list starts at unit 0 (nunits[1] = 0).
 __global__ void __launch_bounds__(1024) build_units_kernel(const int *__restrict__ counts, int nbins, int chunk,
                                                            int *__restrict__ starts, int4 *__restrict__ units,
-                                                           int *__restrict__ nunits, int64_t rlo) {
+                                                           int *__restrict__ nunits, int64_t rlo, int ulo, int uhi) {
     typedef cub::BlockScan<long long, 1024> Scan;
     __shared__ typename Scan::TempStorage tmp;
     const int per = (nbins + 1023) / 1024;
@@ -41,7 +43,7 @@ __global__ void __launch_bounds__(1024) build_units_kernel(const int *__restrict
     for (int b = b0; b < b1; ++b) {
         int c = counts[b];
         cs += c;
-        us += (c + chunk - 1) / chunk;
+        if (b >= ulo && b < uhi) us += (c + chunk - 1) / chunk;
     }
     // pack (count prefix, unit prefix) into one 64-bit scan: counts < 2^31, units < 2^31
     long long packed = (cs << 32) | us, excl;
@@ -50,6 +52,10 @@ __global__ void __launch_bounds__(1024) build_units_kernel(const int *__restrict
     for (int b = b0; b < b1; ++b) {
         int c = counts[b];
         starts[b] = (int)cpos;
+        if (b < ulo || b >= uhi) {
+            cpos += c;
+            continue;
+        }
         for (int s = 0; s < c; s += chunk) {
             const int len = min(chunk, c - s);
             if (rlo >= cpos + s && rlo < cpos + s + len) nunits[1] = (int)upos;
@@ -61,6 +67,7 @@ __global__ void __launch_bounds__(1024) build_units_kernel(const int *__restrict
         starts[nbins] = (int)cpos;
         *nunits = (int)upos;
         if (rlo >= cpos) nunits[1] = (int)upos;
+        if (ulo > 0 || uhi < nbins) nunits[1] = 0;
     }
 }
 
@@ -103,7 +110,8 @@ void binning_reserve(se_plan *pl, Binning &b, int64_t N, int nbins, int chunk, i
 
 // Keys must already be in b.keys and the histogram in b.counts.
 void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, int64_t N, int nbins, int chunk,
-                  int extra_bits, int64_t rlo) {
+                  int extra_bits, int64_t rlo, int ubin_lo, int ubin_hi) {
+    if (ubin_hi < 0) ubin_hi = nbins;
     cudaStream_t st = pl->stream;
     if (N > 0) {
         size_t bytes = b.cub_bytes;
@@ -117,7 +125,7 @@ void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, i
         pl->launches += 1;
     }
     build_units_kernel<<<1, 1024, 0, st>>>(b.counts.as<int>(), nbins, chunk, b.starts.as<int>(),
-                                           b.units.as<int4>(), b.nunits.as<int>(), rlo);
+                                           b.units.as<int4>(), b.nunits.as<int>(), rlo, ubin_lo, ubin_hi);
     SE_LAUNCH_CHECK();
     pl->launches += 1;
 }

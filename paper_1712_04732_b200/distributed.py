@@ -34,6 +34,7 @@ from __future__ import annotations
 
 import contextlib
 import ctypes
+import math
 
 import torch
 import torch.distributed as dist
@@ -118,6 +119,25 @@ class NativeBackend:
     def gather_shard(self, grid, pos, rank, world, phi, accumulate=True):
         self._k("se_gather_shard_dev", _native.ptr(grid), _native.ptr(pos), pos.shape[0],
                      rank, world, _native.ptr(phi), int(bool(accumulate)))
+
+    # domain decomposition (total_potential_domain)
+    def domain_partition(self, world, n_total):
+        return DomainPartition(self.L, self.params, self.peri, world, n_total, self.shape)
+
+    def grid_geometry(self):
+        g = self.plan.grid()
+        return {"M": int(g.M), "P": int(g.P), "h": float(g.h), "shape": tuple(g.shape)}
+
+    def spread_all(self, pos, q, grid):
+        self._k("se_spread_shard_dev", _native.ptr(pos), _native.ptr(q), q.shape[0], 0, 1, _native.ptr(grid))
+
+    def gather_all(self, grid, pos, phi, accumulate=False):
+        self._k("se_gather_shard_dev", _native.ptr(grid), _native.ptr(pos), pos.shape[0], 0, 1, _native.ptr(phi),
+                int(bool(accumulate)))
+
+    def realspace_domain(self, pos, q, n_own, part, rank, phi):
+        _native.call("se_realspace_domain_dev", self.plan.handle, _native.ptr(pos), _native.ptr(q), q.shape[0],
+                     int(n_own), part.ncols, part.col_lo[rank], part.col_hi[rank], _native.ptr(phi), 1)
 
     # slab-decomposed k-space stage (D = 3)
     def slab_geometry(self, world):
@@ -285,3 +305,290 @@ def total_potential_partitioned(pos_local, q_local, backend, group=None, kspace:
 def shard_bounds(N: int, rank: int, world: int) -> tuple[int, int]:
     """Owned range [lo, hi) of a sorted order (same rule as the C ABI)."""
     return N * rank // world, N * (rank + 1) // world
+
+
+# --------------------------------------------------------------------------
+# Domain decomposition: particles partitioned over the ranks (SURVEY 8e)
+# --------------------------------------------------------------------------
+
+class DomainPartition:
+    """x-slabs of whole real-space columns, the same on every rank.
+
+    The real-space column grid is ncols x ncols columns of edge L / ncols >=
+    rc / reach in (x, y) (the kernel's rule: reach 3, or 2 when columns would
+    hold < 256 particles of the whole system); rank r owns the columns
+    cx in [col_lo[r], col_hi[r]) and every particle in them -- for real
+    space (targets), spreading and gathering alike.  Its real-space halo is
+    the `reach` columns beyond col_hi (+x side, wrapping on a periodic x):
+    the half shell of the column kernel points to +x, so each unordered pair
+    is evaluated by exactly one rank and the halo particles' Newton partial
+    sums travel back to their owners.
+
+    The k-space grid's x-planes are owned in equal slabs of M / world planes
+    (D = 3); a rank's particles touch the planes of their stencils, a ring
+    interval of x-planes (touched_planes), which is all a rank sends to and
+    receives from the slab owners.
+    """
+
+    def __init__(self, L, params, periodicity, world, n_total, grid_shape=None):
+        L, rc = float(L), float(params.rc)
+        D = periodicity.D
+        if D >= 1 and rc > L / 2 + 1e-12:
+            raise ValueError("domain decomposition covers the cell path (rc <= L/2); use total_potential_sharded")
+        reach = 3
+        while True:
+            n = int(min(1024, max(1, math.floor(reach * L / rc))))
+            if reach == 2 or n_total / (n * n) >= 256.0:
+                break
+            reach -= 1
+        # the column kernel's reach for this grid (se_realspace.cu cell_bin)
+        reach = max(1, int(math.ceil(rc * n / L - 1e-12)))
+        if D >= 1 and n < 2 * reach + 1:
+            raise ValueError(f"{n} columns per periodic axis are too few for a domain decomposition "
+                             f"(need >= {2 * reach + 1}); use total_potential_sharded")
+        if n < world:
+            raise ValueError(f"{world} ranks for {n} real-space columns; use total_potential_sharded")
+        self.L, self.D, self.rc, self.ncols, self.reach, self.world = L, D, rc, n, reach, world
+        self.edge = L / n
+        self.periodic_x = D >= 1
+        self.col_lo = [n * r // world for r in range(world)]
+        self.col_hi = [n * (r + 1) // world for r in range(world)]
+        owner = []
+        for r in range(world):
+            owner += [r] * (self.col_hi[r] - self.col_lo[r])
+        self.owner_of_col = owner
+        # halo_to[c][d]: column c is in rank d's +x halo
+        self.halo_to = [[self._in_halo(c, d) for d in range(world)] for c in range(n)]
+        self.grid_shape = tuple(grid_shape) if grid_shape is not None else None
+        self.params = params
+
+    def _in_halo(self, c, d):
+        if self.owner_of_col[c] == d:
+            return False
+        off = c - self.col_hi[d]
+        if self.periodic_x:
+            off %= self.ncols
+        return 0 <= off < self.reach
+
+    def columns(self, x):
+        """Column index cx of each x (the kernel's floor(x / edge), clamped)."""
+        return torch.clamp(torch.floor(x / self.edge), 0, self.ncols - 1).to(torch.int64)
+
+    # k-space plane bookkeeping (D = 3 slab mode) -------------------------
+    def slab(self, r, M):
+        nx = M // self.world
+        return r * nx, (r + 1) * nx
+
+    def touched_planes(self, r, M, P, h):
+        """Ring interval (start, count) of x-planes the stencils of rank r's
+        particles can touch: first index floor(x / h - P / 2) + 1 over
+        x in [col_lo edge, col_hi edge), P planes each, one plane of margin
+        on both sides for the rounding of x / h."""
+        if self.col_hi[r] <= self.col_lo[r]:
+            return 0, 0
+        xa, xb = self.col_lo[r] * self.edge, self.col_hi[r] * self.edge
+        f_lo = math.floor(xa / h - 0.5 * P) + 1
+        f_hi = math.floor(xb / h - 0.5 * P) + 1
+        count = min(M, f_hi + P - f_lo + 2)
+        return (f_lo - 1) % M, count
+
+    @staticmethod
+    def ring_pieces(start, count, M):
+        if count <= 0:
+            return []
+        if start + count <= M:
+            return [(start, start + count)]
+        return [(start, M), (0, start + count - M)]
+
+    def exchange_pieces(self, src, dst, M, P, h):
+        """Plane intervals of rank src's touched planes inside rank dst's slab."""
+        a, b = self.slab(dst, M)
+        out = []
+        for lo, hi in self.ring_pieces(*self.touched_planes(src, M, P, h), M):
+            lo2, hi2 = max(lo, a), min(hi, b)
+            if lo2 < hi2:
+                out.append((lo2, hi2))
+        return out
+
+
+def _all_to_allv(send, send_counts, group, multi):
+    """all_to_all_single of the rows of `send` (grouped by destination, counts
+    per rank); returns (recv, recv_counts)."""
+    if not multi:
+        return send, list(send_counts)
+    dev = send.device
+    sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv_counts = [int(v) for v in rc.tolist()]
+    recv = send.new_empty((sum(recv_counts),) + tuple(send.shape[1:]))
+    dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=recv_counts, input_split_sizes=list(send_counts),
+                           group=group)
+    return recv, recv_counts
+
+
+def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str = "auto"):
+    """core.total_potential for particles PARTITIONED over the ranks, by
+    domain decomposition: rank r passes its own (n_r, 3) positions and
+    (n_r,) charges (any subset of the system) and receives their potentials.
+
+      1. migrate: every particle to the rank owning its x-slab of columns
+         (all-to-allv of (x, y, z, q) records);
+      2. halo: the particles of the `reach` columns beyond each slab's +x end
+         to that slab's rank (all-to-allv);
+      3. real space on own + halo particles (se_realspace_domain_dev: targets
+         are the own particles, the half shell points to +x) -- concurrently
+         with the k-space chain on the backend's side stream;
+      4. the halo particles' Newton partial sums back to their owners;
+      5. spread of the own particles into a local grid; the touched x-planes
+         to the k-space slab owners (all-to-allv, summed there) -- D = 3
+         with M divisible by the rank count ("slab"): slab FFT with two
+         all-to-all transposes and the filtered planes back to the ranks that
+         touch them; otherwise ("replicated") a sum all-reduce of the grid and
+         the k-space stage on every rank;
+      6. gather of the own particles, phi = phi_R + phi_self + phi_F + halo
+         sums, and each potential back to the rank that passed the particle
+         (all-to-allv in the order of step 1)."""
+    init = dist.is_initialized()
+    world = dist.get_world_size(group) if init else 1
+    rank = dist.get_rank(group) if init else 0
+    multi = init and world > 1
+    dev = pos_local.device
+    n_in = int(q_local.shape[0])
+    if hasattr(backend, "bind_stream"):
+        backend.bind_stream()
+    if hasattr(backend, "check_system"):
+        _agreed(lambda: backend.check_system(pos_local, q_local, neutrality=False), q_local, group, multi)
+    # the neutrality check of the whole system (core.py:180-191) on the
+    # reduced charge sums
+    sums = torch.stack([q_local.sum(), q_local.abs().sum()]).to(torch.float64)
+    ntot = torch.tensor([n_in], dtype=torch.int64, device=dev)
+    if multi:
+        dist.all_reduce(sums, group=group)
+        dist.all_reduce(ntot, group=group)
+    qsum, qabs = float(sums[0]), float(sums[1])
+    if abs(qsum) > 1e-12 * max(qabs, 1.0):
+        if backend.peri.D > 0:
+            raise ValueError("periodic Ewald summation requires a charge-neutral system")
+        import warnings
+        warnings.warn("system is not charge neutral; free-space potentials are still defined but the Ewald "
+                      "split assumes neutrality", stacklevel=2)
+    part = backend.domain_partition(world, int(ntot.item()))
+    cols_of = torch.tensor(part.owner_of_col, dtype=torch.int64, device=dev)
+
+    # 1. migrate to the owners
+    rec = torch.cat([pos_local, q_local[:, None]], dim=1)
+    dest = cols_of[part.columns(pos_local[:, 0])]
+    order = torch.argsort(dest, stable=True)
+    send_counts = torch.bincount(dest, minlength=world).tolist()
+    own, own_counts = _all_to_allv(rec[order], send_counts, group, multi)
+    n_own = int(own.shape[0])
+
+    # 2. halo: each own particle to the ranks whose +x halo holds its column
+    cx = part.columns(own[:, 0])
+    halo_tab = torch.tensor(part.halo_to, dtype=torch.bool, device=dev)  # (ncols, world)
+    hsel = [torch.nonzero(halo_tab[cx, d], as_tuple=True)[0] for d in range(world)]
+    hidx = torch.cat(hsel) if hsel else torch.zeros(0, dtype=torch.int64, device=dev)
+    halo, halo_counts = _all_to_allv(own[hidx], [int(h.numel()) for h in hsel], group, multi)
+    local = torch.cat([own, halo], dim=0)
+    lpos = local[:, :3].contiguous()
+    lq = local[:, 3].contiguous()
+    opos = own[:, :3].contiguous()
+    oq = own[:, 3].contiguous()
+
+    # 3. + 5. the k-space chain on the side stream, real space on this one
+    ks = getattr(backend, "kstream", None)
+    cur = torch.cuda.current_stream() if ks is not None else None
+    side = torch.cuda.stream(ks) if ks is not None else contextlib.nullcontext()
+    phi_local = backend.empty_phi(lpos.shape[0])
+    phik = backend.empty_phi(n_own)
+    grid = backend.empty_grid()
+    D = backend.peri.D
+    M = backend.params.M
+    if kspace == "auto":
+        kspace = "slab" if (D == 3 and M % world == 0) else "replicated"
+    if kspace not in ("slab", "replicated"):
+        raise ValueError(f"kspace must be 'auto', 'slab' or 'replicated', got {kspace!r}")
+    if kspace == "slab" and not (D == 3 and M % world == 0):
+        raise ValueError("the slab k-space stage needs D = 3 and M divisible by the rank count")
+    if ks is not None:
+        ks.wait_stream(cur)
+    with side:
+        backend.spread_all(opos, oq, grid)
+        if kspace == "replicated":
+            work = dist.all_reduce(grid, op=dist.ReduceOp.SUM, group=group, async_op=True) if multi else None
+    backend.realspace_domain(lpos, lq, n_own, part, rank, phi_local)
+    with side:
+        if kspace == "replicated":
+            if work is not None:
+                work.wait()
+            backend.kspace_apply(grid)
+        else:
+            _slab_kspace_domain(backend, part, grid, rank, world, group, multi)
+        backend.gather_all(grid, opos, phik, accumulate=False)
+    if ks is not None:
+        cur.wait_stream(ks)
+
+    # 4. the halo sums back to the owners (the order of step 2)
+    back, _ = _all_to_allv(phi_local[n_own:].contiguous(), halo_counts, group, multi)
+    phi_own = phi_local[:n_own] + phik
+    if back.numel():
+        phi_own.index_add_(0, hidx, back)
+    _finish(backend, phi_own, group, multi)
+
+    # 6. potentials back to the ranks that passed the particles
+    ret, _ = _all_to_allv(phi_own, own_counts, group, multi)
+    out = torch.empty(n_in, dtype=torch.float64, device=dev)
+    out[order] = ret
+    return out
+
+
+def _slab_kspace_domain(backend, part, grid, rank, world, group, multi):
+    """D = 3 k-space stage over x-slabs with a halo-restricted grid exchange:
+    each rank's touched x-planes go to the slab owners and are summed there
+    (instead of a reduce-scatter of the whole grid), the slab FFT runs with
+    its two all-to-all transposes, and each rank receives back the filtered
+    planes it touches (instead of an all-gather of the whole grid)."""
+    g = backend.grid_geometry()
+    M, P, h = g["M"], g["P"], g["h"]
+    plane = grid.shape[1] * grid.shape[2]
+    flat = grid.reshape(M, plane)
+    a, b = part.slab(rank, M)
+    # forward: my touched planes, grouped by the slab owner
+    send_parts, send_counts = [], []
+    for d in range(world):
+        pieces = part.exchange_pieces(rank, d, M, P, h)
+        send_parts += [flat[lo:hi] for lo, hi in pieces]
+        send_counts.append(sum(hi - lo for lo, hi in pieces))
+    send = torch.cat(send_parts) if send_parts else flat.new_zeros((0, plane))
+    recv, _ = _all_to_allv(send, send_counts, group, multi)
+    slab = flat.new_zeros((b - a, plane))
+    row = 0
+    for s in range(world):
+        for lo, hi in part.exchange_pieces(s, rank, M, P, h):
+            slab[lo - a:hi - a] += recv[row:row + hi - lo]
+            row += hi - lo
+    slab = slab.reshape((b - a,) + tuple(grid.shape[1:]))
+    send_s = backend.empty_spectrum(world)
+    recv_s = torch.empty_like(send_s) if multi else send_s
+    backend.slab_forward(slab, world, send_s)
+    if multi:
+        dist.all_to_all_single(recv_s.reshape(-1), send_s.reshape(-1), group=group)
+    backend.slab_xpass(recv_s, rank, world)
+    if multi:
+        dist.all_to_all_single(send_s.reshape(-1), recv_s.reshape(-1), group=group)
+    backend.slab_inverse(send_s, world, slab)
+    sflat = slab.reshape(b - a, plane)
+    # backward: the filtered planes each rank touches, from my slab
+    parts2, counts2 = [], []
+    for d in range(world):
+        pieces = part.exchange_pieces(d, rank, M, P, h)
+        parts2 += [sflat[lo - a:hi - a] for lo, hi in pieces]
+        counts2.append(sum(hi - lo for lo, hi in pieces))
+    send2 = torch.cat(parts2) if parts2 else flat.new_zeros((0, plane))
+    recv2, _ = _all_to_allv(send2, counts2, group, multi)
+    row = 0
+    for s in range(world):
+        for lo, hi in part.exchange_pieces(rank, s, M, P, h):
+            flat[lo:hi] = recv2[row:row + hi - lo]
+            row += hi - lo
