@@ -31,7 +31,7 @@ __global__ void gather_records_kernel(const double *__restrict__ pos, const doub
 // nunits[0] = number of units; nunits[1] = the unit holding sorted position
 // rlo (the first unit of a rank's shard; the unit count if rlo >= N).
 // Units are emitted only for bins in [ulo, uhi) (all bins: [0, nbins)); a
-// restricted list starts at unit 0 (nunits[1] = 0).
+// restricted list, or rlo < 0, starts at unit 0 (nunits[1] = 0).
 __global__ void __launch_bounds__(1024) build_units_kernel(const int *__restrict__ counts, int nbins, int chunk,
                                                            int *__restrict__ starts, int4 *__restrict__ units,
                                                            int *__restrict__ nunits, int64_t rlo, int ulo, int uhi) {
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(1024) build_units_kernel(const int *__restrict
         starts[nbins] = (int)cpos;
         *nunits = (int)upos;
         if (rlo >= cpos) nunits[1] = (int)upos;
-        if (ulo > 0 || uhi < nbins) nunits[1] = 0;
+        if (rlo < 0 || ulo > 0 || uhi < nbins) nunits[1] = 0;  // no shard start: the list from unit 0
     }
 }
 
