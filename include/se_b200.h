@@ -142,6 +142,16 @@ int se_plan_set_graphs(se_plan_t plan, int on);
  * a pending error (coincident particles -> SE_ESINGULAR) and collects the
  * profiling events. */
 int se_plan_set_deferred_checks(se_plan_t plan, int on);
+/* Deterministic mode (on != 0; default from the environment variable
+ * SE_B200_DETERMINISTIC at plan creation): results are bitwise reproducible
+ * run to run, as the reference's thread-count independence requires
+ * (test_core.py:139-145, test_realspace.py:129-133).  The real-space sum
+ * then runs without Newton's third law (each target sums all its partners
+ * itself, no source-side atomics; ~2x the pair work) and spreading writes
+ * per-work-unit tiles that are reduced into the grid in a fixed order
+ * (instead of fp64 atomic tile flushes).  The default mode agrees with it
+ * to rounding (~1e-15 relative). */
+int se_plan_set_deterministic(se_plan_t plan, int on);
 int se_plan_finish(se_plan_t plan);
 /* Number of kernel launches issued by this plan since creation (for the bench). */
 int se_plan_launch_count(se_plan_t plan, int64_t *count);

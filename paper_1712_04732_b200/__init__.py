@@ -26,4 +26,6 @@ for _mod, _names in _PUBLIC.items():
         globals()[_n] = getattr(_mod, _n)
 
 __all__ = sorted(n for names in _PUBLIC.values() for n in names)
+
+from ._native import set_deterministic  # noqa: E402  (beyond the reference: opt-in bitwise reproducibility)
 del _mod, _names, _n

@@ -70,6 +70,7 @@ SIGNATURES = {
     "se_plan_set_profiling": [_P, ctypes.c_int],
     "se_plan_set_graphs": [_P, ctypes.c_int],
     "se_plan_set_deferred_checks": [_P, ctypes.c_int],
+    "se_plan_set_deterministic": [_P, ctypes.c_int],
     "se_plan_finish": [_P],
     "se_plan_kernel_times": [_P, c_double_p, c_int64_p],
     "se_realspace_pair_count_dev": [_P, _P, _P, ctypes.c_int64, c_int64_p],
@@ -276,6 +277,17 @@ def params_key(p):
 def clear_plans():
     """Drop this thread's cached plans (device memory is freed with them)."""
     _plan_cache().clear()
+
+
+def set_deterministic(on: bool = True):
+    """Bitwise reproducible results for the plans created from now on
+    (se_plan_set_deterministic: real space without Newton's third law,
+    spreading by per-unit tiles reduced in a fixed order).  The reference
+    promises thread-count independent, bit-identical potentials
+    (test_core.py:139-145); the default mode agrees with this one to
+    rounding.  Drops this thread's cached plans."""
+    os.environ["SE_B200_DETERMINISTIC"] = "1" if on else "0"
+    clear_plans()
 
 
 def timings_buffer():

@@ -362,14 +362,14 @@ void plan_release_device(se_plan *pl) {
         if (h) cufftDestroy(h);
     for (Binning *b : {&pl->tbin, &pl->cbin})
         for (DevBuf *d : {&b->keys, &b->keys_sorted, &b->idx, &b->idx_sorted, &b->counts, &b->starts, &b->units,
-                          &b->nunits, &b->cub_tmp, &b->rec})
+                          &b->nunits, &b->ubstart, &b->fhist, &b->fstart, &b->bsum, &b->rec})
             d->release();
     for (ModeTable *t : {&pl->tM, &pl->tg0, &pl->tgs, &pl->tMt, &pl->tNc, &pl->tNh}) {
         t->k.release();
         t->what.release();
     }
     for (DevBuf *d : {&pl->flag, &pl->spec, &pl->spec2, &pl->spec3, &pl->work, &pl->grid_tmp, &pl->rows_I,
-                      &pl->ghat, &pl->grid_dev, &pl->io_pos, &pl->io_q, &pl->io_phi, &pl->io_grid, &pl->check, &pl->pairs, &pl->racc})
+                      &pl->ghat, &pl->grid_dev, &pl->io_pos, &pl->io_q, &pl->io_phi, &pl->io_grid, &pl->check, &pl->pairs, &pl->racc, &pl->sdet})
         d->release();
     if (pl->own_stream) cudaStreamDestroy(pl->own_stream);
 }
@@ -394,6 +394,10 @@ int se_plan_create(se_plan_t *plan, int D, double L, const se_params_t *p, int d
     pl->L = L;
     pl->p = *p;
     pl->device = device;
+    {
+        const char *det = std::getenv("SE_B200_DETERMINISTIC");
+        pl->deterministic = det && det[0] && det[0] != '0';
+    }
     try {
         pl->g = build_grid(D, L, *p);
         SE_CUDA(cudaStreamCreateWithFlags(&pl->own_stream, cudaStreamNonBlocking));
@@ -438,6 +442,15 @@ int se_plan_finish(se_plan_t plan) {
     DeviceGuard dg(pl->device);
     if (pl->flag.ptr) check_flag(pl);
     prof_collect(pl);
+    SE_API_END
+}
+
+int se_plan_set_deterministic(se_plan_t plan, int on) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    pl->deterministic = on != 0;
+    graph_drop(pl);
     SE_API_END
 }
 

@@ -100,9 +100,11 @@ struct ModeTable {
 struct Binning {
     int nbins = 0;
     int64_t capacity = 0;
-    DevBuf keys, keys_sorted, idx, idx_sorted, counts, starts, units, nunits, cub_tmp;
+    DevBuf keys, keys_sorted, idx, idx_sorted, counts, starts, units, nunits, ubstart;
+    DevBuf fhist, fstart, bsum;  // counting sort: fine-bin histogram / starts, scan block sums
     DevBuf rec;  // sorted particle records (x, y, z, q) as double4
-    size_t cub_bytes = 0;
+    int fine_shift = 0;          // index bits refining a coarse key
+    int64_t nfine = 0;           // fine bins
 };
 
 struct TileGeom {
@@ -154,6 +156,7 @@ struct se_plan {
     se::DomainSpec dom{};
     se::Binning cbin;  // cell binning for the real-space sum
     se::DevBuf flag;   // device error flags (int)
+    se::DevBuf sdet;   // deterministic spreading: per-unit padded tiles
 
     // k-space
     bool kspace_ready = false;
@@ -189,6 +192,10 @@ struct se_plan {
     // CUDA graph of the fused total-potential body (real space + spread +
     // k-space + gather), replayed for repeated calls with the same buffers
     bool graphs = true;
+    // bitwise reproducible results (no order-dependent fp64 atomics): the
+    // real-space sum without Newton's third law, spreading through per-unit
+    // tiles reduced in a fixed order; from SE_B200_DETERMINISTIC at creation
+    bool deterministic = false;
     cudaGraphExec_t gexec = nullptr;
     const void *gkey[3] = {};  // pos, q, phi
     int64_t gN = -1;

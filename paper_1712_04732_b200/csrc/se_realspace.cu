@@ -684,11 +684,17 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
         //   [j0, j1)  in-box window (own column: sources above the unit, j > t)
         //   [k0, ce)  the window's part below z = 0, as the image shifted by -L
         //   [cs, k1)  its part above z = L, shifted by +L (periodic z only)
-        const int R = a.reach, nc = (R + 1) + R * (2 * R + 1);
+        // NEWTON: the half shell ((R + 1) + R (2R + 1) columns); otherwise
+        // (the deterministic mode) the full shell of (2R + 1)^2 columns,
+        // R = 2: <= 25 lanes, each target summing all its partners itself
+        const int R = a.reach, nc = NEWTON ? (R + 1) + R * (2 * R + 1) : (2 * R + 1) * (2 * R + 1);
         int j0 = 0, j1 = 0, k0 = 0, k1 = 0, cs = 0, ce = 0, shc = 0;  // shc: x, y image codes (-1, 0, 1)
         if (lane < nc) {
             int ox, oy;
-            if (lane <= R) {
+            if (!NEWTON) {
+                ox = cx - R + lane / (2 * R + 1);
+                oy = cy - R + lane % (2 * R + 1);
+            } else if (lane <= R) {
                 ox = cx;
                 oy = cy + lane;
             } else {
@@ -699,9 +705,10 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
             int xc = ox, yc = oy, sx = 0, sy = 0;
             bool ok = true;
             if (a.mode[0] == 1) {
-                if (xc >= n) { xc -= n; sx = 1; }
+                if (xc < 0) { xc += n; sx = -1; }
+                else if (xc >= n) { xc -= n; sx = 1; }
             } else {
-                ok = ok && xc < n;
+                ok = ok && xc >= 0 && xc < n;
             }
             if (a.mode[1] == 1) {
                 if (yc < 0) { yc += n; sy = -1; }
@@ -709,7 +716,7 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
             } else {
                 ok = ok && yc >= 0 && yc < n;
             }
-            const double gx = max(ox - cx - 1, 0) * a.edge, gy = max(abs(oy - cy) - 1, 0) * a.edge;
+            const double gx = max(abs(ox - cx) - 1, 0) * a.edge, gy = max(abs(oy - cy) - 1, 0) * a.edge;
             const double h2 = a.rc2 - gx * gx - gy * gy;
             ok = ok && h2 >= 0.0;
             if (ok) {
@@ -717,7 +724,7 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
                 ce = starts[xc * n + yc + 1];
                 const double h = sqrt(h2);
                 const double wlo = zmin - h, whi = zmax + h;
-                const bool own = lane == 0;
+                const bool own = NEWTON && lane == 0;  // own column: sources above the unit only
                 j0 = own ? un.y + 1 : zbound(rec, cs, ce, zq(wlo, a.qinv) - 1, false, a.qinv);
                 j1 = zbound(rec, j0, ce, zq(whi, a.qinv) + 1, true, a.qinv);
                 k0 = ce;
@@ -739,7 +746,7 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
                 if (c + 1 < nc && n0 + lane < n1) prefetch_l1(rec + n0 + lane);
             }
             const double shx = (code / 3 - 1) * a.L, shy = (code % 3 - 1) * a.L;
-            if (c0 < c1) run(c0, c1, shx, shy, 0.0, c == 0 ? un.y : -1);
+            if (c0 < c1) run(c0, c1, shx, shy, 0.0, (NEWTON && c == 0) ? un.y : -1);
             if (ck0 < cce) run(ck0, cce, shx, shy, -a.L, -1);
             if (ccs < ck1) run(ccs, ck1, shx, shy, a.L, -1);
         }
@@ -882,6 +889,7 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
         if (reach > kReachMax || nn > 1024)
             fail(SE_EINVAL, "domain column grid: columns must be at least rc / 3 wide and at most 1024 per axis");
     } else {
+        if (pl->deterministic) reach = 2;  // the full shell must fit one lane per column
         for (;; --reach) {
             nn = (long long)std::floor(reach * L / rc);
             if (nn < 1) nn = 1;
@@ -905,13 +913,17 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     int nbins = c.n * c.n;
     {
         // z quantum L / 2^kb <= rc / 256: the windows' one-quantum slack and
-        // the index order inside a quantum cost nothing measurable, and the
-        // key stays short (cfg2: 10 + 12 bits, three radix passes, not four)
+        // the index order inside a quantum cost nothing measurable.  The
+        // counting sort's fine bins (column, quantum) stay <= max(2^22, 4 N)
+        // (cfg2: 900 columns x 2^12 quanta; a coarser quantum only widens
+        // the windows' slack)
         int cb = 1;
         while ((1LL << cb) < (long long)nbins) ++cb;
         int kz = 8;
         while (kz < 20 && (double)(1 << kz) < 256.0 * L / rc) ++kz;
         a.kb = std::min(32 - cb, kz);
+        const long long fine_cap = std::max<long long>(1LL << 22, 4LL * N);
+        while (a.kb > 1 && ((long long)nbins << a.kb) > fine_cap) --a.kb;
         a.qinv = (double)(1 << a.kb) / L;
     }
     for (int ax = 0; ax < 3; ++ax) a.mode[ax] = c.mode[ax];
@@ -948,12 +960,15 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
     // per column + 1 units from nunits[1] on
     if (a.rhi - a.rlo < N) maxu = std::min<int64_t>(maxu, (a.rhi - a.rlo) / unit + nbins + 2);
     const bool mi = c.mode[0] == 2 || c.mode[1] == 2 || c.mode[2] == 2;
+    // deterministic mode: no Newton (no source-side atomics), each target
+    // sums its own partners in a fixed order
+    const bool full = mi || pl->deterministic;
     unsigned blocks = (unsigned)((maxu + kWarps - 1) / kWarps);
     cudaStream_t st = pl->stream;
     const size_t smem = sizeof(WarpBufT<FLD>) * kWarps;
     const int nc = FLD ? 3 : 1;
     double *acc = nullptr;
-    if (!mi) {
+    if (!full) {
         pl->racc.ensure(sizeof(double) * nc * N);
         acc = pl->racc.as<double>();
         SE_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * nc * N, st));
@@ -970,12 +985,15 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
     if (mi)
         args(wide ? realspace_cell_kernel<true, COUNT, false, true, FLD>
                   : realspace_cell_kernel<true, COUNT, false, false, FLD>);
+    else if (full)
+        args(wide ? realspace_cell_kernel<false, COUNT, false, true, FLD>
+                  : realspace_cell_kernel<false, COUNT, false, false, FLD>);
     else
         args(wide ? realspace_cell_kernel<false, COUNT, true, true, FLD>
                   : realspace_cell_kernel<false, COUNT, true, false, FLD>);
     SE_LAUNCH_CHECK();
     pl->launches += 1;
-    if (!mi && !COUNT) {
+    if (!full && !COUNT) {
         if (FLD)
             realspace_finish_field_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(
                 acc, pl->cbin.idx_sorted.as<int>(), N, phi);

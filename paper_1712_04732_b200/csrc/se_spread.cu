@@ -274,7 +274,7 @@ struct LanePairs {
 template <int WIN, int PC>
 __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restrict__ rec, const int4 *__restrict__ units,
                                                           const int *__restrict__ nunits, SpreadArgs a,
-                                                          double *__restrict__ grid) {
+                                                          double *__restrict__ grid, double *__restrict__ dbuf) {
     if ((int)blockIdx.x >= *nunits) return;
     int4 un = units[blockIdx.x];
     int ubeg = (int)max((int64_t)un.y, a.rlo), uend = (int)min((int64_t)un.y + un.z, a.rhi);
@@ -336,10 +336,61 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
         }
     }
     __syncthreads();
+    if (dbuf) {
+        // deterministic mode: the unit's padded tile as it is (coalesced
+        // stores); spread_det_reduce_kernel sums the units in a fixed order
+        double *o = dbuf + (size_t)blockIdx.x * ncell;
+        for (int i = threadIdx.x; i < ncell; i += blockDim.x) o[i] = tile[i];
+        return;
+    }
     for_tile_cells(a, gmap, [&](int ti, long long gi) {
         const double v = tile[ti];
         if (gi >= 0 && v != 0.0) atomicAdd(grid + gi, v);
     });
+}
+
+// Deterministic spreading, second pass: every grid point sums the cells of
+// the per-unit padded tiles that map onto it -- candidate tiles in
+// ascending (x, y, z) tile order, a tile's units in order -- so the grid is
+// bitwise reproducible (the atomic tile flush adds in arbitrary order).
+__global__ void spread_det_reduce_kernel(const double *__restrict__ dbuf, const int4 *__restrict__ units,
+                                         const int *__restrict__ ubstart, SpreadArgs a, int64_t G,
+                                         double *__restrict__ grid) {
+    const int ext[3] = {a.Tp, a.Tp, a.pitch};
+    const int te[3] = {a.T, a.T, a.Tz};
+    const int plane = a.Tp * a.pitch, ncell = a.Tp * plane;
+    for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < G; gi += (int64_t)gridDim.x * blockDim.x) {
+        int g[3];
+        g[2] = (int)(gi % a.shape[2]);
+        g[1] = (int)((gi / a.shape[2]) % a.shape[1]);
+        g[0] = (int)(gi / ((int64_t)a.shape[2] * a.shape[1]));
+        int ct[3][8], cl[3][8], nc[3];
+        for (int ax = 0; ax < 3; ++ax) {
+            nc[ax] = 0;
+            for (int t = 0; t < a.nt[ax] && nc[ax] < 8; ++t) {
+                int l = g[ax] - (a.lo[ax] + t * te[ax]);
+                if (ax < a.D) l = ((l % a.M) + a.M) % a.M;
+                if (l >= 0 && l < ext[ax]) {
+                    ct[ax][nc[ax]] = t;
+                    cl[ax][nc[ax]] = l;
+                    ++nc[ax];
+                }
+            }
+        }
+        double v = 0.0;
+        for (int i = 0; i < nc[0]; ++i)
+            for (int j = 0; j < nc[1]; ++j)
+                for (int k = 0; k < nc[2]; ++k) {
+                    const int b = (ct[0][i] * a.nt[1] + ct[1][j]) * a.nt[2] + ct[2][k];
+                    const int off = cl[0][i] * plane + cl[1][j] * a.pitch + cl[2][k];
+                    for (int u = ubstart[b]; u < ubstart[b + 1]; ++u) {
+                        const int4 un = units[u];
+                        if ((int64_t)un.y + un.z <= a.rlo || (int64_t)un.y >= a.rhi) continue;  // not this shard's
+                        v += dbuf[(size_t)u * ncell + off];
+                    }
+                }
+        grid[gi] = v;
+    }
 }
 
 template <int WIN, int PC>
@@ -638,7 +689,9 @@ void spread_run(se_plan *pl, const double *pos, const double *q, int64_t N, doub
     if (pl->p.P > pl->g.M) fail(SE_EINVAL, "window support P must not exceed M");
     const se_grid_t &g = pl->g;
     size_t gsize = (size_t)g.shape[0] * g.shape[1] * g.shape[2];
-    SE_CUDA(cudaMemsetAsync(grid, 0, sizeof(double) * gsize, pl->stream));
+    tile_setup(pl);
+    const bool det = pl->deterministic && pl->tile.T > 0;
+    if (!det || N <= 0) SE_CUDA(cudaMemsetAsync(grid, 0, sizeof(double) * gsize, pl->stream));
     if (N <= 0) return;
     bin_tiles(pl, pos, q, N);
     SpreadArgs a = make_args(pl);
@@ -649,14 +702,26 @@ void spread_run(se_plan *pl, const double *pos, const double *q, int64_t N, doub
     if (t.T > 0) {
         int64_t maxu = binning_max_units(pl->tbin, N, t.nt[0] * t.nt[1] * t.nt[2], kUnit);
         const int PC = t.nwarps == pl->p.P ? pl->p.P : 0;
+        double *dbuf = nullptr;
+        if (det) {
+            pl->sdet.ensure(sizeof(double) * (size_t)maxu * t.Tp * t.Tp * t.pitch);
+            dbuf = pl->sdet.as<double>();
+        }
         dispatch_window(pl->p.window, [&](auto W) {
             dispatch_p(PC, [&](auto PCv) {
                 auto kern = spread_tile_kernel<decltype(W)::value, decltype(PCv)::value>;
                 SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)t.smem));
                 kern<<<(unsigned)maxu, 32 * t.nwarps, t.smem, pl->stream>>>(rec, pl->tbin.units.as<int4>(),
-                                                                             pl->tbin.nunits.as<int>(), a, grid);
+                                                                             pl->tbin.nunits.as<int>(), a, grid, dbuf);
             });
         });
+        if (det) {
+            SE_LAUNCH_CHECK();
+            pl->launches += 1;
+            spread_det_reduce_kernel<<<(unsigned)std::min<int64_t>((gsize + 255) / 256, 148 * 16), 256, 0,
+                                       pl->stream>>>(dbuf, pl->tbin.units.as<int4>(), pl->tbin.ubstart.as<int>(), a,
+                                                     (int64_t)gsize, grid);
+        }
     } else {
         int64_t n = a.rhi - a.rlo;
         int wpb = 4;

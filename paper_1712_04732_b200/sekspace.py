@@ -20,7 +20,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _native, windows
+from . import _native, aft, windows  # noqa: F401  (aft: reachable as sekspace.aft, as in the reference)
 from .core import ParticleSystem, Periodicity, SEParams
 
 
@@ -94,6 +94,30 @@ def _stage_plan(grid: Grid, wspec: windows.WindowSpec):
     if grid.P > grid.M:
         raise ValueError("window support P must not exceed M")
     return _native.plan_for(grid.D, grid.L, _stage_params(grid, wspec))
+
+
+def _stencil(system: ParticleSystem, wspec: windows.WindowSpec, grid: Grid, sel) -> tuple[list, list]:
+    """Per-axis stencil indices (n, P) and window weights of a particle
+    selection (sekspace.py:105-121): first = floor(u / h - P / 2) + 1 with
+    u = x + the free-axis offset, idx = first + t (mod M on periodic axes),
+    weights = window(idx h - u).  The host-side view of what the spreading
+    and gathering kernels compute per particle (the reference's tests use it
+    for the mass identity); the weights come from the library's window
+    evaluation."""
+    P, h = grid.P, grid.h
+    t = np.arange(P)
+    idxs, wts = [], []
+    offs = grid.offsets
+    for a in range(3):
+        u = np.asarray(system.positions[sel, a]) + offs[a]
+        first = np.floor(u / h - 0.5 * P).astype(np.int64) + 1
+        idx = first[:, None] + t[None, :]
+        delta = idx * h - u[:, None]
+        if a < grid.D:
+            idx = np.mod(idx, grid.M)
+        wts.append(windows.evaluate(delta, wspec))
+        idxs.append(idx)
+    return idxs, wts
 
 
 def spread(system: ParticleSystem, wspec: windows.WindowSpec, grid: Grid,

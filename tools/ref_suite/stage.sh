@@ -21,6 +21,7 @@ cat > "$OUT/run.sh" <<'EOS'
 # the reference's 190 tests against paper_1712_04732_b200 via the pmewald alias
 cd "$(dirname "$0")"
 export PMEWALD_REF_STAGED=$PWD/_ref_modules
+export SE_B200_DETERMINISTIC=1
 export PYTHONPATH=$PWD:$PWD/../..${PYTHONPATH:+:$PYTHONPATH}
 python -m pytest tests -q -p no:cacheprovider -rf "$@"
 EOS
