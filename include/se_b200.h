@@ -257,8 +257,12 @@ int se_kspace_field_host(se_plan_t plan, const double *pos, const double *q, int
 /* Slab-decomposed k-space stage of D = 3 (aft.py:203-206 + sekspace.py:198-206
  * + aft.py:237-238 split over `world` ranks).  Rank r owns the
  * x-slab of nx = M / world planes (block r of the C-order grid, as a
- * reduce-scatter leaves it); M % world == 0.  Complex buffers are interleaved
- * fp64 (re, im):
+ * reduce-scatter leaves it); M % world == 0.  Also D = 0 on the truncated-
+ * kernel path (_kspace_freespace_kernel, sekspace.py:301-337): the transform
+ * size is then nconv (se_plan_d0_geometry), nx = nconv / world padded
+ * x-planes per rank, and the slab buffers hold the (nx, Mt, Mt) planes of
+ * the Mt^3 spread grid (planes >= Mt are zero), zero-padded / restricted
+ * inside.  Complex buffers are interleaved fp64 (re, im):
  *   se_slab_forward_dev: slab (nx, M, M) real -> send (world, nx, nky, nkz)
  *     complex: 2-D R2C over (y, z), block s = this rank's planes x ky-chunk s;
  *   (caller: all-to-all of equal blocks -> recv, i.e. (M, nky, nkz) = all kx
@@ -268,7 +272,8 @@ int se_kspace_field_host(se_plan_t plan, const double *pos, const double *q, int
  *   (caller: all-to-all back)
  *   se_slab_inverse_dev: back (world, nx, nky, nkz) -> slab (nx, M, M) real
  *     (the slab of the k-space-filtered grid; an all-gather gives the grid).
- * se_slab_geometry returns nx, nky = M / world and nkz = M / 2 + 1. */
+ * se_slab_geometry returns nx, nky = n / world and nkz = n / 2 + 1 (n = M, or
+ * nconv for D = 0). */
 int se_slab_geometry(se_plan_t plan, int world, int64_t *nx, int64_t *nky, int64_t *nkz);
 int se_slab_forward_dev(se_plan_t plan, int world, const double *slab, double *send);
 int se_slab_xpass_dev(se_plan_t plan, int world, int rank, double *recv);

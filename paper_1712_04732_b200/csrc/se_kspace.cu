@@ -672,13 +672,40 @@ __global__ void scale_slab_kernel(cplx *__restrict__ F, int M, int nky, int ky0,
     }
 }
 
+// D = 0 (truncated-kernel path): F *= ghat * 4 pi af[kx] af[ky] ah[kz] / n^3 on
+// this rank's ky-chunk of the (kx, ky, kz) spectrum (layout (n, nky, nh))
+__global__ void scale_d0k_slab_kernel(cplx *__restrict__ F, int n, int nky, int ky0, const double *__restrict__ ghat,
+                                      const double *__restrict__ af, const double *__restrict__ ah, double norm) {
+    const int nh = n / 2 + 1;
+    const int64_t total = (int64_t)n * nky * nh;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int iz = (int)(i % nh);
+        const int64_t r = i / nh;
+        const int iy = ky0 + (int)(r % nky), ix = (int)(r / nky);
+        const double fac = ghat[((int64_t)ix * n + iy) * nh + iz] * (4.0 * M_PI * af[ix]) * af[iy] * ah[iz] * norm;
+        const cplx v = F[i];
+        F[i] = make_double2(v.x * fac, v.y * fac);
+    }
+}
+
+// Slab-decomposed k-space stage: D = 3 on the M^3 grid; D = 0 (the
+// truncated-kernel path, sekspace.py:301-337) on the nconv^3 zero-padded
+// grid, whose x-planes >= Mt are zero.  n = M or nconv; rank r owns x-planes
+// [r n / world, (r + 1) n / world) and, after the transpose, ky-chunk r.
+static int slab_n(se_plan *pl) {
+    if (pl->D == 3) return pl->g.M;
+    if (pl->D == 0) return d0_geometry(pl->g.L, pl->g.M, pl->g.P, pl->p.s0, pl->p.rc, true).nconv;
+    fail(SE_EINVAL, "the slab-decomposed k-space stage covers D = 3 and the D = 0 kernel path");
+    return 0;
+}
+
 void slab_geometry(se_plan *pl, int world, int64_t *nx, int64_t *nky, int64_t *nkz) {
-    if (pl->D != 3) fail(SE_EINVAL, "the slab-decomposed k-space stage covers D = 3");
-    const int M = pl->g.M;
-    if (world < 1 || M % world) fail(SE_EINVAL, "slab decomposition needs M divisible by the number of ranks");
-    *nx = M / world;
-    *nky = M / world;
-    *nkz = M / 2 + 1;
+    const int n = slab_n(pl);
+    if (world < 1 || n % world)
+        fail(SE_EINVAL, "slab decomposition needs the transform size (M, or nconv for D = 0) divisible by the ranks");
+    *nx = n / world;
+    *nky = n / world;
+    *nkz = n / 2 + 1;
 }
 
 static void slab_ffts(se_plan *pl, int world) {
@@ -687,25 +714,34 @@ static void slab_ffts(se_plan *pl, int world) {
         if (*h) cufftDestroy(*h);
         *h = 0;
     }
-    const int M = pl->g.M, nx = M / world, nky = M / world, nh = M / 2 + 1;
-    int n2[2] = {M, M}, rin[2] = {M, M}, cout[2] = {M, nh};
-    SE_CUFFT(cufftPlanMany(&pl->slab_f2, 2, n2, rin, 1, M * M, cout, 1, M * nh, CUFFT_D2Z, nx));
-    SE_CUFFT(cufftPlanMany(&pl->slab_i2, 2, n2, cout, 1, M * nh, rin, 1, M * M, CUFFT_Z2D, nx));
-    int n1[1] = {M}, e1[1] = {M};
+    const int n = slab_n(pl), nx = n / world, nky = n / world, nh = n / 2 + 1;
+    int n2[2] = {n, n}, rin[2] = {n, n}, cout[2] = {n, nh};
+    SE_CUFFT(cufftPlanMany(&pl->slab_f2, 2, n2, rin, 1, n * n, cout, 1, n * nh, CUFFT_D2Z, nx));
+    SE_CUFFT(cufftPlanMany(&pl->slab_i2, 2, n2, cout, 1, n * nh, rin, 1, n * n, CUFFT_Z2D, nx));
+    int n1[1] = {n}, e1[1] = {n};
     SE_CUFFT(cufftPlanMany(&pl->slab_x, 1, n1, e1, nky * nh, 1, e1, nky * nh, 1, CUFFT_Z2Z, nky * nh));
     pl->slab_world = world;
 }
 
+// slab: (nx, M, M) real for D = 3; for D = 0 the (nx, Mt, Mt) planes of the
+// spread grid (zero for planes >= Mt), zero-padded to (nx, n, n) here
 void slab_forward(se_plan *pl, int world, const double *slab, double *send) {
     int64_t nx, nky, nkz;
     slab_geometry(pl, world, &nx, &nky, &nkz);
     slab_ffts(pl, world);
     set_streams(pl, {pl->slab_f2});
-    const int M = pl->g.M;
-    pl->spec.ensure(sizeof(cplx) * (size_t)nx * M * nkz);
-    SE_CUFFT(cufftExecD2Z(pl->slab_f2, const_cast<double *>(slab), pl->spec.as<cplx>()));
+    const int n = slab_n(pl);
+    pl->spec.ensure(sizeof(cplx) * (size_t)nx * n * nkz);
+    const double *src = slab;
+    if (pl->D == 0) {
+        const int Mt = pl->g.Mt;
+        pl->grid_tmp.ensure(sizeof(double) * (size_t)nx * n * n);
+        LAUNCH(pad_real_kernel, nx * n * n, slab, (int)nx, Mt, Mt, pl->grid_tmp.as<double>(), (int)nx, n, n);
+        src = pl->grid_tmp.as<double>();
+    }
+    SE_CUFFT(cufftExecD2Z(pl->slab_f2, const_cast<double *>(src), pl->spec.as<cplx>()));
     // (nx, world, nky * nkz) -> (world, nx, nky * nkz)
-    LAUNCH(swap01_kernel, nx * M * nkz, pl->spec.as<cplx>(), (int)nx, world, nky * nkz, reinterpret_cast<cplx *>(send));
+    LAUNCH(swap01_kernel, nx * n * nkz, pl->spec.as<cplx>(), (int)nx, world, nky * nkz, reinterpret_cast<cplx *>(send));
 }
 
 void slab_xpass(se_plan *pl, int world, int rank, double *recv) {
@@ -713,27 +749,41 @@ void slab_xpass(se_plan *pl, int world, int rank, double *recv) {
     slab_geometry(pl, world, &nx, &nky, &nkz);
     if (rank < 0 || rank >= world) fail(SE_EINVAL, "rank out of range");
     ensure_tables(pl);
+    if (pl->D == 0) d0_kernel_prepare(pl, nullptr);
     slab_ffts(pl, world);
     set_streams(pl, {pl->slab_x});
-    const int M = pl->g.M;
+    const int n = slab_n(pl);
     cplx *F = reinterpret_cast<cplx *>(recv);
     SE_CUFFT(cufftExecZ2Z(pl->slab_x, F, F, CUFFT_FORWARD));
-    LAUNCH(scale_slab_kernel, (int64_t)M * nky * nkz, F, M, (int)nky, (int)(rank * nky), pl->tM.k.as<double>(),
-           pl->tM.what.as<double>(), pl->p.xi, 1.0 / ((double)M * M * M));
+    if (pl->D == 3)
+        LAUNCH(scale_slab_kernel, (int64_t)n * nky * nkz, F, n, (int)nky, (int)(rank * nky), pl->tM.k.as<double>(),
+               pl->tM.what.as<double>(), pl->p.xi, 1.0 / ((double)n * n * n));
+    else
+        LAUNCH(scale_d0k_slab_kernel, (int64_t)n * nky * nkz, F, n, (int)nky, (int)(rank * nky), pl->ghat.as<double>(),
+               pl->tNc.what.as<double>(), pl->tNh.what.as<double>(), 1.0 / ((double)n * n * n));
     SE_CUFFT(cufftExecZ2Z(pl->slab_x, F, F, CUFFT_INVERSE));
 }
 
+// back (world, nx, nky, nkz) -> slab: (nx, M, M) for D = 3, the (nx, Mt, Mt)
+// restriction of the padded planes for D = 0
 void slab_inverse(se_plan *pl, int world, const double *back, double *slab) {
     int64_t nx, nky, nkz;
     slab_geometry(pl, world, &nx, &nky, &nkz);
     slab_ffts(pl, world);
     set_streams(pl, {pl->slab_i2});
-    const int M = pl->g.M;
-    pl->spec.ensure(sizeof(cplx) * (size_t)nx * M * nkz);
-    // (world, nx, nky * nkz) -> (nx, world, nky * nkz) = (nx, M, nkz)
-    LAUNCH(swap01_kernel, nx * M * nkz, reinterpret_cast<const cplx *>(back), world, (int)nx, nky * nkz,
+    const int n = slab_n(pl);
+    pl->spec.ensure(sizeof(cplx) * (size_t)nx * n * nkz);
+    // (world, nx, nky * nkz) -> (nx, world, nky * nkz) = (nx, n, nkz)
+    LAUNCH(swap01_kernel, nx * n * nkz, reinterpret_cast<const cplx *>(back), world, (int)nx, nky * nkz,
            pl->spec.as<cplx>());
-    SE_CUFFT(cufftExecZ2D(pl->slab_i2, pl->spec.as<cplx>(), slab));
+    if (pl->D == 3) {
+        SE_CUFFT(cufftExecZ2D(pl->slab_i2, pl->spec.as<cplx>(), slab));
+        return;
+    }
+    const int Mt = pl->g.Mt;
+    pl->grid_tmp.ensure(sizeof(double) * (size_t)nx * n * n);
+    SE_CUFFT(cufftExecZ2D(pl->slab_i2, pl->spec.as<cplx>(), pl->grid_tmp.as<double>()));
+    LAUNCH(restrict_real_kernel, nx * Mt * Mt, pl->grid_tmp.as<double>(), n, n, slab, (int)nx, Mt, Mt, 1.0);
 }
 
 // ------------------------------------------------------ field (D = 3, ik)

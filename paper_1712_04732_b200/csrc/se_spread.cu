@@ -359,36 +359,36 @@ __global__ void spread_det_reduce_kernel(const double *__restrict__ dbuf, const 
     const int ext[3] = {a.Tp, a.Tp, a.pitch};
     const int te[3] = {a.T, a.T, a.Tz};
     const int plane = a.Tp * a.pitch, ncell = a.Tp * plane;
+    // first local coordinate of grid index g in the padded tile t along
+    // axis ax (-1: not covered); on a periodic axis the padded tile may wrap
+    // onto g more than once (l, l + M, ... < ext: a tile wider than the grid)
+    // and a wide window with small tiles has up to ceil((T + P - 1) / T)
+    // covering tiles per axis
+    auto local = [&](int ax, int g, int t) {
+        int l = g - (a.lo[ax] + t * te[ax]);
+        if (ax < a.D) l = ((l % a.M) + a.M) % a.M;
+        return (l >= 0 && l < ext[ax]) ? l : -1;
+    };
+    auto step = [&](int ax) { return ax < a.D ? a.M : 1 << 30; };
     for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < G; gi += (int64_t)gridDim.x * blockDim.x) {
-        int g[3];
-        g[2] = (int)(gi % a.shape[2]);
-        g[1] = (int)((gi / a.shape[2]) % a.shape[1]);
-        g[0] = (int)(gi / ((int64_t)a.shape[2] * a.shape[1]));
-        int ct[3][8], cl[3][8], nc[3];
-        for (int ax = 0; ax < 3; ++ax) {
-            nc[ax] = 0;
-            for (int t = 0; t < a.nt[ax] && nc[ax] < 8; ++t) {
-                int l = g[ax] - (a.lo[ax] + t * te[ax]);
-                if (ax < a.D) l = ((l % a.M) + a.M) % a.M;
-                if (l >= 0 && l < ext[ax]) {
-                    ct[ax][nc[ax]] = t;
-                    cl[ax][nc[ax]] = l;
-                    ++nc[ax];
-                }
-            }
-        }
+        const int gz = (int)(gi % a.shape[2]);
+        const int gy = (int)((gi / a.shape[2]) % a.shape[1]);
+        const int gx = (int)(gi / ((int64_t)a.shape[2] * a.shape[1]));
         double v = 0.0;
-        for (int i = 0; i < nc[0]; ++i)
-            for (int j = 0; j < nc[1]; ++j)
-                for (int k = 0; k < nc[2]; ++k) {
-                    const int b = (ct[0][i] * a.nt[1] + ct[1][j]) * a.nt[2] + ct[2][k];
-                    const int off = cl[0][i] * plane + cl[1][j] * a.pitch + cl[2][k];
-                    for (int u = ubstart[b]; u < ubstart[b + 1]; ++u) {
-                        const int4 un = units[u];
-                        if ((int64_t)un.y + un.z <= a.rlo || (int64_t)un.y >= a.rhi) continue;  // not this shard's
-                        v += dbuf[(size_t)u * ncell + off];
-                    }
-                }
+        for (int tx = 0; tx < a.nt[0]; ++tx)
+            for (int lx = local(0, gx, tx); lx >= 0 && lx < ext[0]; lx += step(0))
+                for (int ty = 0; ty < a.nt[1]; ++ty)
+                    for (int ly = local(1, gy, ty); ly >= 0 && ly < ext[1]; ly += step(1))
+                        for (int tz = 0; tz < a.nt[2]; ++tz)
+                            for (int lz = local(2, gz, tz); lz >= 0 && lz < ext[2]; lz += step(2)) {
+                                const int b = (tx * a.nt[1] + ty) * a.nt[2] + tz;
+                                const int off = lx * plane + ly * a.pitch + lz;
+                                for (int u = ubstart[b]; u < ubstart[b + 1]; ++u) {
+                                    const int4 un = units[u];
+                                    if ((int64_t)un.y + un.z <= a.rlo || (int64_t)un.y >= a.rhi) continue;
+                                    v += dbuf[(size_t)u * ncell + off];
+                                }
+                            }
         grid[gi] = v;
     }
 }

@@ -124,9 +124,19 @@ class NativeBackend:
     def domain_partition(self, world, n_total):
         return DomainPartition(self.L, self.params, self.peri, world, n_total, self.shape)
 
-    def grid_geometry(self):
+    def slab_kgeo(self):
+        """Plane geometry of the slab k-space stage (DomainPartition.touched_pieces)."""
         g = self.plan.grid()
-        return {"M": int(g.M), "P": int(g.P), "h": float(g.h), "shape": tuple(g.shape)}
+        D = self.peri.D
+        if D == 3:
+            n = int(g.M)
+        else:
+            nconv, g0, R = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
+            _native.call("se_plan_d0_geometry", self.plan_k.handle, ctypes.byref(nconv), ctypes.byref(g0),
+                         ctypes.byref(R))
+            n = int(nconv.value)
+        return {"planes": int(g.shape[0]), "n": n, "P": int(g.P), "h": float(g.h),
+                "off": 0.0 if D >= 1 else 0.5 * g.P * g.h, "periodic": D >= 1}
 
     def spread_all(self, pos, q, grid):
         self._k("se_spread_shard_dev", _native.ptr(pos), _native.ptr(q), q.shape[0], 0, 1, _native.ptr(grid))
@@ -374,37 +384,41 @@ class DomainPartition:
         """Column index cx of each x (the kernel's floor(x / edge), clamped)."""
         return torch.clamp(torch.floor(x / self.edge), 0, self.ncols - 1).to(torch.int64)
 
-    # k-space plane bookkeeping (D = 3 slab mode) -------------------------
-    def slab(self, r, M):
-        nx = M // self.world
+    # k-space plane bookkeeping (slab mode) ---------------------------------
+    # kg: {"planes": x-planes of the spread grid (M, or Mt for D = 0),
+    #      "n": the slab transform size (M, or nconv), "P", "h",
+    #      "off": the x offset of the stencil (0, or P h / 2 on a free x),
+    #      "periodic": x periodic}
+    def slab(self, r, kg):
+        nx = kg["n"] // self.world
         return r * nx, (r + 1) * nx
 
-    def touched_planes(self, r, M, P, h):
-        """Ring interval (start, count) of x-planes the stencils of rank r's
-        particles can touch: first index floor(x / h - P / 2) + 1 over
-        x in [col_lo edge, col_hi edge), P planes each, one plane of margin
-        on both sides for the rounding of x / h."""
+    def touched_pieces(self, r, kg):
+        """x-plane intervals the stencils of rank r's particles can touch:
+        first index floor((x + off) / h - P / 2) + 1 over x in
+        [col_lo edge, col_hi edge), P planes each, one plane of margin on
+        both sides for the rounding of x / h; a ring interval mod M on a
+        periodic x, clipped to [0, planes) on a free one."""
         if self.col_hi[r] <= self.col_lo[r]:
-            return 0, 0
-        xa, xb = self.col_lo[r] * self.edge, self.col_hi[r] * self.edge
-        f_lo = math.floor(xa / h - 0.5 * P) + 1
-        f_hi = math.floor(xb / h - 0.5 * P) + 1
-        count = min(M, f_hi + P - f_lo + 2)
-        return (f_lo - 1) % M, count
-
-    @staticmethod
-    def ring_pieces(start, count, M):
-        if count <= 0:
             return []
-        if start + count <= M:
-            return [(start, start + count)]
-        return [(start, M), (0, start + count - M)]
+        P, h, planes, off = kg["P"], kg["h"], kg["planes"], kg["off"]
+        xa, xb = self.col_lo[r] * self.edge + off, self.col_hi[r] * self.edge + off
+        f_lo = math.floor(xa / h - 0.5 * P) + 1 - 1
+        f_hi = math.floor(xb / h - 0.5 * P) + 1 + P
+        if kg["periodic"]:
+            count = min(planes, f_hi - f_lo + 1)
+            start = f_lo % planes
+            if start + count <= planes:
+                return [(start, start + count)]
+            return [(start, planes), (0, start + count - planes)]
+        lo, hi = max(0, f_lo), min(planes, f_hi + 1)
+        return [(lo, hi)] if lo < hi else []
 
-    def exchange_pieces(self, src, dst, M, P, h):
+    def exchange_pieces(self, src, dst, kg):
         """Plane intervals of rank src's touched planes inside rank dst's slab."""
-        a, b = self.slab(dst, M)
+        a, b = self.slab(dst, kg)
         out = []
-        for lo, hi in self.ring_pieces(*self.touched_planes(src, M, P, h), M):
+        for lo, hi in self.touched_pieces(src, kg):
             lo2, hi2 = max(lo, a), min(hi, b)
             if lo2 < hi2:
                 out.append((lo2, hi2))
@@ -503,14 +517,15 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
     phi_local = backend.empty_phi(lpos.shape[0])
     phik = backend.empty_phi(n_own)
     grid = backend.empty_grid()
-    D = backend.peri.D
-    M = backend.params.M
+    kg = backend.slab_kgeo() if backend.peri.D in (0, 3) else None
+    slab_ok = kg is not None and kg["n"] % world == 0
     if kspace == "auto":
-        kspace = "slab" if (D == 3 and M % world == 0) else "replicated"
+        kspace = "slab" if slab_ok else "replicated"
     if kspace not in ("slab", "replicated"):
         raise ValueError(f"kspace must be 'auto', 'slab' or 'replicated', got {kspace!r}")
-    if kspace == "slab" and not (D == 3 and M % world == 0):
-        raise ValueError("the slab k-space stage needs D = 3 and M divisible by the rank count")
+    if kspace == "slab" and not slab_ok:
+        raise ValueError("the slab k-space stage needs D = 3 or 0 and its transform size (M, or nconv for D = 0) "
+                         "divisible by the rank count")
     if ks is not None:
         ks.wait_stream(cur)
     with side:
@@ -524,7 +539,7 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
                 work.wait()
             backend.kspace_apply(grid)
         else:
-            _slab_kspace_domain(backend, part, grid, rank, world, group, multi)
+            _slab_kspace_domain(backend, part, kg, grid, rank, world, group, multi)
         backend.gather_all(grid, opos, phik, accumulate=False)
     if ks is not None:
         cur.wait_stream(ks)
@@ -543,21 +558,21 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
     return out
 
 
-def _slab_kspace_domain(backend, part, grid, rank, world, group, multi):
-    """D = 3 k-space stage over x-slabs with a halo-restricted grid exchange:
-    each rank's touched x-planes go to the slab owners and are summed there
+def _slab_kspace_domain(backend, part, kg, grid, rank, world, group, multi):
+    """k-space stage over x-slabs (D = 3, or the D = 0 kernel path on its
+    zero-padded nconv^3 grid) with a halo-restricted grid exchange: each
+    rank's touched x-planes go to the slab owners and are summed there
     (instead of a reduce-scatter of the whole grid), the slab FFT runs with
     its two all-to-all transposes, and each rank receives back the filtered
     planes it touches (instead of an all-gather of the whole grid)."""
-    g = backend.grid_geometry()
-    M, P, h = g["M"], g["P"], g["h"]
+    planes = kg["planes"]
     plane = grid.shape[1] * grid.shape[2]
-    flat = grid.reshape(M, plane)
-    a, b = part.slab(rank, M)
+    flat = grid.reshape(planes, plane)
+    a, b = part.slab(rank, kg)
     # forward: my touched planes, grouped by the slab owner
     send_parts, send_counts = [], []
     for d in range(world):
-        pieces = part.exchange_pieces(rank, d, M, P, h)
+        pieces = part.exchange_pieces(rank, d, kg)
         send_parts += [flat[lo:hi] for lo, hi in pieces]
         send_counts.append(sum(hi - lo for lo, hi in pieces))
     send = torch.cat(send_parts) if send_parts else flat.new_zeros((0, plane))
@@ -565,7 +580,7 @@ def _slab_kspace_domain(backend, part, grid, rank, world, group, multi):
     slab = flat.new_zeros((b - a, plane))
     row = 0
     for s in range(world):
-        for lo, hi in part.exchange_pieces(s, rank, M, P, h):
+        for lo, hi in part.exchange_pieces(s, rank, kg):
             slab[lo - a:hi - a] += recv[row:row + hi - lo]
             row += hi - lo
     slab = slab.reshape((b - a,) + tuple(grid.shape[1:]))
@@ -582,13 +597,13 @@ def _slab_kspace_domain(backend, part, grid, rank, world, group, multi):
     # backward: the filtered planes each rank touches, from my slab
     parts2, counts2 = [], []
     for d in range(world):
-        pieces = part.exchange_pieces(d, rank, M, P, h)
+        pieces = part.exchange_pieces(d, rank, kg)
         parts2 += [sflat[lo - a:hi - a] for lo, hi in pieces]
         counts2.append(sum(hi - lo for lo, hi in pieces))
     send2 = torch.cat(parts2) if parts2 else flat.new_zeros((0, plane))
     recv2, _ = _all_to_allv(send2, counts2, group, multi)
     row = 0
     for s in range(world):
-        for lo, hi in part.exchange_pieces(rank, s, M, P, h):
+        for lo, hi in part.exchange_pieces(rank, s, kg):
             flat[lo:hi] = recv2[row:row + hi - lo]
             row += hi - lo

@@ -52,8 +52,10 @@ class DomainOracleBackend:
         from paper_1712_04732_b200.distributed import DomainPartition
         return DomainPartition(self.L, self.params, self.peri, world, n_total, self.g["shape"])
 
-    def grid_geometry(self):
-        return {"M": self.prm["M"], "P": self.prm["P"], "h": self.g["h"], "shape": tuple(self.g["shape"])}
+    def slab_kgeo(self):
+        n = self.prm["M"] if self.D == 3 else self.nconv
+        return {"planes": self.g["shape"][0], "n": n, "P": self.prm["P"], "h": self.g["h"],
+                "off": 0.0 if self.D >= 1 else 0.5 * self.prm["P"] * self.g["h"], "periodic": self.D >= 1}
 
     def empty_grid(self):
         return torch.empty(tuple(self.g["shape"]), dtype=torch.float64)
@@ -117,10 +119,14 @@ class DomainOracleBackend:
         out[n_own:] = (np.where(oh, f, 0.0).T @ qq)[n_own:]
         phi.copy_(torch.from_numpy(out))
 
-    # slab k-space stage (D = 3), numpy transforms in the library's layouts
+    # slab k-space stage (D = 3, and D = 0 on its zero-padded nconv^3 grid),
+    # numpy transforms in the library's layouts
+    def _n(self):
+        return self.prm["M"] if self.D == 3 else self.nconv
+
     def slab_geometry(self, world):
-        M = self.prm["M"]
-        return M // world, M // world, M // 2 + 1
+        n = self._n()
+        return n // world, n // world, n // 2 + 1
 
     def empty_spectrum(self, world):
         nx, nky, nkz = self.slab_geometry(world)
@@ -137,28 +143,42 @@ class DomainOracleBackend:
 
     def slab_forward(self, slab, world, send):
         nx, nky, nkz = self.slab_geometry(world)
-        A = np.fft.rfft2(slab.numpy(), axes=(1, 2))
+        n = self._n()
+        A = np.fft.rfft2(slab.numpy(), s=(n, n), axes=(1, 2))  # zero-padded for D = 0
         self._put(send, A.reshape(nx, world, nky, nkz).transpose(1, 0, 2, 3))
 
     def slab_xpass(self, recv, rank, world):
         nx, nky, nkz = self.slab_geometry(world)
-        M = self.prm["M"]
+        n = self._n()
         g, xi = self.g, self.prm["xi"]
-        k = self.orc.wavenumbers(M, g["h"])
-        wh = self.orc.window_fourier_checked(self.prm["window"], self.prm["shape"], 0.5 * g["P"] * g["h"], k)
+        orc = self.orc
+        w = 0.5 * g["P"] * g["h"]
         ky = slice(rank * nky, (rank + 1) * nky)
-        k2 = k[:, None, None] ** 2 + k[None, ky, None] ** 2 + k[None, None, :nkz] ** 2
-        inv = np.where(k2 > 0, 1.0 / np.where(k2 > 0, k2, 1.0), 0.0)
-        W = wh[:, None, None] * wh[None, ky, None] * wh[None, None, :nkz]
-        mult = self.orc.FOUR_PI * self.orc._mollify(k2, xi) * inv / W ** 2
-        C = self._get(recv).reshape(M, nky, nkz)
+        if self.D == 3:
+            k = orc.wavenumbers(n, g["h"])
+            wh = orc.window_fourier_checked(self.prm["window"], self.prm["shape"], w, k)
+            k2 = k[:, None, None] ** 2 + k[None, ky, None] ** 2 + k[None, None, :nkz] ** 2
+            inv = np.where(k2 > 0, 1.0 / np.where(k2 > 0, k2, 1.0), 0.0)
+            W = wh[:, None, None] * wh[None, ky, None] * wh[None, None, :nkz]
+            mult = orc.FOUR_PI * orc._mollify(k2, xi) * inv / W ** 2
+        else:
+            kf = orc.wavenumbers(n, g["h"])
+            kh = 2.0 * np.pi * np.fft.rfftfreq(n, d=g["h"])
+            af = orc._mollify(kf ** 2, xi) / orc.window_fourier_checked(self.prm["window"], self.prm["shape"], w,
+                                                                         kf) ** 2
+            ah = orc._mollify(kh ** 2, xi) / orc.window_fourier_checked(self.prm["window"], self.prm["shape"], w,
+                                                                         kh) ** 2
+            mult = (self.table[:, ky, :] * orc.FOUR_PI * af[:, None, None] * af[None, ky, None]
+                    * ah[None, None, :])
+        C = self._get(recv).reshape(n, nky, nkz)
         self._put(recv, np.fft.ifft(np.fft.fft(C, axis=0) * mult, axis=0).reshape(world, nx, nky, nkz))
 
     def slab_inverse(self, back, world, slab):
         nx, nky, nkz = self.slab_geometry(world)
-        M = self.prm["M"]
-        B = self._get(back).transpose(1, 0, 2, 3).reshape(nx, M, nkz)
-        slab.copy_(torch.from_numpy(np.fft.irfft2(B, s=(M, M), axes=(1, 2))))
+        n = self._n()
+        B = self._get(back).transpose(1, 0, 2, 3).reshape(nx, n, nkz)
+        out = np.fft.irfft2(B, s=(n, n), axes=(1, 2))
+        slab.copy_(torch.from_numpy(np.ascontiguousarray(out[:, :slab.shape[1], :slab.shape[2]])))
 
 
 def _case(D):
@@ -197,7 +217,7 @@ def _worker(rank, world, port, out_path, D, kspace):
 
 
 @pytest.mark.parametrize("world,D,kspace", [(2, 3, "slab"), (3, 3, "slab"), (2, 3, "replicated"),
-                                            (2, 0, "replicated")])
+                                            (2, 0, "replicated"), (2, 0, "slab"), (4, 0, "slab")])
 def test_domain_decomposition_gloo(tmp_path, world, D, kspace):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import se_oracle as orc
@@ -246,12 +266,20 @@ def test_partition_geometry():
                 want = [c for c in want if part.owner_of_col[c] != d]
                 assert halo == sorted(want)
             M, P, h = 128, 8, 10.0 / 128
-            if D != 3 or M % world:
-                continue  # the slab exchange is the D = 3, M % world == 0 path
+            kg = {"planes": M if D == 3 else M + P, "n": M if D == 3 else 240, "P": P, "h": h,
+                  "off": 0.0 if D == 3 else 0.5 * P * h, "periodic": D == 3}
+            if kg["n"] % world:
+                continue  # the slab exchange needs the transform size divisible by the ranks
             for r in range(world):
-                start, count = part.touched_planes(r, M, P, h)
-                got = sorted(p for d in range(world) for lo, hi in part.exchange_pieces(r, d, M, P, h)
+                touched = sorted(p for lo, hi in part.touched_pieces(r, kg) for p in range(lo, hi))
+                assert len(touched) == len(set(touched))
+                got = sorted(p for d in range(world) for lo, hi in part.exchange_pieces(r, d, kg)
                              for p in range(lo, hi))
-                assert got == sorted((start + i) % M for i in range(count))
+                assert got == touched
+                # the planes every particle of the slab touches are inside
+                x = np.linspace(part.col_lo[r] * part.edge, part.col_hi[r] * part.edge, 2001)[:-1]
+                f = np.floor((x + kg["off"]) / h - 0.5 * P).astype(int) + 1
+                need = {int(v) % M if D == 3 else int(v) for v in (f[:, None] + np.arange(P)).ravel()}
+                assert need <= set(touched)
     with pytest.raises(ValueError):
         DomainPartition(1.0, SimpleNamespace(rc=0.6, M=16, P=4), Periodicity(3), 2, 100)
