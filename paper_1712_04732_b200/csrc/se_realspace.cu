@@ -912,17 +912,20 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     a.zper = c.mode[2] == 1;
     int nbins = c.n * c.n;
     {
-        // z quantum L / 2^kb <= rc / 256: the windows' one-quantum slack and
-        // the index order inside a quantum cost nothing measurable.  The
-        // counting sort's fine bins (column, quantum) stay <= max(2^22, 4 N)
-        // (cfg2: 900 columns x 2^12 quanta; a coarser quantum only widens
-        // the windows' slack)
+        // z quantum L / 2^kb <= rc / 256 at least: the windows' one-quantum
+        // slack costs nothing measurable.  The counting sort's fine bins
+        // (column, quantum) stay <= max(2^22, 4 N) (cfg2: 900 columns x 2^12
+        // quanta; a coarser quantum would only widen the windows' slack)
         int cb = 1;
         while ((1LL << cb) < (long long)nbins) ++cb;
         int kz = 8;
         while (kz < 20 && (double)(1 << kz) < 256.0 * L / rc) ++kz;
-        a.kb = std::min(32 - cb, kz);
+        // as fine as the counting sort's bin budget allows (clustered inputs
+        // then keep ~1 particle per fine bin as well)
         const long long fine_cap = std::max<long long>(1LL << 22, 4LL * N);
+        a.kb = std::max(kz, 1);
+        while (a.kb < 20 && ((long long)nbins << (a.kb + 1)) <= fine_cap) ++a.kb;
+        a.kb = std::min(32 - cb, a.kb);
         while (a.kb > 1 && ((long long)nbins << a.kb) > fine_cap) --a.kb;
         a.qinv = (double)(1 << a.kb) / L;
     }

@@ -62,8 +62,8 @@ def test_domain_realspace_virtual_ranks(D, world):
     assert err < 1e-13
 
 
-@pytest.mark.parametrize("D", [3, 0])
-def test_domain_pipeline_one_rank_matches_fused(D):
+@pytest.mark.parametrize("D,kspace", [(3, "slab"), (3, "replicated"), (0, "slab"), (0, "replicated")])
+def test_domain_pipeline_one_rank_matches_fused(D, kspace):
     pos, q, L = _system(D, N=40000)
     prm = se.SEParams(xi=6.0, rc=0.4, M=32, P=8, window="bm", shape=20.0, s0=4.0, R=3.5)
     peri = se.Periodicity(D)
@@ -73,10 +73,10 @@ def test_domain_pipeline_one_rank_matches_fused(D):
     be = NativeBackend(L, prm, peri, dev)
     # a permuted input order: potentials come back in the caller's order
     perm = torch.randperm(len(q), generator=torch.Generator().manual_seed(3)).to(dev)
-    phi = total_potential_domain(pd[perm].contiguous(), qd[perm].contiguous(), be)
+    phi = total_potential_domain(pd[perm].contiguous(), qd[perm].contiguous(), be, kspace=kspace)
     ref = sedev.total_potential(pd, qd, L, prm, peri)[perm]
     err = se.relative_rms_error(phi.cpu().numpy(), ref.cpu().numpy())
-    print(f"D={D} one-rank domain pipeline vs fused: {err:.2e}")
+    print(f"D={D} {kspace}: one-rank domain pipeline vs fused: {err:.2e}")
     assert err < 1e-13
 
 
