@@ -474,13 +474,13 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
     if hasattr(backend, "check_system"):
         _agreed(lambda: backend.check_system(pos_local, q_local, neutrality=False), q_local, group, multi)
     # the neutrality check of the whole system (core.py:180-191) on the
-    # reduced charge sums
-    sums = torch.stack([q_local.sum(), q_local.abs().sum()]).to(torch.float64)
-    ntot = torch.tensor([n_in], dtype=torch.int64, device=dev)
+    # reduced charge sums, and the total particle count, in one all-reduce
+    sums = torch.stack([q_local.sum(), q_local.abs().sum(),
+                        torch.tensor(float(n_in), dtype=torch.float64, device=dev)])
     if multi:
         dist.all_reduce(sums, group=group)
-        dist.all_reduce(ntot, group=group)
-    qsum, qabs = float(sums[0]), float(sums[1])
+    qsum, qabs, n_all = sums.tolist()
+    ntot = torch.tensor([int(n_all)])
     if abs(qsum) > 1e-12 * max(qabs, 1.0):
         if backend.peri.D > 0:
             raise ValueError("periodic Ewald summation requires a charge-neutral system")
@@ -501,9 +501,15 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
     # 2. halo: each own particle to the ranks whose +x halo holds its column
     cx = part.columns(own[:, 0])
     halo_tab = torch.tensor(part.halo_to, dtype=torch.bool, device=dev)  # (ncols, world)
-    hsel = [torch.nonzero(halo_tab[cx, d], as_tuple=True)[0] for d in range(world)]
-    hidx = torch.cat(hsel) if hsel else torch.zeros(0, dtype=torch.int64, device=dev)
-    halo, halo_counts = _all_to_allv(own[hidx], [int(h.numel()) for h in hsel], group, multi)
+    # every (own particle, destination) halo pair, grouped by destination
+    # (a stable sort of the row-major nonzero list): one host sync for the
+    # pairs and one for the counts, whatever the rank count
+    pairs = torch.nonzero(halo_tab[cx], as_tuple=False)  # (k, 2): particle, rank
+    if pairs.shape[0]:
+        pairs = pairs[torch.argsort(pairs[:, 1], stable=True)]
+    hidx = pairs[:, 0]
+    hcounts = torch.bincount(pairs[:, 1], minlength=world).tolist() if pairs.shape[0] else [0] * world
+    halo, halo_counts = _all_to_allv(own[hidx], hcounts, group, multi)
     local = torch.cat([own, halo], dim=0)
     lpos = local[:, :3].contiguous()
     lq = local[:, 3].contiguous()
