@@ -874,7 +874,7 @@ static int dense_threshold() {
 static int real_unit(int64_t N) { return N < 50000 ? kT / 2 : kT; }
 
 // columns of edge >= rc/reach and the particle binning by (column, z)
-static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N, RealArgs &a) {
+static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N, RealArgs &a, bool full = false) {
     const double L = pl->L, rc = pl->p.rc;
     if (N >= (1LL << 27)) fail(SE_EINVAL, "real-space kernel supports N < 2^27 particles per call");
     CellGeom &c = pl->cell;
@@ -889,7 +889,7 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
         if (reach > kReachMax || nn > 1024)
             fail(SE_EINVAL, "domain column grid: columns must be at least rc / 3 wide and at most 1024 per axis");
     } else {
-        if (pl->deterministic) reach = 2;  // the full shell must fit one lane per column
+        if (full) reach = 2;  // the full shell must fit one lane per column
         for (;; --reach) {
             nn = (long long)std::floor(reach * L / rc);
             if (nn < 1) nn = 1;
@@ -953,6 +953,16 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     prof_end(pl, SE_K_SORT);
 }
 
+// The full shell without Newton's third law: in the deterministic mode
+// (no source-side atomics) and for the field, where the three source-side
+// fp64 atomics per pair cost more than evaluating every pair twice
+// (cfg2: 30.5 ms full shell against 33.9 ms with Newton, B200)
+// (the domain decomposition relies on the +x half shell: Newton there)
+template <bool FLD>
+static bool full_shell(const se_plan *pl) {
+    return pl->dom.ncols == 0 && (FLD || pl->deterministic);
+}
+
 template <bool COUNT, bool FLD = false>
 static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, unsigned long long *npairs) {
     const CellGeom &c = pl->cell;
@@ -965,7 +975,7 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
     const bool mi = c.mode[0] == 2 || c.mode[1] == 2 || c.mode[2] == 2;
     // deterministic mode: no Newton (no source-side atomics), each target
     // sums its own partners in a fixed order
-    const bool full = mi || pl->deterministic;
+    const bool full = mi || full_shell<FLD>(pl);
     unsigned blocks = (unsigned)((maxu + kWarps - 1) / kWarps);
     cudaStream_t st = pl->stream;
     const size_t smem = sizeof(WarpBufT<FLD>) * kWarps;
@@ -1043,7 +1053,7 @@ static void realspace_impl(se_plan *pl, const double *pos, const double *q, int6
         prof_end(pl, SE_K_REALSPACE);
         pl->launches += 1;
     } else {
-        cell_bin(pl, pos, q, N, a);
+        cell_bin(pl, pos, q, N, a, full_shell<FLD>(pl));
         launch_cell<false, FLD>(pl, N, a, phi, nullptr);
     }
 }
@@ -1105,7 +1115,7 @@ void realspace_pair_count(se_plan *pl, const double *pos, const double *q, int64
     SE_CUDA(cudaMemsetAsync(pl->flag.ptr, 0, sizeof(int) * 4, pl->stream));
     pl->pairs.ensure(sizeof(unsigned long long));
     SE_CUDA(cudaMemsetAsync(pl->pairs.ptr, 0, sizeof(unsigned long long), pl->stream));
-    cell_bin(pl, pos, q, N, a);
+    cell_bin(pl, pos, q, N, a, full_shell<false>(pl));
     launch_cell<true>(pl, N, a, nullptr, pl->pairs.as<unsigned long long>());
     unsigned long long h = 0;
     SE_CUDA(cudaMemcpyAsync(&h, pl->pairs.ptr, sizeof(h), cudaMemcpyDeviceToHost, pl->stream));
