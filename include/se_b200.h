@@ -238,19 +238,22 @@ int se_realspace_shard_dev(se_plan_t plan, const double *pos, const double *q, i
 int se_realspace_domain_dev(se_plan_t plan, const double *pos, const double *q, int64_t n_local, int64_t n_own,
                             int ncols, int col_lo, int col_hi, double *phi, int add_self);
 
-/* Electric field E = -grad phi at every particle, D = 3 (forces F = q E; the
+/* Electric field E = -grad phi at every particle (forces F = q E; the
  * reference stops at potentials: SPEC.md:16 notes the force integration "has
  * to be performed three times").  E is (N, 3) in caller
  * order: the real-space pair field q_s (erfc(xi r)/r + 2 xi/sqrt(pi)
  * exp(-xi^2 r^2)) (x_t - x_s)/r^2 over the same pair set as
- * real_space_sum, plus the Fourier field gathered from the spectrally
- * differentiated grid (-i k times the scaled spectrum, one inverse transform
- * and one gather per component).  No self term (the self-interaction is a
- * constant).  Errors as se_total_potential_*. */
+ * real_space_sum, plus the Fourier field: D = 3 gathered from the
+ * spectrally differentiated grid (-i k times the scaled spectrum, one
+ * inverse transform and one gather per component); D < 3 the gradient of
+ * the gather on the filtered grid of the potential (window derivative;
+ * SE_EINVAL for the ES window, whose derivative is singular at the support
+ * edge).  No self term (the self-interaction is a constant).  Errors as
+ * se_total_potential_*. */
 int se_total_field_dev(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E);
 int se_total_field_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E);
 /* The two parts separately (host pointers): the real-space pair field (any
- * D; the same pair set as real_space_sum) and the Fourier field (D = 3). */
+ * D; the same pair set as real_space_sum) and the Fourier field. */
 int se_realspace_field_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E);
 int se_kspace_field_host(se_plan_t plan, const double *pos, const double *q, int64_t N, double *E);
 

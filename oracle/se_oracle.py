@@ -700,6 +700,65 @@ def kspace_field_d3(pos, q, L, prm, targets=None):
     return out
 
 
+def window_deriv(kind, shape, w, x):
+    """d/dx of window_eval (windows.py:74-84, 106-112): Gaussian
+    -m^2 x / w^2 w(x); Kaiser-Bessel -beta I1(beta s) r / (w s I0(beta)),
+    s = sqrt(1 - r^2), r = x / w (finite at the edge).  Not for the ES
+    window (singular derivative at the support edge)."""
+    from scipy.special import i1 as _i1
+
+    x = np.asarray(x, dtype=float)
+    inside = np.abs(x) <= w
+    if kind == "gaussian":
+        v = -(shape * shape) * x / (w * w) * window_eval(kind, shape, w, x)
+    elif kind == "kb":
+        r = x / w
+        sq = np.sqrt(np.clip(1.0 - r * r, 0.0, None))
+        i1s = np.where(sq > 1e-8, _i1(shape * sq) / np.where(sq > 1e-8, sq, 1.0), 0.5 * shape)
+        v = -shape * i1s * r / w / _i0(shape)
+    else:
+        raise ValueError("the window-gradient field needs the Gaussian or Kaiser-Bessel window")
+    return np.where(inside, v, 0.0)
+
+
+def kspace_field_grad(pos, q, L, D, prm, targets=None, use_kernel=None):
+    """E_F = -grad phi_F for any D by the gradient of the gather: the filtered
+    grid H~ of se_kspace (sekspace.py:340-381) and
+    E_a(x) = h^3 sum_g H~[g] w'(delta_a) prod_{b != a} w(delta_b),
+    delta = g h - (x + offset) (the derivative of gather, sekspace.py:159-178,
+    with respect to the particle position)."""
+    g = geometry(L, D, prm["M"], prm["P"], prm.get("s0", 1.0), prm.get("s", 1.0), prm.get("R", 0.0))
+    kind, shape, xi = prm["window"], prm["shape"], prm["xi"]
+    H = spread(pos, q, g, kind, shape)
+    if D == 3:
+        Ht = kspace_d3(H, g, xi, kind, shape)
+    elif D == 0 and (use_kernel or use_kernel is None):
+        tab, kg = d0_kernel_table(L, prm["M"], prm["P"], prm["s0"], prm["rc"])
+        Ht = kspace_d0_kernel(H, g, xi, kind, shape, tab, kg["nconv"])
+    else:
+        Ht = kspace_mixed(H, g, xi, kind, shape, prm["nI"])
+    tpos = pos if targets is None else pos[np.asarray(targets)]
+    P, h = g["P"], g["h"]
+    w = 0.5 * P * h
+    t = np.arange(P)
+    idx, wv, dv = [], [], []
+    for a in range(3):
+        u = tpos[:, a] + g["offsets"][a]
+        first = np.floor(u / h - 0.5 * P).astype(np.int64) + 1
+        ia = first[:, None] + t[None, :]
+        d = ia * h - u[:, None]
+        if a < D:
+            ia = np.mod(ia, g["M"])
+        idx.append(ia)
+        wv.append(window_eval(kind, shape, w, d))
+        dv.append(window_deriv(kind, shape, w, d))
+    v = Ht[idx[0][:, :, None, None], idx[1][:, None, :, None], idx[2][:, None, None, :]]
+    ex = np.einsum("npqr,np,nq,nr->n", v, dv[0], wv[1], wv[2])
+    ey = np.einsum("npqr,np,nq,nr->n", v, wv[0], dv[1], wv[2])
+    ez = np.einsum("npqr,np,nq,nr->n", v, wv[0], wv[1], dv[2])
+    return np.stack([ex, ey, ez], axis=1) * h ** 3
+
+
 def total_field(pos, q, L, prm):
     """E = E_R + E_F (D = 3)."""
     return realspace_field(pos, q, L, 3, prm["xi"], prm["rc"]) + kspace_field_d3(pos, q, L, prm)

@@ -681,8 +681,22 @@ __global__ void field_combine_kernel(const double *__restrict__ ek, int64_t N, d
 // differentiated inverse transforms -> three gathers; E = E_F (accumulate
 // 0) or E += E_F.
 void kspace_field_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *E, int accumulate) {
-    if (pl->D != 3) fail(SE_EINVAL, "the electric field (forces) covers D = 3");
     if (N <= 0) return;
+    if (pl->D != 3) {
+        // D < 3: the potential's k-space stage (AFT or the D = 0 kernel path),
+        // then the gradient of the gather (window derivative; Gaussian / KB)
+        if (pl->p.window == SE_WINDOW_BM)
+            fail(SE_EINVAL, "forces for D < 3 need the Gaussian or Kaiser-Bessel window (the ES window's "
+                            "derivative is singular at its support edge)");
+        pl->grid_dev.ensure(sizeof(double) * grid_points(pl));
+        double *grid = pl->grid_dev.as<double>();
+        spread_run(pl, pos, q, N, grid, 0, 1);
+        prof_begin(pl, SE_K_KSPACE);
+        kspace_run(pl, grid, 1, nullptr);
+        prof_end(pl, SE_K_KSPACE);
+        grad_gather_run(pl, grid, pos, N, E, accumulate);
+        return;
+    }
     const size_t G = grid_points(pl);
     pl->grid_dev.ensure(sizeof(double) * G);
     pl->fgrid.ensure(sizeof(double) * 3 * G);
@@ -701,7 +715,6 @@ void kspace_field_pipeline(se_plan *pl, const double *pos, const double *q, int6
 }
 
 void field_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *E) {
-    if (pl->D != 3) fail(SE_EINVAL, "the electric field (forces) covers D = 3");
     check_system(pl, pos, q, N, true);
     realspace_field_run(pl, pos, q, N, E, 0, 1);
     kspace_field_pipeline(pl, pos, q, N, E, 1);

@@ -260,6 +260,7 @@ void gather_run(se_plan *pl, const double *grid, const double *pos, int64_t N, d
 void kspace_run(se_plan *pl, double *grid, int use_kernel, double *timings);
 void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi,
                    int add_self, int rank, int world);
+void grad_gather_run(se_plan *pl, const double *grid, const double *pos, int64_t N, double *E, int accumulate);
 void realspace_domain_run(se_plan *pl, const double *pos, const double *q, int64_t n_local, int64_t n_own, int ncols,
                           int col_lo, int col_hi, double *phi, int add_self);
 void realspace_field_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *E,

@@ -782,4 +782,113 @@ void gather_run(se_plan *pl, const double *grid, const double *pos, int64_t N, d
     pl->launches += 1;
 }
 
+// ------------------------------------------- gradient gather (E = -grad phi_F)
+// Derivative of the window (windows.py:74-84, 106-112): Gaussian
+// w' = 2 gcoef x w; Kaiser-Bessel w' = -beta I1(beta s) r / (w s I0(beta)),
+// s = sqrt(1 - r^2), r = x / w (I1(beta s) / s -> beta / 2 at the support
+// edge: finite).  The ES window's derivative is singular at the edge and
+// is not used here (the D = 3 field differentiates spectrally instead).
+template <int WIN>
+__device__ __forceinline__ double window_deriv(double x, const SpreadArgs &a) {
+    if (!(fabs(x) <= a.w)) return 0.0;
+    if (WIN == SE_WINDOW_GAUSSIAN) return 2.0 * a.gcoef * x * (a.peak * exp_nonpos(a.gcoef * (x * x)));
+    const double r = x * a.invw;
+    double t = fma(-r, r, 1.0);
+    t = t < 0.0 ? 0.0 : t;
+    const double sq = sqrt(t), z = a.shapep * sq;
+    const double i1_over_s = sq > 1e-8 ? cyl_bessel_i1(z) / sq : 0.5 * a.shapep;
+    return -a.shapep * i1_over_s * r * a.invw / a.i0b;
+}
+
+// One warp per particle (sorted by tile, so that neighbouring warps share
+// grid lines in L2): E_a = h^3 sum_g H[g] w'(delta_a) prod_{b != a} w(delta_b)
+// with delta = g h - (x + offset) -- the gradient of sekspace.gather's
+// h^3 sum H w w w (sekspace.py:159-178) with respect to the particle position.
+template <int WIN>
+__global__ void __launch_bounds__(128) grad_gather_kernel(const double4 *__restrict__ rec, const int *__restrict__ sidx,
+                                                         int64_t N, SpreadArgs a, const double *__restrict__ grid,
+                                                         double *__restrict__ E, double h3, int accumulate) {
+    extern __shared__ double gsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int P = a.P;
+    double *w = gsm + warp * 6 * P;                      // w[axis][t], then dw[axis][t]
+    int *gi = reinterpret_cast<int *>(gsm + nw * 6 * P) + warp * 3 * P;  // grid index per axis and t (-1: off)
+    for (int64_t p = blockIdx.x * (int64_t)nw + warp; p < N; p += (int64_t)gridDim.x * nw) {
+        const double4 r = rec[p];
+        for (int task = lane; task < 3 * P; task += 32) {
+            const int ax = task / P, t = task - ax * P;
+            const double x = ax == 0 ? r.x : (ax == 1 ? r.y : r.z);
+            const double u = __dadd_rn(x, a.off[ax]);
+            const long long f = stencil_first(u, a) + t;
+            const double d = __dsub_rn(__dmul_rn((double)f, a.h), u);  // sekspace.py:116
+            w[ax * P + t] = window_eval<WIN>(d, a);
+            w[(3 + ax) * P + t] = window_deriv<WIN>(d, a);
+            long long g = f;
+            if (ax < a.D) {
+                g %= a.M;
+                if (g < 0) g += a.M;
+            } else if (g < 0 || g >= a.Mt) {
+                g = -1;
+            }
+            gi[ax * P + t] = (int)g;
+        }
+        __syncwarp();
+        double ex = 0.0, ey = 0.0, ez = 0.0;
+        for (int pi = lane; pi < P * P; pi += 32) {
+            const int ty = pi / P, tz = pi - ty * P;
+            const int gy = gi[P + ty], gz = gi[2 * P + tz];
+            if (gy < 0 || gz < 0) continue;
+            double s = 0.0, sd = 0.0;
+            for (int t = 0; t < P; ++t) {
+                const int gx = gi[t];
+                if (gx < 0) continue;
+                const double c = grid[((int64_t)gx * a.shape[1] + gy) * a.shape[2] + gz];
+                s = fma(w[t], c, s);
+                sd = fma(w[3 * P + t], c, sd);
+            }
+            const double wy = w[P + ty], wz = w[2 * P + tz];
+            ex = fma(wy * wz, sd, ex);
+            ey = fma(w[4 * P + ty] * wz, s, ey);
+            ez = fma(wy * w[5 * P + tz], s, ez);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ex += __shfl_xor_sync(0xffffffffu, ex, o);
+            ey += __shfl_xor_sync(0xffffffffu, ey, o);
+            ez += __shfl_xor_sync(0xffffffffu, ez, o);
+        }
+        if (lane == 0) {
+            double *o = E + 3 * (int64_t)sidx[p];
+            o[0] = accumulate ? o[0] + h3 * ex : h3 * ex;
+            o[1] = accumulate ? o[1] + h3 * ey : h3 * ey;
+            o[2] = accumulate ? o[2] + h3 * ez : h3 * ez;
+        }
+        __syncwarp();
+    }
+}
+
+void grad_gather_run(se_plan *pl, const double *grid, const double *pos, int64_t N, double *E, int accumulate) {
+    if (N <= 0) return;
+    if (pl->p.window == SE_WINDOW_BM)
+        fail(SE_EINVAL, "the window-gradient field needs the Gaussian or Kaiser-Bessel window (the ES window's "
+                        "derivative is singular at its support edge)");
+    bin_tiles(pl, pos, nullptr, N);
+    SpreadArgs a = make_args(pl);
+    const double h3 = pl->g.h * pl->g.h * pl->g.h;
+    const int wpb = 4;
+    const size_t sm = (sizeof(double) * 6 + sizeof(int) * 3) * (size_t)pl->p.P * wpb;
+    int64_t blocks = (N + wpb - 1) / wpb;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    prof_begin(pl, SE_K_GATHER);
+    dispatch_window(pl->p.window, [&](auto W) {
+        auto kern = grad_gather_kernel<decltype(W)::value>;
+        SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        kern<<<(unsigned)blocks, 32 * wpb, sm, pl->stream>>>(pl->tbin.rec.as<double4>(), pl->tbin.idx_sorted.as<int>(),
+                                                             N, a, grid, E, h3, accumulate);
+    });
+    SE_LAUNCH_CHECK();
+    prof_end(pl, SE_K_GATHER);
+    pl->launches += 1;
+}
+
 }  // namespace se

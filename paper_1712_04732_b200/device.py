@@ -49,12 +49,13 @@ def total_potential(positions: torch.Tensor, charges: torch.Tensor, L: float, pa
 
 def total_field(positions: torch.Tensor, charges: torch.Tensor, L: float, params: SEParams,
                 periodicity: Periodicity, out: torch.Tensor | None = None) -> torch.Tensor:
-    """core.total_field on device tensors: E (N, 3), D = 3."""
+    """core.total_field on device tensors: E (N, 3)."""
     N = charges.shape[0]
     _check(positions, (N, 3), "positions")
     _check(charges, (N,), "charges")
-    if periodicity.D != 3:
-        raise ValueError("the electric field (forces) covers D = 3")
+    if periodicity.D != 3 and params.window == "bm":
+        raise ValueError("forces for D < 3 need the Gaussian or Kaiser-Bessel window (the ES window's "
+                         "derivative is singular at its support edge)")
     params.validate(L, periodicity)
     pl = plan(L, params, periodicity, positions.device)
     if out is None:

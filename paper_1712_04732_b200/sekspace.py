@@ -252,12 +252,15 @@ def se_kspace(system: ParticleSystem, params: SEParams, periodicity: Periodicity
 
 def se_kspace_field(system: ParticleSystem, params: SEParams, periodicity: Periodicity,
                     threads: int = 1) -> np.ndarray:
-    """Fourier part of E = -grad phi at every source, (N, 3), D = 3: the
+    """Fourier part of E = -grad phi at every source, (N, 3).  D = 3: the
     scaled spectrum of se_kspace times -i k per axis, three inverse
-    transforms and three gathers.  Beyond the reference (forces, SURVEY 8f
-    item 4)."""
-    if periodicity.D != 3:
-        raise ValueError("the electric field (forces) covers D = 3")
+    transforms and three gathers; D < 3: the filtered grid of se_kspace and
+    the gradient of the gather, h^3 sum H w'(delta_a) prod_{b != a} w(delta_b)
+    (Gaussian / Kaiser-Bessel windows).  Beyond the reference (forces,
+    SURVEY 8f item 4)."""
+    if periodicity.D != 3 and params.window == "bm":
+        raise ValueError("forces for D < 3 need the Gaussian or Kaiser-Bessel window (the ES window's "
+                         "derivative is singular at its support edge)")
     params.validate(system.L, periodicity)
     plan = _native.plan_for(periodicity.D, system.L, params)
     E = np.empty((system.N, 3))

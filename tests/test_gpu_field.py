@@ -176,3 +176,50 @@ def test_field_empty_and_zero_charge_systems():
     Er = se.realspace.real_space_field(se.ParticleSystem(np.zeros((0, 3)), np.zeros(0), 1.0), 8.0, 0.4,
                                        se.Periodicity(1))
     assert Er.shape == (0, 3)
+
+
+G3 = np.load(os.path.join(ROOT, "tests", "golden", "field_dlt3.npz"))
+
+
+@pytest.mark.parametrize("D", [2, 1, 0])
+@pytest.mark.parametrize("window", ["gaussian", "kb"])
+def test_field_dlt3_matches_oracle(D, window):
+    # D < 3: real-space pair field + the gradient of the gather on the
+    # filtered grid (window derivative), device vs oracle restatement
+    pos, q = _system(3000, 1.5, 70 + D)
+    shape = np.sqrt(8 * np.pi) if window == "gaussian" else 2.3 * 8
+    p = se.SEParams(xi=7.0, rc=0.5, M=24, P=8, window=window, shape=shape, s0=3.0, s=2.0, nI=4, R=2.5,
+                    eps=1e-8)
+    s = se.ParticleSystem(pos, q, 1.5)
+    E = se.total_field(s, p, se.Periodicity(D))
+    prm = dict(xi=p.xi, rc=p.rc, M=p.M, P=p.P, window=p.window, shape=p.shape, s0=p.s0, s=p.s, nI=p.nI, R=p.R)
+    ref = orc.realspace_field(pos, q, 1.5, D, p.xi, p.rc) + orc.kspace_field_grad(pos, q, 1.5, D, prm)
+    err = _rel(E, ref)
+    Ek = se.sekspace.se_kspace_field(s, p, se.Periodicity(D))
+    errk = _rel(Ek, orc.kspace_field_grad(pos, q, 1.5, D, prm))
+    print(f"D={D} {window}: total {err:.2e} k-space {errk:.2e}")
+    assert err < 1e-12 and errk < 1e-12
+
+
+@pytest.mark.parametrize("D", [2, 1, 0])
+def test_field_dlt3_vs_reference_differences(D):
+    # tight parameters: the device field against central differences of the
+    # reference's own real_space_sum and direct Fourier-space sums
+    L, xi, rc, kmax, delta = G3[f"D{D}_prm"]
+    pos, q = G3[f"D{D}_pos"], G3[f"D{D}_q"]
+    s = se.ParticleSystem(pos, q, L)
+    p, _ = se.auto_params(s, se.Periodicity(D), xi, 1e-13, window="gaussian")
+    pr = se.SEParams(xi=p.xi, rc=rc, M=p.M, P=p.P, window=p.window, shape=p.shape, s0=p.s0, s=p.s, nI=p.nI,
+                     R=p.R, eps=p.eps)
+    E = se.total_field(s, pr, se.Periodicity(D))
+    ref = G3[f"D{D}_E_real_fd"] + G3[f"D{D}_E_kspace_direct_fd"]
+    err = _rel(E, ref)
+    print(f"D={D}: device field vs reference differences {err:.2e}")
+    assert err < 1e-6
+
+
+def test_field_dlt3_rejects_es_window():
+    pos, q = _system(500, 1.0, 3)
+    p = se.SEParams(xi=7.0, rc=0.45, M=20, P=8, window="bm", shape=20.0, s0=3.0, s=2.0, nI=4, R=2.0)
+    with pytest.raises(ValueError):
+        se.total_field(se.ParticleSystem(pos, q, 1.0), p, se.Periodicity(2))
