@@ -490,31 +490,38 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
     part = backend.domain_partition(world, int(ntot.item()))
     cols_of = torch.tensor(part.owner_of_col, dtype=torch.int64, device=dev)
 
-    # 1. migrate to the owners
-    rec = torch.cat([pos_local, q_local[:, None]], dim=1)
-    dest = cols_of[part.columns(pos_local[:, 0])]
-    order = torch.argsort(dest, stable=True)
-    send_counts = torch.bincount(dest, minlength=world).tolist()
-    own, own_counts = _all_to_allv(rec[order], send_counts, group, multi)
-    n_own = int(own.shape[0])
+    if multi:
+        # 1. migrate to the owners
+        rec = torch.cat([pos_local, q_local[:, None]], dim=1)
+        dest = cols_of[part.columns(pos_local[:, 0])]
+        order = torch.argsort(dest, stable=True)
+        send_counts = torch.bincount(dest, minlength=world).tolist()
+        own, own_counts = _all_to_allv(rec[order], send_counts, group, multi)
+        n_own = int(own.shape[0])
 
-    # 2. halo: each own particle to the ranks whose +x halo holds its column
-    cx = part.columns(own[:, 0])
-    halo_tab = torch.tensor(part.halo_to, dtype=torch.bool, device=dev)  # (ncols, world)
-    # every (own particle, destination) halo pair, grouped by destination
-    # (a stable sort of the row-major nonzero list): one host sync for the
-    # pairs and one for the counts, whatever the rank count
-    pairs = torch.nonzero(halo_tab[cx], as_tuple=False)  # (k, 2): particle, rank
-    if pairs.shape[0]:
-        pairs = pairs[torch.argsort(pairs[:, 1], stable=True)]
-    hidx = pairs[:, 0]
-    hcounts = torch.bincount(pairs[:, 1], minlength=world).tolist() if pairs.shape[0] else [0] * world
-    halo, halo_counts = _all_to_allv(own[hidx], hcounts, group, multi)
-    local = torch.cat([own, halo], dim=0)
-    lpos = local[:, :3].contiguous()
-    lq = local[:, 3].contiguous()
-    opos = own[:, :3].contiguous()
-    oq = own[:, 3].contiguous()
+        # 2. halo: each own particle to the ranks whose +x halo holds its column
+        cx = part.columns(own[:, 0])
+        halo_tab = torch.tensor(part.halo_to, dtype=torch.bool, device=dev)  # (ncols, world)
+        # every (own particle, destination) halo pair, grouped by destination
+        # (a stable sort of the row-major nonzero list): one host sync for the
+        # pairs and one for the counts, whatever the rank count
+        pairs = torch.nonzero(halo_tab[cx], as_tuple=False)  # (k, 2): particle, rank
+        if pairs.shape[0]:
+            pairs = pairs[torch.argsort(pairs[:, 1], stable=True)]
+        hidx = pairs[:, 0]
+        hcounts = torch.bincount(pairs[:, 1], minlength=world).tolist() if pairs.shape[0] else [0] * world
+        halo, halo_counts = _all_to_allv(own[hidx], hcounts, group, multi)
+        local = torch.cat([own, halo], dim=0)
+        lpos = local[:, :3].contiguous()
+        lq = local[:, 3].contiguous()
+        opos = own[:, :3].contiguous()
+        oq = own[:, 3].contiguous()
+    else:
+        # one rank: every particle is its own, no halo, no exchange
+        n_own = n_in
+        lpos = opos = pos_local.contiguous()
+        lq = oq = q_local.contiguous()
+        hidx = None
 
     # 3. + 5. the k-space chain on the side stream, real space on this one
     ks = getattr(backend, "kstream", None)
@@ -549,6 +556,11 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
         backend.gather_all(grid, opos, phik, accumulate=False)
     if ks is not None:
         cur.wait_stream(ks)
+
+    if not multi:
+        phi_local += phik
+        _finish(backend, phi_local, group, multi)
+        return phi_local
 
     # 4. the halo sums back to the owners (the order of step 2)
     back, _ = _all_to_allv(phi_local[n_own:].contiguous(), halo_counts, group, multi)
