@@ -290,6 +290,22 @@ def set_deterministic(on: bool = True):
     clear_plans()
 
 
+def host_out(shape):
+    """A fresh float64 output array for a _host entry point, in page-locked
+    memory when CUDA is up: the device-to-host copy then runs at full link
+    speed without the driver's pageable staging and without first-touch page
+    faults on a new array (~0.5 ms for 8 MB).  The array owns its memory
+    like any numpy array (torch's caching host allocator takes the block back
+    when it is collected)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    except Exception:  # noqa: BLE001 -- fall back to pageable memory
+        pass
+    return np.empty(shape)
+
+
 def timings_buffer():
     return np.zeros(len(TIMING_KEYS))
 

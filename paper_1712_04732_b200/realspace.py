@@ -60,7 +60,7 @@ def real_space_sum(system: ParticleSystem, xi: float, rc: float, periodicity: Pe
     if xi <= 0 or rc <= 0:
         raise ValueError("xi and rc must be positive")
     plan = _native.plan_for(periodicity.D, system.L, _real_params(xi, rc))
-    phi = np.empty(system.N)
+    phi = _native.host_out(system.N)
     _native.call("se_realspace_host", plan.handle, _native.ptr(system.positions),
                  _native.ptr(system.charges), system.N, _native.ptr(phi), 0)
     return phi
@@ -74,7 +74,7 @@ def real_space_field(system: ParticleSystem, xi: float, rc: float, periodicity: 
     if xi <= 0 or rc <= 0:
         raise ValueError("xi and rc must be positive")
     plan = _native.plan_for(periodicity.D, system.L, _real_params(xi, rc))
-    E = np.empty((system.N, 3))
+    E = _native.host_out((system.N, 3))
     _native.call("se_realspace_field_host", plan.handle, _native.ptr(system.positions),
                  _native.ptr(system.charges), system.N, _native.ptr(E))
     return E

@@ -138,7 +138,7 @@ def gather(field: GridField, system: ParticleSystem, wspec: windows.WindowSpec,
     H = np.ascontiguousarray(field.values, dtype=np.float64)
     if H.shape != grid.shape:
         raise ValueError("grid values do not match the grid shape")
-    phi = np.empty(system.N)
+    phi = _native.host_out(system.N)
     _native.call("se_gather_host", plan.handle, _native.ptr(H), _native.ptr(system.positions),
                  system.N, _native.ptr(phi))
     return phi
@@ -239,7 +239,7 @@ def se_kspace(system: ParticleSystem, params: SEParams, periodicity: Periodicity
     params.validate(system.L, periodicity)
     plan = _native.plan_for(periodicity.D, system.L, params)
     uk = 1 if (periodicity.D == 0 and (use_kernel or use_kernel is None)) else 0
-    phi = np.empty(system.N)
+    phi = _native.host_out(system.N)
     tb = _native.timings_buffer() if timings is not None else None
     _native.call("se_kspace_potential_host", plan.handle, _native.ptr(system.positions),
                  _native.ptr(system.charges), system.N, _native.ptr(phi), uk,
@@ -263,7 +263,7 @@ def se_kspace_field(system: ParticleSystem, params: SEParams, periodicity: Perio
                          "derivative is singular at its support edge)")
     params.validate(system.L, periodicity)
     plan = _native.plan_for(periodicity.D, system.L, params)
-    E = np.empty((system.N, 3))
+    E = _native.host_out((system.N, 3))
     _native.call("se_kspace_field_host", plan.handle, _native.ptr(system.positions),
                  _native.ptr(system.charges), system.N, _native.ptr(E))
     return E
