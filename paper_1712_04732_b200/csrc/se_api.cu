@@ -362,7 +362,7 @@ void plan_release_device(se_plan *pl) {
         if (h) cufftDestroy(h);
     for (Binning *b : {&pl->tbin, &pl->cbin})
         for (DevBuf *d : {&b->keys, &b->keys_sorted, &b->idx, &b->idx_sorted, &b->counts, &b->starts, &b->units,
-                          &b->nunits, &b->ubstart, &b->fhist, &b->fstart, &b->bsum, &b->rec})
+                          &b->nunits, &b->ubstart, &b->fhist, &b->fstart, &b->bsum, &b->large, &b->nlarge, &b->rec})
             d->release();
     for (ModeTable *t : {&pl->tM, &pl->tg0, &pl->tgs, &pl->tMt, &pl->tNc, &pl->tNh}) {
         t->k.release();

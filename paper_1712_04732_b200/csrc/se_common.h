@@ -102,6 +102,7 @@ struct Binning {
     int64_t capacity = 0;
     DevBuf keys, keys_sorted, idx, idx_sorted, counts, starts, units, nunits, ubstart;
     DevBuf fhist, fstart, bsum;  // counting sort: fine-bin histogram / starts, scan block sums
+    DevBuf large, nlarge;        // counting sort: fine bins too large for the per-thread insertion sort
     DevBuf rec;  // sorted particle records (x, y, z, q) as double4
     int fine_shift = 0;          // index bits refining a coarse key
     int64_t nfine = 0;           // fine bins

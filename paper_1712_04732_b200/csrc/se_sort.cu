@@ -117,11 +117,20 @@ __global__ void scatter_kernel(const unsigned *__restrict__ fkey, const int *__r
     idx_sorted[fstart[fkey[i]] + rank[i]] = (int)i;
 }
 
-// the entries of each fine bin in index order (bins hold a few particles)
-__global__ void bin_order_kernel(const int *__restrict__ fstart, int64_t nfine, int64_t n, int *__restrict__ idx) {
+// the entries of each fine bin in index order: an insertion sort per bin
+// (bins hold a few particles); bins above kSmallBin entries (coincident z
+// layers, extreme clusters) go to a list for bin_order_large_kernel
+constexpr int kSmallBin = 48, kLargeBin = 12288;
+__global__ void bin_order_kernel(const int *__restrict__ fstart, int64_t nfine, int64_t n, int *__restrict__ idx,
+                                 int *__restrict__ large, int *__restrict__ nlarge, int cap) {
     int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (b >= nfine) return;
     const int s = fstart[b], e = b + 1 < nfine ? fstart[b + 1] : (int)n;
+    if (e - s > kSmallBin) {
+        const int k = atomicAdd(nlarge, 1);
+        if (k < cap) large[k] = (int)b;
+        return;
+    }
     for (int i = s + 1; i < e; ++i) {
         const int v = idx[i];
         int j = i - 1;
@@ -130,6 +139,32 @@ __global__ void bin_order_kernel(const int *__restrict__ fstart, int64_t nfine, 
             --j;
         }
         idx[j + 1] = v;
+    }
+}
+
+// One CTA per large fine bin: each entry's rank = the number of entries with
+// a smaller particle index (the bin in shared memory), written back in
+// index order.  Bins beyond kLargeBin entries keep the atomic arrival order
+// (correct, not bitwise reproducible); the real-space and spreading work of
+// such a bin is quadratic in its size anyway.
+__global__ void __launch_bounds__(1024) bin_order_large_kernel(const int *__restrict__ fstart, int64_t nfine, int64_t n,
+                                                               int *__restrict__ idx, const int *__restrict__ large,
+                                                               const int *__restrict__ nlarge, int cap) {
+    __shared__ int v[kLargeBin];
+    const int nl = min(*nlarge, cap);
+    for (int l = blockIdx.x; l < nl; l += gridDim.x) {
+        const int64_t b = large[l];
+        const int s = fstart[b], e = b + 1 < nfine ? fstart[b + 1] : (int)n, k = e - s;
+        if (k > kLargeBin) continue;
+        __syncthreads();
+        for (int i = threadIdx.x; i < k; i += blockDim.x) v[i] = idx[s + i];
+        __syncthreads();
+        for (int i = threadIdx.x; i < k; i += blockDim.x) {
+            const int x = v[i];
+            int r = 0;
+            for (int j = 0; j < k; ++j) r += v[j] < x;
+            idx[s + r] = x;
+        }
     }
 }
 
@@ -241,6 +276,8 @@ void binning_reserve(se_plan *pl, Binning &b, int64_t N, int nbins, int chunk, i
     b.fhist.ensure(sizeof(int) * nfine);
     b.fstart.ensure(sizeof(int) * nfine);
     b.bsum.ensure(sizeof(int) * ((nfine + kScanTile - 1) / kScanTile + 1));
+    b.large.ensure(sizeof(int) * (cap / (kSmallBin + 1) + 1));
+    b.nlarge.ensure(sizeof(int));
     b.nbins = nbins;
     (void)pl;
 }
@@ -265,10 +302,15 @@ void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, i
                                                        b.fstart.as<int>());
         scatter_kernel<<<nb, 256, 0, st>>>(b.keys_sorted.as<unsigned>(), b.idx.as<int>(), N, b.fstart.as<int>(),
                                            b.idx_sorted.as<int>());
-        bin_order_kernel<<<fb, 256, 0, st>>>(b.fstart.as<int>(), nfine, N, b.idx_sorted.as<int>());
+        SE_CUDA(cudaMemsetAsync(b.nlarge.ptr, 0, sizeof(int), st));
+        const int cap = (int)std::min<int64_t>(N / (kSmallBin + 1) + 1, 1 << 20);
+        bin_order_kernel<<<fb, 256, 0, st>>>(b.fstart.as<int>(), nfine, N, b.idx_sorted.as<int>(), b.large.as<int>(),
+                                             b.nlarge.as<int>(), cap);
+        bin_order_large_kernel<<<148, 1024, 0, st>>>(b.fstart.as<int>(), nfine, N, b.idx_sorted.as<int>(),
+                                                     b.large.as<int>(), b.nlarge.as<int>(), cap);
         gather_records_kernel<<<nb, 256, 0, st>>>(pos, q, b.idx_sorted.as<int>(), b.rec.as<double4>(), N);
         SE_LAUNCH_CHECK();
-        pl->launches += 7;
+        pl->launches += 8;
     }
     build_units_kernel<<<1, 1024, 0, st>>>(b.counts.as<int>(), nbins, chunk, b.starts.as<int>(),
                                            b.units.as<int4>(), b.nunits.as<int>(), rlo, ubin_lo, ubin_hi,
