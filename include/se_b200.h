@@ -278,6 +278,29 @@ int se_kspace_field_host(se_plan_t plan, const double *pos, const double *q, int
  * se_slab_geometry returns nx, nky = n / world and nkz = n / 2 + 1 (n = M, or
  * nconv for D = 0). */
 int se_slab_geometry(se_plan_t plan, int world, int64_t *nx, int64_t *nky, int64_t *nkz);
+
+/* Row-distributed adaptive FFT of D = 1, 2 (aft.py:168-265 + sekspace.py:217-254
+ * split over `world` ranks).  Rank r holds the z-chunk
+ * z in [nz0, nz0 + nz), nz0 = Mt r / world, of the grid (every x, y): the
+ * periodic R2C is local to z-planes, its rows (periodic modes: (kx, ky < M/2+1)
+ * for D = 2 in chunks of M / world kx values, kx < M/2+1 for D = 1 in chunks of
+ * ceil((M/2+1) / world)) are grouped by chunk, and an all-to-all gives each rank
+ * every z of its rows, where the zero / I / J free-axis blocks are padded,
+ * transformed, scaled and inverted as in se_kspace_apply_dev.  Complex buffers
+ * are interleaved fp64:
+ *   se_zslab_geometry: out6 = {nz0, nz, row0, nrows, rows_total, per_y} (a row
+ *     carries per_y x (z) values: per_y = 1 for D = 2, Mt for D = 1);
+ *   se_zslab_forward_dev: zslab (M, M or Mt, nz) real -> spec (rows_total,
+ *     per_y, nz): rows of rank d's chunk are contiguous (the all-to-all's send
+ *     blocks: nrows_d x per_y x nz values to rank d);
+ *   se_zslab_rows_dev: in place on recv = (source s) x (nrows, per_y, nz_s):
+ *     this rank's rows through the free-axis blocks;
+ *   se_zslab_inverse_dev: spec (rows_total, per_y, nz) -> zslab real (the
+ *     spectrum is used as scratch). */
+int se_zslab_geometry(se_plan_t plan, int world, int rank, int64_t *out6);
+int se_zslab_forward_dev(se_plan_t plan, int world, int rank, const double *zslab, double *spec);
+int se_zslab_rows_dev(se_plan_t plan, int world, int rank, double *recv);
+int se_zslab_inverse_dev(se_plan_t plan, int world, int rank, const double *spec, double *zslab);
 int se_slab_forward_dev(se_plan_t plan, int world, const double *slab, double *send);
 int se_slab_xpass_dev(se_plan_t plan, int world, int rank, double *recv);
 int se_slab_inverse_dev(se_plan_t plan, int world, const double *back, double *slab);

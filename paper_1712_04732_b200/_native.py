@@ -89,6 +89,10 @@ SIGNATURES = {
     "se_realspace_field_host": [_P, _P, _P, ctypes.c_int64, _P],
     "se_kspace_field_host": [_P, _P, _P, ctypes.c_int64, _P],
     "se_slab_geometry": [_P, ctypes.c_int, c_int64_p, c_int64_p, c_int64_p],
+    "se_zslab_geometry": [_P, ctypes.c_int, ctypes.c_int, c_int64_p],
+    "se_zslab_forward_dev": [_P, ctypes.c_int, ctypes.c_int, _P, _P],
+    "se_zslab_rows_dev": [_P, ctypes.c_int, ctypes.c_int, _P],
+    "se_zslab_inverse_dev": [_P, ctypes.c_int, ctypes.c_int, _P, _P],
     "se_slab_forward_dev": [_P, ctypes.c_int, _P, _P],
     "se_slab_xpass_dev": [_P, ctypes.c_int, ctypes.c_int, _P],
     "se_slab_inverse_dev": [_P, ctypes.c_int, _P, _P],

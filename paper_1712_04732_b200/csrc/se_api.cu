@@ -358,7 +358,8 @@ void plan_release_device(se_plan *pl) {
     for (auto &ev : pl->gfence)
         if (ev) cudaEventDestroy(ev);
     for (cufftHandle h : {pl->fft_fwd, pl->fft_inv, pl->fft_rowJ, pl->fft_rowI, pl->fft_row0, pl->fft_c_fwd,
-                          pl->fft_c_inv, pl->fft_f_fwd, pl->fft_f_inv, pl->slab_f2, pl->slab_i2, pl->slab_x})
+                          pl->fft_c_inv, pl->fft_f_fwd, pl->fft_f_inv, pl->slab_f2, pl->slab_i2, pl->slab_x,
+                          pl->zs_fwd, pl->zs_inv, pl->zs_rowJ, pl->zs_rowI, pl->zs_row0})
         if (h) cufftDestroy(h);
     for (Binning *b : {&pl->tbin, &pl->cbin})
         for (DevBuf *d : {&b->keys, &b->keys_sorted, &b->idx, &b->idx_sorted, &b->counts, &b->starts, &b->units,
@@ -369,7 +370,8 @@ void plan_release_device(se_plan *pl) {
         t->what.release();
     }
     for (DevBuf *d : {&pl->flag, &pl->spec, &pl->spec2, &pl->spec3, &pl->work, &pl->grid_tmp, &pl->rows_I,
-                      &pl->ghat, &pl->grid_dev, &pl->io_pos, &pl->io_q, &pl->io_phi, &pl->io_grid, &pl->check, &pl->pairs, &pl->racc, &pl->sdet})
+                      &pl->ghat, &pl->grid_dev, &pl->io_pos, &pl->io_q, &pl->io_phi, &pl->io_grid, &pl->check, &pl->pairs, &pl->racc, &pl->sdet,
+                      &pl->zs_rowsI, &pl->zs_Hk, &pl->zs_Z, &pl->zs_B})
         d->release();
     if (pl->own_stream) cudaStreamDestroy(pl->own_stream);
 }
@@ -584,6 +586,38 @@ int se_slab_inverse_dev(se_plan_t plan, int world, const double *back, double *s
     se_plan *pl = checked(plan);
     DeviceGuard dg(pl->device);
     slab_inverse(pl, world, back, slab);
+    SE_API_END
+}
+
+int se_zslab_geometry(se_plan_t plan, int world, int rank, int64_t *out6) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    if (!out6) fail(SE_EINVAL, "null output pointer");
+    zslab_geometry(pl, world, rank, out6);
+    SE_API_END
+}
+
+int se_zslab_forward_dev(se_plan_t plan, int world, int rank, const double *zslab, double *spec) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    zslab_forward(pl, world, rank, zslab, spec);
+    SE_API_END
+}
+
+int se_zslab_rows_dev(se_plan_t plan, int world, int rank, double *recv) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    zslab_rows(pl, world, rank, recv);
+    SE_API_END
+}
+
+int se_zslab_inverse_dev(se_plan_t plan, int world, int rank, const double *spec, double *zslab) {
+    SE_API_BEGIN
+    se_plan *pl = checked(plan);
+    DeviceGuard dg(pl->device);
+    zslab_inverse(pl, world, rank, spec, zslab);
     SE_API_END
 }
 

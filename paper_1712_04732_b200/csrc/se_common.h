@@ -219,6 +219,10 @@ struct se_plan {
     // (device error flags, profiling events); se_plan_finish does both
     bool defer = false;
     cufftHandle slab_f2 = 0, slab_i2 = 0, slab_x = 0;
+    // row-distributed AFT (D = 1, 2), for one (world, rank)
+    int zs_world = -1, zs_rank = -1, zs_nI = 0;
+    cufftHandle zs_fwd = 0, zs_inv = 0, zs_rowJ = 0, zs_rowI = 0, zs_row0 = 0;
+    se::DevBuf zs_rowsI, zs_Hk, zs_Z, zs_B;
 };
 
 namespace se {
@@ -262,6 +266,10 @@ void kspace_run(se_plan *pl, double *grid, int use_kernel, double *timings);
 void realspace_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi,
                    int add_self, int rank, int world);
 void grad_gather_run(se_plan *pl, const double *grid, const double *pos, int64_t N, double *E, int accumulate);
+void zslab_geometry(se_plan *pl, int world, int rank, int64_t *out);
+void zslab_forward(se_plan *pl, int world, int rank, const double *zslab, double *spec);
+void zslab_rows(se_plan *pl, int world, int rank, double *recv);
+void zslab_inverse(se_plan *pl, int world, int rank, const double *spec, double *zslab);
 void realspace_domain_run(se_plan *pl, const double *pos, const double *q, int64_t n_local, int64_t n_own, int ncols,
                           int col_lo, int col_hi, double *phi, int add_self);
 void realspace_field_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *E,

@@ -234,6 +234,7 @@ struct MixArgs {
     int D, M, nI, half;  // half = M/2+1 (number of carried modes along the halved periodic axis)
     double xi, R;
     const double *kp, *wp;  // periodic mode table (length M)
+    int row0 = 0, nrows = -1;  // a chunk of the periodic-mode rows (multi-GPU); nrows < 0: all rows
 };
 
 __device__ __forceinline__ int absmode(int i, int M) { return i < M / 2 ? i : M - i; }
@@ -246,11 +247,12 @@ __global__ void scale_mixJ_kernel(cplx *__restrict__ Hk, MixArgs a, int Mt, cons
                                   const double *__restrict__ wf, double norm) {
     const int nfree = 3 - a.D;
     int64_t per = nfree == 1 ? Mt : (int64_t)Mt * Mt;
-    int64_t rowsN = a.D == 2 ? (int64_t)a.M * a.half : a.half;
+    int64_t rowsN = a.nrows >= 0 ? a.nrows : (a.D == 2 ? (int64_t)a.M * a.half : a.half);
     int64_t total = rowsN * per;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t row = i / per;
-        int64_t e = i - row * per;
+        const int64_t lrow = i / per;
+        const int64_t e = i - lrow * per;
+        const int64_t row = lrow + a.row0;
         double kr2, wr;
         int mu;
         if (a.D == 2) {
@@ -289,7 +291,7 @@ __global__ void scale_mixI_kernel(cplx *__restrict__ B, MixArgs a, const int *__
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         int r = (int)(i / per);
         int64_t e = i - (int64_t)r * per;
-        int row = rows[r];
+        int row = rows[r] + a.row0;  // rows[] index the (chunk's) rows; modes are global
         double kr2, wr;
         if (a.D == 2) {
             int ix = row / a.half, iy = row - ix * a.half;
@@ -784,6 +786,194 @@ void slab_inverse(se_plan *pl, int world, const double *back, double *slab) {
     pl->grid_tmp.ensure(sizeof(double) * (size_t)nx * n * n);
     SE_CUFFT(cufftExecZ2D(pl->slab_i2, pl->spec.as<cplx>(), pl->grid_tmp.as<double>()));
     LAUNCH(restrict_real_kernel, nx * Mt * Mt, pl->grid_tmp.as<double>(), n, n, slab, (int)nx, Mt, Mt, 1.0);
+}
+
+// ------------------------------------ row-distributed adaptive FFT (D = 1, 2)
+// The AFT of D in {1, 2} (aft.py:168-265, sekspace.py:217-254) over `world`
+// ranks: rank r holds the z-chunk z in [nz0, nz0 + nz) of the
+// grid (every x, y): the periodic R2C (2-D over (x, y) for D = 2, 1-D over x
+// for D = 1) is local to a z-plane; its output rows (periodic modes, the
+// halved axis last) are grouped by row chunk, so an all-to-all hands rank d
+// every z of its rows [row0, row0 + nrows); there the free-axis blocks (zero
+// mode padded to g0, I rows to gs, J rows at Mt) are transformed, scaled and
+// inverted exactly as in the single-GPU stage, and the reverse all-to-all and
+// the inverse periodic C2R return the filtered z-chunk.
+//   rows: D = 2: (kx, ky) with ky < M/2 + 1, chunks of (M / world) kx values;
+//         D = 1: kx < M/2 + 1, chunks of ceil((M/2 + 1) / world);
+//   a row carries per_y x Mt values (per_y = 1 for D = 2, Mt for D = 1).
+struct ZGeom {
+    int nz0, nz, row0, nrows, rows_total, per_y;
+};
+
+static ZGeom zslab_geom(const se_plan *pl, int world, int rank) {
+    const int D = pl->D, M = pl->g.M, Mt = pl->g.Mt, half = M / 2 + 1;
+    if (D != 1 && D != 2) fail(SE_EINVAL, "the row-distributed AFT covers D = 1 and D = 2");
+    if (world < 1 || rank < 0 || rank >= world) fail(SE_EINVAL, "invalid (rank, world)");
+    if (Mt < world) fail(SE_EINVAL, "more ranks than free-axis planes");
+    ZGeom z{};
+    z.nz0 = (int)((int64_t)Mt * rank / world);
+    z.nz = (int)((int64_t)Mt * (rank + 1) / world) - z.nz0;
+    if (D == 2) {
+        if (M % world) fail(SE_EINVAL, "the row-distributed AFT of D = 2 needs M divisible by the ranks");
+        z.rows_total = M * half;
+        z.nrows = (M / world) * half;
+        z.row0 = rank * z.nrows;
+        z.per_y = 1;
+    } else {
+        const int c = (half + world - 1) / world;
+        z.rows_total = half;
+        z.row0 = std::min(rank * c, half);
+        z.nrows = std::min(half, z.row0 + c) - z.row0;
+        z.per_y = Mt;
+    }
+    return z;
+}
+
+static void zslab_plans(se_plan *pl, int world, int rank) {
+    if (pl->zs_world == world && pl->zs_rank == rank) return;
+    for (cufftHandle *h : {&pl->zs_fwd, &pl->zs_inv, &pl->zs_rowJ, &pl->zs_rowI, &pl->zs_row0}) {
+        if (*h) cufftDestroy(*h);
+        *h = 0;
+    }
+    ensure_tables(pl);
+    const ZGeom z = zslab_geom(pl, world, rank);
+    const se_grid_t &g = pl->g;
+    const int D = pl->D, M = g.M, Mt = g.Mt, half = M / 2 + 1;
+    if (D == 2) {
+        int n[2] = {M, M}, rin[2] = {M, M}, cout[2] = {M, half};
+        SE_CUFFT(cufftPlanMany(&pl->zs_fwd, 2, n, rin, z.nz, 1, cout, z.nz, 1, CUFFT_D2Z, z.nz));
+        SE_CUFFT(cufftPlanMany(&pl->zs_inv, 2, n, cout, z.nz, 1, rin, z.nz, 1, CUFFT_Z2D, z.nz));
+    } else {
+        int n[1] = {M}, rin[1] = {M}, cout[1] = {half};
+        const int lines = Mt * z.nz;
+        SE_CUFFT(cufftPlanMany(&pl->zs_fwd, 1, n, rin, lines, 1, cout, lines, 1, CUFFT_D2Z, lines));
+        SE_CUFFT(cufftPlanMany(&pl->zs_inv, 1, n, cout, lines, 1, rin, lines, 1, CUFFT_Z2D, lines));
+    }
+    // this chunk's I rows (local indices) and the zero row (global row 0)
+    std::vector<int> m = signed_modes(M), rows;
+    for (int lr = 0; lr < z.nrows; ++lr) {
+        const int row = z.row0 + lr;
+        int mu;
+        if (D == 2) {
+            const int ix = row / half, iy = row - ix * half;
+            mu = std::max(std::abs(m[ix]), std::abs(m[iy]));
+        } else {
+            mu = std::abs(m[row]);
+        }
+        if (mu >= 1 && mu <= pl->p.nI) rows.push_back(lr);
+    }
+    pl->zs_nI = (int)rows.size();
+    pl->zs_rowsI.ensure(sizeof(int) * (rows.size() + 1));
+    if (!rows.empty())
+        SE_CUDA(cudaMemcpy(pl->zs_rowsI.ptr, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
+    if (D == 2) {
+        int nJ[1] = {Mt}, nI1[1] = {g.gs}, n0[1] = {g.g0};
+        if (z.nrows > 0)
+            SE_CUFFT(cufftPlanMany(&pl->zs_rowJ, 1, nJ, nullptr, 1, Mt, nullptr, 1, Mt, CUFFT_Z2Z, z.nrows));
+        if (pl->zs_nI > 0)
+            SE_CUFFT(cufftPlanMany(&pl->zs_rowI, 1, nI1, nullptr, 1, g.gs, nullptr, 1, g.gs, CUFFT_Z2Z, pl->zs_nI));
+        SE_CUFFT(cufftPlanMany(&pl->zs_row0, 1, n0, nullptr, 1, g.g0, nullptr, 1, g.g0, CUFFT_Z2Z, 1));
+        pl->zs_Z.ensure(sizeof(cplx) * (size_t)g.g0);
+        pl->zs_B.ensure(sizeof(cplx) * (size_t)(pl->zs_nI ? pl->zs_nI : 1) * g.gs);
+    } else {
+        int nJ[2] = {Mt, Mt}, nI2[2] = {g.gs, g.gs}, n0[2] = {g.g0, g.g0};
+        if (z.nrows > 0)
+            SE_CUFFT(cufftPlanMany(&pl->zs_rowJ, 2, nJ, nullptr, 1, Mt * Mt, nullptr, 1, Mt * Mt, CUFFT_Z2Z, z.nrows));
+        if (pl->zs_nI > 0)
+            SE_CUFFT(cufftPlanMany(&pl->zs_rowI, 2, nI2, nullptr, 1, g.gs * g.gs, nullptr, 1, g.gs * g.gs, CUFFT_Z2Z,
+                                   pl->zs_nI));
+        SE_CUFFT(cufftPlanMany(&pl->zs_row0, 2, n0, nullptr, 1, g.g0 * g.g0, nullptr, 1, g.g0 * g.g0, CUFFT_Z2Z, 1));
+        pl->zs_Z.ensure(sizeof(cplx) * (size_t)g.g0 * g.g0);
+        pl->zs_B.ensure(sizeof(cplx) * (size_t)(pl->zs_nI ? pl->zs_nI : 1) * g.gs * g.gs);
+    }
+    pl->zs_Hk.ensure(sizeof(cplx) * ((size_t)z.nrows * z.per_y * Mt + 1));
+    pl->zs_world = world;
+    pl->zs_rank = rank;
+}
+
+// recv [source s][my rows][per_y][nz_s] <-> Hk [my rows][per_y][Mt] (z of
+// source s at [nz0_s, nz0_s + nz_s), nz0_s = Mt s / world)
+template <bool TO_ROWS>
+__global__ void zslab_reorder_kernel(cplx *__restrict__ recv, cplx *__restrict__ Hk, int64_t nrows_py, int Mt,
+                                     int world) {
+    const int64_t total = nrows_py * Mt;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int z = (int)(i % Mt);
+        const int64_t rp = i / Mt;
+        int s = 0;
+        while (s + 1 < world && (int)((int64_t)Mt * (s + 1) / world) <= z) ++s;
+        const int nz0 = (int)((int64_t)Mt * s / world), nz = (int)((int64_t)Mt * (s + 1) / world) - nz0;
+        const int64_t j = nrows_py * nz0 + rp * nz + (z - nz0);
+        if (TO_ROWS)
+            Hk[i] = recv[j];
+        else
+            recv[j] = Hk[i];
+    }
+}
+
+void zslab_geometry(se_plan *pl, int world, int rank, int64_t *out) {
+    const ZGeom z = zslab_geom(pl, world, rank);
+    out[0] = z.nz0;
+    out[1] = z.nz;
+    out[2] = z.row0;
+    out[3] = z.nrows;
+    out[4] = z.rows_total;
+    out[5] = z.per_y;
+}
+
+// zslab (M, M or Mt, nz) real -> spec (rows_total, per_y, nz) complex
+void zslab_forward(se_plan *pl, int world, int rank, const double *zslab, double *spec) {
+    zslab_plans(pl, world, rank);
+    set_streams(pl, {pl->zs_fwd});
+    SE_CUFFT(cufftExecD2Z(pl->zs_fwd, const_cast<double *>(zslab), reinterpret_cast<cplx *>(spec)));
+}
+
+void zslab_inverse(se_plan *pl, int world, int rank, const double *spec, double *zslab) {
+    zslab_plans(pl, world, rank);
+    set_streams(pl, {pl->zs_inv});
+    // cuFFT's C2R may overwrite its input: the caller's spectrum is scratch here
+    SE_CUFFT(cufftExecZ2D(pl->zs_inv, reinterpret_cast<cplx *>(const_cast<double *>(spec)), zslab));
+}
+
+// in place on recv: this rank's rows, every z, through the free-axis blocks
+void zslab_rows(se_plan *pl, int world, int rank, double *recv) {
+    zslab_plans(pl, world, rank);
+    const ZGeom z = zslab_geom(pl, world, rank);
+    if (z.nrows <= 0) return;
+    const se_grid_t &g = pl->g;
+    const int D = pl->D, M = g.M, Mt = g.Mt, half = M / 2 + 1, nfree = 3 - D;
+    set_streams(pl, {pl->zs_rowJ, pl->zs_rowI, pl->zs_row0});
+    cplx *R = reinterpret_cast<cplx *>(recv), *Hk = pl->zs_Hk.as<cplx>(), *Z = pl->zs_Z.as<cplx>(),
+         *B = pl->zs_B.as<cplx>();
+    const int64_t nrp = (int64_t)z.nrows * z.per_y;
+    LAUNCH(zslab_reorder_kernel<true>, nrp * Mt, R, Hk, nrp, Mt, world);
+    const int *rows = pl->zs_rowsI.as<int>();
+    const int nI = pl->zs_nI;
+    const bool zero_here = z.row0 == 0;  // the k = 0 row lives in the first chunk
+    MixArgs ma{D, M, pl->p.nI, half, pl->p.xi, g.R, pl->tM.k.as<double>(), pl->tM.what.as<double>()};
+    ma.row0 = z.row0;
+    ma.nrows = z.nrows;
+    const double perN = D == 2 ? (double)M * M : (double)M;
+    auto pw = [&](int n) { return nfree == 1 ? (double)n : (double)n * n; };
+    if (zero_here) LAUNCH(pack_kernel, (int64_t)pw(g.g0), Hk, Mt, nfree, nullptr, 1, Z, g.g0);
+    if (nI) LAUNCH(pack_kernel, (int64_t)pw(g.gs) * nI, Hk, Mt, nfree, rows, nI, B, g.gs);
+    SE_CUFFT(cufftExecZ2Z(pl->zs_rowJ, Hk, Hk, CUFFT_FORWARD));
+    if (nI) SE_CUFFT(cufftExecZ2Z(pl->zs_rowI, B, B, CUFFT_FORWARD));
+    if (zero_here) SE_CUFFT(cufftExecZ2Z(pl->zs_row0, Z, Z, CUFFT_FORWARD));
+    LAUNCH(scale_mixJ_kernel, (int64_t)z.nrows * (int64_t)pw(Mt), Hk, ma, Mt, pl->tMt.k.as<double>(),
+           pl->tMt.what.as<double>(), 1.0 / (pw(Mt) * perN));
+    if (nI)
+        LAUNCH(scale_mixI_kernel, (int64_t)pw(g.gs) * nI, B, ma, rows, nI, g.gs, pl->tgs.k.as<double>(),
+               pl->tgs.what.as<double>(), 1.0 / (pw(g.gs) * perN));
+    if (zero_here)
+        LAUNCH(scale_mix0_kernel, (int64_t)pw(g.g0), Z, ma, g.g0, pl->tg0.k.as<double>(), pl->tg0.what.as<double>(),
+               1.0 / (pw(g.g0) * perN));
+    SE_CUFFT(cufftExecZ2Z(pl->zs_rowJ, Hk, Hk, CUFFT_INVERSE));
+    if (nI) SE_CUFFT(cufftExecZ2Z(pl->zs_rowI, B, B, CUFFT_INVERSE));
+    if (zero_here) SE_CUFFT(cufftExecZ2Z(pl->zs_row0, Z, Z, CUFFT_INVERSE));
+    if (nI) LAUNCH(unpack_kernel, (int64_t)pw(Mt) * nI, B, g.gs, nfree, rows, nI, Hk, Mt);
+    if (zero_here) LAUNCH(unpack_kernel, (int64_t)pw(Mt), Z, g.g0, nfree, nullptr, 1, Hk, Mt);
+    LAUNCH(zslab_reorder_kernel<false>, nrp * Mt, R, Hk, nrp, Mt, world);
 }
 
 // ------------------------------------------------------ field (D = 3, ik)

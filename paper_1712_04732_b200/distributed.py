@@ -128,7 +128,7 @@ class NativeBackend:
         """Plane geometry of the slab k-space stage (DomainPartition.touched_pieces)."""
         g = self.plan.grid()
         D = self.peri.D
-        if D == 3:
+        if D >= 1:
             n = int(g.M)
         else:
             nconv, g0, R = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
@@ -148,6 +148,21 @@ class NativeBackend:
     def realspace_domain(self, pos, q, n_own, part, rank, phi):
         _native.call("se_realspace_domain_dev", self.plan.handle, _native.ptr(pos), _native.ptr(q), q.shape[0],
                      int(n_own), part.ncols, part.col_lo[rank], part.col_hi[rank], _native.ptr(phi), 1)
+
+    # row-distributed adaptive FFT (D = 1, 2)
+    def zslab_geometry(self, world, rank):
+        out = (ctypes.c_int64 * 6)()
+        _native.call("se_zslab_geometry", self.plan_k.handle, world, rank, out)
+        return dict(zip(("nz0", "nz", "row0", "nrows", "rows_total", "per_y"), (int(v) for v in out)))
+
+    def zslab_forward(self, zslab, world, rank, spec):
+        self._k("se_zslab_forward_dev", world, rank, _native.ptr(zslab), _native.ptr(spec))
+
+    def zslab_rows(self, recv, world, rank):
+        self._k("se_zslab_rows_dev", world, rank, _native.ptr(recv))
+
+    def zslab_inverse(self, spec, world, rank, zslab):
+        self._k("se_zslab_inverse_dev", world, rank, _native.ptr(spec), _native.ptr(zslab))
 
     # slab-decomposed k-space stage (D = 3)
     def slab_geometry(self, world):
@@ -530,15 +545,20 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
     phi_local = backend.empty_phi(lpos.shape[0])
     phik = backend.empty_phi(n_own)
     grid = backend.empty_grid()
-    kg = backend.slab_kgeo() if backend.peri.D in (0, 3) else None
-    slab_ok = kg is not None and kg["n"] % world == 0
+    D = backend.peri.D
+    kg = backend.slab_kgeo()
+    slab_ok = D in (0, 3) and kg["n"] % world == 0
+    zslab_ok = D in (1, 2) and (D == 1 or kg["planes"] % world == 0) and grid.shape[2] >= world
     if kspace == "auto":
-        kspace = "slab" if slab_ok else "replicated"
-    if kspace not in ("slab", "replicated"):
-        raise ValueError(f"kspace must be 'auto', 'slab' or 'replicated', got {kspace!r}")
+        kspace = "slab" if slab_ok else ("zslab" if zslab_ok and multi else "replicated")
+    if kspace not in ("slab", "zslab", "replicated"):
+        raise ValueError(f"kspace must be 'auto', 'slab', 'zslab' or 'replicated', got {kspace!r}")
     if kspace == "slab" and not slab_ok:
         raise ValueError("the slab k-space stage needs D = 3 or 0 and its transform size (M, or nconv for D = 0) "
                          "divisible by the rank count")
+    if kspace == "zslab" and not zslab_ok:
+        raise ValueError("the row-distributed AFT needs D = 1 or 2 (D = 2: M divisible by the rank count) and at "
+                         "least one free-axis plane per rank")
     if ks is not None:
         ks.wait_stream(cur)
     with side:
@@ -551,6 +571,8 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
             if work is not None:
                 work.wait()
             backend.kspace_apply(grid)
+        elif kspace == "zslab":
+            _zslab_kspace_domain(backend, part, kg, grid, rank, world, group, multi)
         else:
             _slab_kspace_domain(backend, part, kg, grid, rank, world, group, multi)
         backend.gather_all(grid, opos, phik, accumulate=False)
@@ -625,3 +647,62 @@ def _slab_kspace_domain(backend, part, kg, grid, rank, world, group, multi):
         for lo, hi in part.exchange_pieces(rank, s, kg):
             flat[lo:hi] = recv2[row:row + hi - lo]
             row += hi - lo
+
+
+def _zslab_kspace_domain(backend, part, kg, grid, rank, world, group, multi):
+    """D = 1, 2: the adaptive FFT distributed over rows of periodic modes
+    ("all-to-all to (kx, ky)-row ownership ... kx-plane
+    ownership").  Each rank's touched x-planes go, cut into z-chunks, to the
+    chunk owners (summed there); each rank transforms its z-chunk over the
+    periodic axes, an all-to-all gives every rank all z of its row chunk, the
+    zero / I / J free-axis blocks run there, and the reverse all-to-all, the
+    inverse periodic transform and the return of the touched planes (every z)
+    give each rank the filtered grid it gathers from."""
+    X, Y, Zt = grid.shape
+    geo = [backend.zslab_geometry(world, r) for r in range(world)]
+    me = geo[rank]
+    mine = part.touched_pieces(rank, kg)
+    parts, counts = [], []
+    for d in range(world):
+        z0, z1 = geo[d]["nz0"], geo[d]["nz0"] + geo[d]["nz"]
+        blocks = [grid[lo:hi, :, z0:z1].reshape(-1) for lo, hi in mine]
+        parts += blocks
+        counts.append(sum(int(b.numel()) for b in blocks))
+    send = torch.cat(parts) if parts else grid.new_zeros(0)
+    recv, _ = _all_to_allv(send, counts, group, multi)
+    nz = me["nz"]
+    zslab = grid.new_zeros((X, Y, nz))
+    off = 0
+    for s in range(world):
+        for lo, hi in part.touched_pieces(s, kg):
+            n = (hi - lo) * Y * nz
+            zslab[lo:hi] += recv[off:off + n].view(hi - lo, Y, nz)
+            off += n
+    per_y = me["per_y"]
+    spec = grid.new_empty(me["rows_total"] * per_y * nz * 2)
+    backend.zslab_forward(zslab, world, rank, spec)
+    send_c = [geo[d]["nrows"] * per_y * nz * 2 for d in range(world)]
+    recv_c = [me["nrows"] * per_y * geo[s]["nz"] * 2 for s in range(world)]
+    if multi:
+        rows = grid.new_empty(sum(recv_c))
+        dist.all_to_all_single(rows, spec, output_split_sizes=recv_c, input_split_sizes=send_c, group=group)
+    else:
+        rows = spec
+    backend.zslab_rows(rows, world, rank)
+    if multi:
+        dist.all_to_all_single(spec, rows, output_split_sizes=send_c, input_split_sizes=recv_c, group=group)
+    backend.zslab_inverse(spec, world, rank, zslab)
+    parts2, counts2 = [], []
+    for s in range(world):
+        blocks = [zslab[lo:hi].reshape(-1) for lo, hi in part.touched_pieces(s, kg)]
+        parts2 += blocks
+        counts2.append(sum(int(b.numel()) for b in blocks))
+    send2 = torch.cat(parts2) if parts2 else grid.new_zeros(0)
+    recv2, _ = _all_to_allv(send2, counts2, group, multi)
+    off = 0
+    for d in range(world):
+        z0, nzd = geo[d]["nz0"], geo[d]["nz"]
+        for lo, hi in mine:
+            n = (hi - lo) * Y * nzd
+            grid[lo:hi, :, z0:z0 + nzd] = recv2[off:off + n].view(hi - lo, Y, nzd)
+            off += n

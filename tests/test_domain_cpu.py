@@ -53,7 +53,7 @@ class DomainOracleBackend:
         return DomainPartition(self.L, self.params, self.peri, world, n_total, self.g["shape"])
 
     def slab_kgeo(self):
-        n = self.prm["M"] if self.D == 3 else self.nconv
+        n = self.prm["M"] if self.D >= 1 else self.nconv
         return {"planes": self.g["shape"][0], "n": n, "P": self.prm["P"], "h": self.g["h"],
                 "off": 0.0 if self.D >= 1 else 0.5 * self.prm["P"] * self.g["h"], "periodic": self.D >= 1}
 
@@ -181,6 +181,95 @@ class DomainOracleBackend:
         slab.copy_(torch.from_numpy(np.ascontiguousarray(out[:, :slab.shape[1], :slab.shape[2]])))
 
 
+    # row-distributed adaptive FFT (D = 1, 2): numpy restatement of the
+    # se_zslab_* stages in the library's layouts
+    def zslab_geometry(self, world, rank):
+        M, Mt = self.prm["M"], self.g["Mt"]
+        half = M // 2 + 1
+        nz0 = Mt * rank // world
+        nz = Mt * (rank + 1) // world - nz0
+        if self.D == 2:
+            nrows = (M // world) * half
+            return dict(nz0=nz0, nz=nz, row0=rank * nrows, nrows=nrows, rows_total=M * half, per_y=1)
+        c = -(-half // world)
+        row0 = min(rank * c, half)
+        return dict(nz0=nz0, nz=nz, row0=row0, nrows=min(half, row0 + c) - row0, rows_total=half, per_y=Mt)
+
+    def zslab_forward(self, zslab, world, rank, spec):
+        z = zslab.numpy()
+        A = np.fft.rfftn(z, axes=(0, 1)) if self.D == 2 else np.fft.rfft(z, axis=0)
+        self._put(spec.view(-1, 2), A.reshape(-1))
+
+    def zslab_inverse(self, spec, world, rank, zslab):
+        M = self.prm["M"]
+        me = self.zslab_geometry(world, rank)
+        A = self._get(spec.view(-1, 2))
+        if self.D == 2:
+            out = np.fft.irfftn(A.reshape(M, M // 2 + 1, me["nz"]), s=(M, M), axes=(0, 1))
+        else:
+            out = np.fft.irfft(A.reshape(M // 2 + 1, self.g["Mt"], me["nz"]), n=M, axis=0)
+        zslab.copy_(torch.from_numpy(np.ascontiguousarray(out)))
+
+    def zslab_rows(self, recv, world, rank):
+        orc, g, D = self.orc, self.g, self.D
+        M, Mt, h = self.prm["M"], g["Mt"], g["h"]
+        half = M // 2 + 1
+        me = self.zslab_geometry(world, rank)
+        geo = [self.zslab_geometry(world, s) for s in range(world)]
+        nr, py = me["nrows"], me["per_y"]
+        flat = self._get(recv.view(-1, 2))
+        blocks, off = [], 0
+        for s in range(world):
+            n = nr * py * geo[s]["nz"]
+            blocks.append(flat[off:off + n].reshape(nr, py, geo[s]["nz"]))
+            off += n
+        Hk = np.concatenate(blocks, axis=2)  # (rows, per_y, Mt)
+        kind, shape, xi = self.prm["window"], self.prm["shape"], self.prm["xi"]
+        w = 0.5 * g["P"] * h
+        kp = orc.wavenumbers(M, h)
+        wp = orc.window_fourier_checked(kind, shape, w, kp)
+        m = np.where(np.arange(M) < M // 2, np.arange(M), np.arange(M) - M)
+        nfree = 3 - D
+        faxes = tuple(range(1, 1 + nfree))
+        for i in range(nr):
+            row = me["row0"] + i
+            if D == 2:
+                ix, iy = divmod(row, half)
+                mu = max(abs(m[ix]), abs(m[iy]))
+                kr2, wr = kp[ix] ** 2 + kp[iy] ** 2, wp[ix] * wp[iy]
+            else:
+                ix = row
+                mu = abs(m[ix])
+                kr2, wr = kp[ix] ** 2, wp[ix]
+            data = Hk[i].reshape(Mt) if D == 2 else Hk[i]
+            glen = g["g0"] if mu == 0 else (g["gs"] if mu <= self.prm["nI"] else Mt)
+            B = orc._zero_pad_axes(data[None], glen, faxes)[0]
+            B = np.fft.fftn(B)
+            kf = orc.wavenumbers(glen, h)
+            wf = orc.window_fourier_checked(kind, shape, w, kf)
+            if nfree == 1:
+                kap2, wfree = kf ** 2, wf
+            else:
+                kap2 = kf[:, None] ** 2 + kf[None, :] ** 2
+                wfree = wf[:, None] * wf[None, :]
+            if mu == 0:
+                B *= (orc.FOUR_PI * orc._mollify(kap2, xi) * orc.greens_zero_block(D, g["R"], np.sqrt(kap2))
+                      / ((wp[0] ** D) * wfree) ** 2)
+            else:
+                k2 = kr2 + kap2
+                B *= orc.FOUR_PI * orc._mollify(k2, xi) / (k2 * (wr * wfree) ** 2)
+            out = np.fft.ifftn(B)[(slice(0, Mt),) * nfree]
+            Hk[i] = out.reshape(Hk[i].shape)
+        off = 0
+        res = np.empty_like(flat)
+        for s in range(world):
+            z0, nzs = geo[s]["nz0"], geo[s]["nz"]
+            n = nr * py * nzs
+            res[off:off + n] = Hk[:, :, z0:z0 + nzs].reshape(-1)
+            off += n
+        self._put(recv.view(-1, 2), res)
+
+
 def _case(D):
     rng = np.random.default_rng(11 + D)
     N, L = 500, 1.0
@@ -190,6 +279,8 @@ def _case(D):
     prm = dict(xi=9.0, rc=0.3, M=24, P=8, window="bm", shape=20.0)
     if D == 0:
         prm.update(s0=4.0, R=1.2)
+    if D in (1, 2):
+        prm.update(s0=3.0, s=2.0, nI=3, R=2.0)
     return pos, q, L, prm
 
 
@@ -217,7 +308,9 @@ def _worker(rank, world, port, out_path, D, kspace):
 
 
 @pytest.mark.parametrize("world,D,kspace", [(2, 3, "slab"), (3, 3, "slab"), (2, 3, "replicated"),
-                                            (2, 0, "replicated"), (2, 0, "slab"), (4, 0, "slab")])
+                                            (2, 0, "replicated"), (2, 0, "slab"), (4, 0, "slab"),
+                                            (2, 2, "zslab"), (3, 2, "zslab"), (2, 1, "zslab"), (3, 1, "zslab"),
+                                            (2, 2, "replicated")])
 def test_domain_decomposition_gloo(tmp_path, world, D, kspace):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import se_oracle as orc
