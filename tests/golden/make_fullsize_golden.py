@@ -6,6 +6,7 @@ Run in the build container (the reference is not on the GPU box); cfg2 takes
 ~20 min of the reference's CPU path on 8 threads:
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_fullsize_golden.py cfg1 cfg3 cfg4 cfg2
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_fullsize_golden.py cfg1_tol cfg4_tol cfg2_tol
 
 Writes `tests/golden/full_<cfg>.npz`: the reference's total potential
 (core.total_potential), Fourier part (sekspace.se_kspace) and real-space part
@@ -15,11 +16,12 @@ checksums of the total potential (sum q phi -- the reference's core.energy
 count.  A full vector is 8 bytes per particle; the sample plus checksums
 keep the fixtures small while the checksums still cover every entry.
 
-cfg5 is not generated: the reference's real-space path builds dense
+cfg5 (D = 0, N = 5e5, clustered): the reference's real space builds dense
 (|home|, |neighbour|, 3) distance blocks of ~24k x 24k particles per cell
-pair there (~32 GB per thread) -- infeasible in this 62 GB
-container; its parity rests on the sampled oracle and the device direct
-sums (tests/test_gpu_direct.py).
+pair there (~32 GB per thread), so it runs with THREADS=1 in the
+62 GB container (round 2: 5,334 s, real space 5,304 s):
+
+    THREADS=1 PYTHONPATH=/root/reference/pkg/src python tests/golden/make_fullsize_golden.py cfg5
 """
 
 from __future__ import annotations
