@@ -284,14 +284,17 @@ def _case(D):
     return pos, q, L, prm
 
 
-def _subset(rank, world, N, seed=3):
-    """An arbitrary (unsorted, uneven) subset of the particles per rank."""
+def _subset(rank, world, N, seed=3, empty_rank=None):
+    """An arbitrary (unsorted, uneven) subset of the particles per rank
+    (empty_rank: that rank passes no particle at all)."""
     owner = np.random.default_rng(seed).integers(0, world, N)
     owner[:world] = np.arange(world)
+    if empty_rank is not None:
+        owner[owner == empty_rank] = (empty_rank + 1) % world
     return np.nonzero(owner == rank)[0]
 
 
-def _worker(rank, world, port, out_path, D, kspace):
+def _worker(rank, world, port, out_path, D, kspace, empty_rank=None):
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     import se_oracle as orc
     from paper_1712_04732_b200.distributed import total_potential_domain
@@ -299,7 +302,7 @@ def _worker(rank, world, port, out_path, D, kspace):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     pos, q, L, prm = _case(D)
-    mine = _subset(rank, world, len(q))
+    mine = _subset(rank, world, len(q), empty_rank=empty_rank)
     be = DomainOracleBackend(orc, L, D, prm)
     phi = total_potential_domain(torch.from_numpy(pos[mine].copy()), torch.from_numpy(q[mine].copy()), be,
                                  kspace=kspace)
@@ -324,6 +327,24 @@ def test_domain_decomposition_gloo(tmp_path, world, D, kspace):
         phi = np.load(f"{out}.{r}.npy")
         assert phi.shape == (len(mine),)
         assert orc.relative_rms(phi, ref[mine]) < 1e-13, (r, orc.relative_rms(phi, ref[mine]))
+
+
+def test_domain_rank_with_no_particles(tmp_path):
+    """A rank that passes an empty set still owns a slab: it receives its
+    particles by migration and returns nothing."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import se_oracle as orc
+
+    out = str(tmp_path / "phi")
+    mp.spawn(_worker, args=(3, _free_port(), out, 3, "slab", 1), nprocs=3, join=True)
+    pos, q, L, prm = _case(3)
+    ref = orc.total_potential(pos, q, L, 3, prm)
+    for r in range(3):
+        mine = _subset(r, 3, len(q), empty_rank=1)
+        phi = np.load(f"{out}.{r}.npy")
+        assert phi.shape == (len(mine),)
+        if len(mine):
+            assert orc.relative_rms(phi, ref[mine]) < 1e-13
 
 
 def test_domain_single_process():
