@@ -403,25 +403,43 @@ struct PreTargets {
 // are evaluated at r = rc and multiplied by 0.  Newton (half-shell) path only.
 template <bool WIDE, class WB>
 __device__ __forceinline__ void dense_batch(WB &wb, int lane, int j, int m, double xs, double ys, double zs, double qs,
-                                            const RealArgs &a, unsigned amask, int tbase, int hs,
+                                            const RealArgs &a, unsigned amask, int tbase, int hs, const double3 org,
                                             double *__restrict__ acc_s, int &singular) {
     const bool sval = lane < m;
+    if (!sval) {  // past the run's end: a harmless nearby point (never counted)
+        xs = org.x;
+        ys = org.y;
+        zs = org.z;
+    }
+    // valid (target, this source) pairs as a 16-bit mask over the target
+    // SLOTS (tslot order), built once per batch: active targets, and in the
+    // own column only targets t < j (the pair j <= t is visited from j's side)
+    unsigned vt = amask & 0xffffu;
+    if (hs >= 0) {
+        const int c = min(max(j - tbase, 0), kT);
+        vt &= (1u << c) - 1u;
+    }
+    if (!sval) vt = 0u;
+    const unsigned vs = (vt & 0x00ffu) | ((vt & 0x0f00u) << 4) | ((vt & 0xf000u) >> 4);
     double accs = 0.0;
 #pragma unroll 2
     for (int st = 0; st < kT; ++st) {
-        const int tu = (lane + st) & (kT - 1);
-        const int sl = tslot(tu);
+        const int sl = (lane + st) & (kT - 1);  // a slot; lanes l and l + 16 share it
         const double2 t01 = wb.txy[sl], t23 = wb.tzq[sl];
-        const bool v = sval && ((amask >> tu) & 1u) && (hs < 0 || j > tbase + tu);
+        const bool v = (vs >> sl) & 1u;
         const double dx = t01.x - xs, dy = t01.y - ys, dz = t23.x - zs;
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
         const bool zero = r2 < 1e-28;
         singular |= (v && zero) ? 1 : 0;
-        const bool in = v && r2 < a.rc2 && !zero;  // a.rc2 = rc^2 (1 + 1e-12): never drops a pair
-        const double r2s = in ? r2 : a.rc2;        // a safe argument for every other slot
+        // a valid pair is a real pair of the column window (r <~ 2 rc: erfc_fast's
+        // argument stays bounded; pairs beyond rc get w = 0); every other slot
+        // (inactive target slots hold zeros, the self pair r = 0) is evaluated
+        // at r = rc and dropped
+        const bool use = v && !zero;
+        const double r2s = use ? r2 : a.rc2;
         const double rinv = rsqrt_nr(r2s);
         const double rr = r2s * rinv;
-        const double w = (in && rr < a.rc) ? rinv : 0.0;
+        const double w = (use && rr < a.rc) ? rinv : 0.0;
         const double f = erfc_fast<WIDE>(a.xi * rr, w);
         double *slot = &wb.acc[0][sl][lane];
         *slot = fma(qs, f, *slot);
@@ -520,7 +538,7 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     }
     const int c = __popc(hit);
     if (!COUNT && !FLD && NEWTON && __reduce_add_sync(0xffffffffu, (unsigned)c) >= (unsigned)a.dense_min) {
-        dense_batch<WIDE>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, hs, acc_src + jb, singular);
+        dense_batch<WIDE>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, hs, org, acc_src + jb, singular);
         return;
     }
     const int incl = warp_incl_scan(c, lane);
