@@ -122,7 +122,11 @@ class NativeBackend:
 
     # domain decomposition (total_potential_domain)
     def domain_partition(self, world, n_total):
-        return DomainPartition(self.L, self.params, self.peri, world, n_total, self.shape)
+        key = (world, n_total)
+        cache = self.__dict__.setdefault("_partitions", {})
+        if key not in cache:
+            cache[key] = DomainPartition(self.L, self.params, self.peri, world, n_total, self.shape)
+        return cache[key]
 
     def slab_kgeo(self):
         """Plane geometry of the slab k-space stage (DomainPartition.touched_pieces)."""
@@ -395,6 +399,14 @@ class DomainPartition:
             off %= self.ncols
         return 0 <= off < self.reach
 
+    def device_tables(self, dev):
+        """(owner rank per column, halo[column, rank]) on `dev`, built once."""
+        tabs = self.__dict__.setdefault("_tables", {})
+        if dev not in tabs:
+            tabs[dev] = (torch.tensor(self.owner_of_col, dtype=torch.int64, device=dev),
+                         torch.tensor(self.halo_to, dtype=torch.bool, device=dev))
+        return tabs[dev]
+
     def columns(self, x):
         """Column index cx of each x (the kernel's floor(x / edge), clamped)."""
         return torch.clamp(torch.floor(x / self.edge), 0, self.ncols - 1).to(torch.int64)
@@ -440,16 +452,20 @@ class DomainPartition:
         return out
 
 
-def _all_to_allv(send, send_counts, group, multi):
+def _all_to_allv(send, send_counts, group, multi, recv_counts=None):
     """all_to_all_single of the rows of `send` (grouped by destination, counts
-    per rank); returns (recv, recv_counts)."""
+    per rank); returns (recv, recv_counts).  recv_counts, when the caller
+    knows them (the partition fixes every plane exchange; a return path
+    mirrors its outbound exchange), skip the count exchange and its host
+    synchronisation."""
     if not multi:
         return send, list(send_counts)
-    dev = send.device
-    sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
-    rc = torch.empty_like(sc)
-    dist.all_to_all_single(rc, sc, group=group)
-    recv_counts = [int(v) for v in rc.tolist()]
+    if recv_counts is None:
+        dev = send.device
+        sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+        rc = torch.empty_like(sc)
+        dist.all_to_all_single(rc, sc, group=group)
+        recv_counts = [int(v) for v in rc.tolist()]
     recv = send.new_empty((sum(recv_counts),) + tuple(send.shape[1:]))
     dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=recv_counts, input_split_sizes=list(send_counts),
                            group=group)
@@ -503,7 +519,7 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
         warnings.warn("system is not charge neutral; free-space potentials are still defined but the Ewald "
                       "split assumes neutrality", stacklevel=2)
     part = backend.domain_partition(world, int(ntot.item()))
-    cols_of = torch.tensor(part.owner_of_col, dtype=torch.int64, device=dev)
+    cols_of, halo_tab = part.device_tables(dev)
 
     if multi:
         # 1. migrate to the owners
@@ -516,7 +532,6 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
 
         # 2. halo: each own particle to the ranks whose +x halo holds its column
         cx = part.columns(own[:, 0])
-        halo_tab = torch.tensor(part.halo_to, dtype=torch.bool, device=dev)  # (ncols, world)
         # every (own particle, destination) halo pair, grouped by destination
         # (a stable sort of the row-major nonzero list): one host sync for the
         # pairs and one for the counts, whatever the rank count
@@ -585,14 +600,14 @@ def total_potential_domain(pos_local, q_local, backend, group=None, kspace: str 
         return phi_local
 
     # 4. the halo sums back to the owners (the order of step 2)
-    back, _ = _all_to_allv(phi_local[n_own:].contiguous(), halo_counts, group, multi)
+    back, _ = _all_to_allv(phi_local[n_own:].contiguous(), halo_counts, group, multi, recv_counts=hcounts)
     phi_own = phi_local[:n_own] + phik
     if back.numel():
         phi_own.index_add_(0, hidx, back)
     _finish(backend, phi_own, group, multi)
 
     # 6. potentials back to the ranks that passed the particles
-    ret, _ = _all_to_allv(phi_own, own_counts, group, multi)
+    ret, _ = _all_to_allv(phi_own, own_counts, group, multi, recv_counts=send_counts)
     out = torch.empty(n_in, dtype=torch.float64, device=dev)
     out[order] = ret
     return out
@@ -616,7 +631,8 @@ def _slab_kspace_domain(backend, part, kg, grid, rank, world, group, multi):
         send_parts += [flat[lo:hi] for lo, hi in pieces]
         send_counts.append(sum(hi - lo for lo, hi in pieces))
     send = torch.cat(send_parts) if send_parts else flat.new_zeros((0, plane))
-    recv, _ = _all_to_allv(send, send_counts, group, multi)
+    rcounts = [sum(hi - lo for lo, hi in part.exchange_pieces(s, rank, kg)) for s in range(world)]
+    recv, _ = _all_to_allv(send, send_counts, group, multi, recv_counts=rcounts)
     slab = flat.new_zeros((b - a, plane))
     row = 0
     for s in range(world):
@@ -641,7 +657,8 @@ def _slab_kspace_domain(backend, part, kg, grid, rank, world, group, multi):
         parts2 += [sflat[lo - a:hi - a] for lo, hi in pieces]
         counts2.append(sum(hi - lo for lo, hi in pieces))
     send2 = torch.cat(parts2) if parts2 else flat.new_zeros((0, plane))
-    recv2, _ = _all_to_allv(send2, counts2, group, multi)
+    rcounts2 = [sum(hi - lo for lo, hi in part.exchange_pieces(rank, s, kg)) for s in range(world)]
+    recv2, _ = _all_to_allv(send2, counts2, group, multi, recv_counts=rcounts2)
     row = 0
     for s in range(world):
         for lo, hi in part.exchange_pieces(rank, s, kg):
@@ -669,8 +686,9 @@ def _zslab_kspace_domain(backend, part, kg, grid, rank, world, group, multi):
         parts += blocks
         counts.append(sum(int(b.numel()) for b in blocks))
     send = torch.cat(parts) if parts else grid.new_zeros(0)
-    recv, _ = _all_to_allv(send, counts, group, multi)
     nz = me["nz"]
+    rcounts = [sum((hi - lo) * Y * nz for lo, hi in part.touched_pieces(s, kg)) for s in range(world)]
+    recv, _ = _all_to_allv(send, counts, group, multi, recv_counts=rcounts)
     zslab = grid.new_zeros((X, Y, nz))
     off = 0
     for s in range(world):
@@ -698,7 +716,8 @@ def _zslab_kspace_domain(backend, part, kg, grid, rank, world, group, multi):
         parts2 += blocks
         counts2.append(sum(int(b.numel()) for b in blocks))
     send2 = torch.cat(parts2) if parts2 else grid.new_zeros(0)
-    recv2, _ = _all_to_allv(send2, counts2, group, multi)
+    rcounts2 = [sum((hi - lo) * Y * geo[d]["nz"] for lo, hi in mine) for d in range(world)]
+    recv2, _ = _all_to_allv(send2, counts2, group, multi, recv_counts=rcounts2)
     off = 0
     for d in range(world):
         z0, nzd = geo[d]["nz0"], geo[d]["nz"]
