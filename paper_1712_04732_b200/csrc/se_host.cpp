@@ -4,6 +4,7 @@
 // consume.  These are plan-time computations (microseconds), the analogue of
 // the reference's Grid.build / padded_size / windows.fourier /
 // greens.zero_mode_values; no per-particle or per-grid-point work runs here.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -262,6 +263,65 @@ double greens_zero_mode(int D, double R, double kappa) {
     if (D == 0) return R * R * (1.0 - std::cos(t)) / (t * t);
     if (D == 1) return (1.0 - ::j0(t)) / (kappa * kappa) - (R * std::log(R)) * ::j1(t) / kappa;
     return R * R * (1.0 - std::cos(t) - t * std::sin(t)) / (t * t);
+}
+
+// Polynomial pair term of the real-space kernel (se_realspace.cu, pair_poly):
+// Q(t) = xi P(xi^2 rc^2 (t + 1)/2), P(s) = erf(sqrt s)/sqrt s, t in [-1, 1],
+// as the Chebyshev interpolant (long double) of the smallest degree in
+// {20, 24, 28, 32} whose interpolation error, checked on 513 points, stays
+// below a quarter ulp of Q(0) = 2 xi / sqrt(pi) (the rounding of the
+// coefficients to double then adds ~1 ulp of Q, |coefficients| < Q(0) --
+// comparable to the rounding of 1/r at the cutoff).  Monomial coefficients
+// in t go to pc[0..32]; returns the degree, 0 if none suffices (xi rc > ~5).
+static long double pair_P(long double s) {
+    if (s <= 0.0L) return 2.0L / std::sqrt(3.14159265358979323846264338327950288L);
+    const long double x = std::sqrt(s);
+    return std::erf(x) / x;
+}
+
+int pair_poly_fit(double xi_, double rc_, double *pc) {
+    static constexpr int kDegrees[] = {20, 24, 28, 32};
+    const long double xi = xi_, S = (long double)xi_ * xi_ * rc_ * rc_;
+    const long double pi = 3.14159265358979323846264338327950288L;
+    auto fq = [&](long double t) { return xi * pair_P(S * (t + 1.0L) / 2.0L); };
+    const long double qtol = std::ldexp(1.0L, -54) * fq(-1.0L);
+    for (int d : kDegrees) {
+        const int n = d + 1;
+        std::vector<long double> fv(n), c(n), mono(n, 0.0L), Tp(n, 0.0L), Tc(n, 0.0L);
+        for (int j = 0; j < n; ++j) fv[j] = fq(std::cos(pi * (j + 0.5L) / n));
+        for (int m = 0; m < n; ++m) {
+            long double acc = 0.0L;
+            for (int j = 0; j < n; ++j) acc += fv[j] * std::cos(pi * m * (j + 0.5L) / n);
+            c[m] = 2.0L * acc / n;
+        }
+        c[0] /= 2.0L;
+        // Chebyshev -> monomial: T_0 = 1, T_1 = t, T_{m+1} = 2 t T_m - T_{m-1}
+        Tc[0] = 1.0L;
+        for (int m = 0; m < n; ++m) {
+            for (int i = 0; i <= m; ++i) mono[i] += c[m] * Tc[i];
+            std::vector<long double> nx(n, 0.0L);
+            if (m == 0) {
+                if (n > 1) nx[1] = 1.0L;
+            } else {
+                for (int i = 0; i + 1 < n; ++i) nx[i + 1] += 2.0L * Tc[i];
+                for (int i = 0; i < n; ++i) nx[i] -= Tp[i];
+            }
+            Tp = Tc;
+            Tc = nx;
+        }
+        long double err = 0.0L;
+        for (int k = 0; k <= 512; ++k) {
+            const long double t = -1.0L + 2.0L * k / 512.0L;
+            long double p = mono[d];
+            for (int i = d - 1; i >= 0; --i) p = p * t + mono[i];
+            err = std::max(err, std::fabs(p - fq(t)));
+        }
+        if (err <= qtol) {
+            for (int i = 0; i < 33; ++i) pc[i] = i < n ? (double)mono[i] : 0.0;
+            return d;
+        }
+    }
+    return 0;
 }
 
 }  // namespace se

@@ -24,6 +24,9 @@
 //    for small n, realspace.py:98-109, gives the same pair set).
 // Image path (D >= 1 and rc > L/2): all pairs x explicit images
 // (realspace.py:138-165), one thread per target.
+#include <algorithm>
+#include <vector>
+
 #include "se_common.h"
 #include "se_erfc_coeffs.h"
 
@@ -45,6 +48,12 @@ struct RealArgs {
     int dense_min;    // prefilter hits per full batch (of kT x 32) from which the batch is
                       // evaluated densely (all pairs, no compaction); > kT * 32: never
     int64_t n_own;    // domain mode: caller-order particles [0, n_own) get the self term; -1: off
+    // Polynomial pair term (kernels with DEG > 0, see pair_poly):
+    //   erfc(xi r)/r = 1/r - Q(r^2),  Q(u) = sum_i pc[i] t^i,  t = u pscale - 1
+    double rc2x;               // rc^2: the exact cutoff test r^2 < rc^2
+    double pscale;             // 2 / rc^2: u in [0, rc^2] -> t in [-1, 1]
+    double pc[33];             // monomial coefficients in t (degree <= 32)
+    int pdeg;                  // host: degree fitted (0: use erfc_fast)
 };
 
 constexpr double kTwoOverSqrtPi = 1.1283791670955126;  // field mode: c = 2 xi / sqrt(pi)
@@ -214,12 +223,37 @@ __device__ __forceinline__ void erfc_parts(double x, double &p, double &e) {
     e = scale2(exp_neg(x * x, n), n);
 }
 
+// Pair term without exp / erfc: erfc(xi r)/r = 1/r - xi erf(xi r)/(xi r), and
+// erf(x)/x is an entire function of x^2 = xi^2 u, so on u in [0, rc^2] it is a
+// single polynomial in t = u (2/rc^2) - 1 (degree DEG, fitted per plan by
+// fit_pair_poly: Chebyshev interpolant of xi erf(xi sqrt u)/(xi sqrt u) in
+// long double, truncation error below 2e-16 / rc -- the rounding of 1/r at
+// the cutoff; its monomial coefficients are < 1 in magnitude, so Horner in
+// fp64 is well conditioned).  Compared with erfc_fast (a rational transform,
+// a reciprocal, erfcx and exp polynomials, an exponent scale) this is one
+// DFMA for t, DEG DFMAs and one DADD: no MUFU.RCP, no integer work.  The
+// result is exact to the rounding of 1/r plus ~2 ulp of Q in ABSOLUTE terms
+// (the subtraction cancels towards the cutoff, where the term is ~eps/rc).
+// Valid for u in [0, rc^2]; outside, the caller discards the value.
+template <int DEG>
+__device__ __forceinline__ double pair_poly(double u, const RealArgs &a) {
+    const double y = rsqrt_nr(u);
+    const double t = fma(u, a.pscale, -1.0);
+    double p = a.pc[DEG];
+#pragma unroll
+    for (int i = DEG - 1; i >= 0; --i) p = fma(p, t, a.pc[i]);
+    return y - p;
+}
+
 __device__ __forceinline__ double min_image(double d, double L) { return d - L * rint(d / L); }
 __device__ __forceinline__ float min_image_f(float d, float L, float invL) { return d - L * rintf(d * invL); }
 
 constexpr int kWarps = 1;  // warps (units) per block: one, so that the WarpBuf base is
                            // block-uniform (shared addresses fold into [R + UR + imm])
-constexpr int kMinBlocks = 27;  // 27 x (7 KB + 1 KB reserved) of shared memory per SM
+#ifndef SE_RS_MINBLOCKS
+#define SE_RS_MINBLOCKS 27
+#endif
+constexpr int kMinBlocks = SE_RS_MINBLOCKS;  // 27 x (7 KB + 1 KB reserved) of shared memory per SM
 constexpr int kT = 16;     // targets per warp unit: lane l tests target l % 16 against half of a 32-source batch
 constexpr int kDenseMin = 410;  // ~0.8 kT x 32: dense evaluation of a batch from this many prefilter hits
 
@@ -333,6 +367,27 @@ __device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const WB
     const double x = hit_geometry<MI, NEWTON, FLD>(en, true, a, wb, jb, tbase, singular, h);
     hit_value<WIDE, FLD>(x, a, h);
     return h;
+}
+
+// Polynomial path (DEG > 0: NEWTON, no minimum image, potential): one
+// compacted hit (slot tt, source k) -> h.f = erfc(xi r)/r, 0 outside the
+// cutoff or for an invalid (duplicate) slot.  Any zero distance among the
+// hits is a coincidence (the self pair is never compacted with NEWTON).
+template <int DEG, class WB>
+__device__ __forceinline__ void hit_poly(unsigned en, bool valid, const RealArgs &a, const WB &wb, int &singular,
+                                         Hit &h) {
+    h.tt = (int)(en >> 5);
+    h.k = (int)(en & 31u);
+    const double2 t01 = wb.txy[h.tt], t23 = wb.tzq[h.tt];
+    const double2 s01 = wb.sxy[h.k], s23 = wb.szq[h.k];
+    const double dx = t01.x - s01.x, dy = t01.y - s01.y, dz = t23.x - s23.x;
+    const double u = fma(dz, dz, fma(dy, dy, dx * dx));
+    singular |= u < 1e-28 ? 1 : 0;
+    h.ok = valid && u < a.rc2x;
+    const double f = pair_poly<DEG>(u, a);
+    h.f = h.ok ? f : 0.0;
+    h.qt = t23.y;
+    h.qs = s23.y;
 }
 
 // Target side into the lane's private slot; with NEWTON the source side
@@ -449,6 +504,62 @@ __device__ __forceinline__ void dense_batch(WB &wb, int lane, int j, int m, doub
     __syncwarp();
 }
 
+// Dense batch, polynomial pair term (DEG > 0): lane l keeps source l in
+// registers; step t (unrolled, t = 0..kT-1) pairs it with unit target t,
+// the same for all lanes -- the target is a broadcast shared-memory read
+// (2 LDS.128 of one address), its accumulator row acc[tslot(t)][lane] and
+// the target's address are compile-time offsets, and the validity of the
+// (t, source) slot is bit t of one per-lane mask.  Pairs outside the
+// cutoff and invalid slots are computed and multiplied out by a select;
+// the source side leaves with one REDG per source and batch.
+template <int DEG, class WB>
+__device__ __forceinline__ void dense_batch_poly(WB &wb, int lane, int j, int m, double xs, double ys, double zs,
+                                                 double qs, const RealArgs &a, unsigned amask, int tbase, int hs,
+                                                 double *__restrict__ acc_s, int &singular) {
+    // valid (target, this source) pairs as a 16-bit mask over the targets:
+    // active targets, and in the own column only targets t < j
+    unsigned vt = amask & 0xffffu;
+    if (hs >= 0) {
+        const int c = min(max(j - tbase, 0), kT);
+        vt &= (1u << c) - 1u;
+    }
+    if (lane >= m) vt = 0u;
+    double accs = 0.0;
+    int sing = 0;
+    // two targets per step, their polynomials as two interleaved Horner
+    // chains (the chain latency, not the fp64 pipe, bounds one chain per
+    // warp); a rolled loop keeps the code in the instruction cache
+#pragma unroll 2
+    for (int t = 0; t < kT; t += 2) {
+        const int sa = tslot(t), sb = tslot(t + 1);
+        const double2 a01 = wb.txy[sa], a23 = wb.tzq[sa];
+        const double2 b01 = wb.txy[sb], b23 = wb.tzq[sb];
+        const bool va = (vt >> t) & 1u, vb = (vt >> (t + 1)) & 1u;
+        const double dxa = a01.x - xs, dya = a01.y - ys, dza = a23.x - zs;
+        const double dxb = b01.x - xs, dyb = b01.y - ys, dzb = b23.x - zs;
+        const double ua = fma(dza, dza, fma(dya, dya, dxa * dxa));
+        const double ub = fma(dzb, dzb, fma(dyb, dyb, dxb * dxb));
+        sing |= ((va && ua < 1e-28) || (vb && ub < 1e-28)) ? 1 : 0;
+        const double ya = rsqrt_nr(ua), yb = rsqrt_nr(ub);
+        const double ta = fma(ua, a.pscale, -1.0), tb = fma(ub, a.pscale, -1.0);
+        double pa = a.pc[DEG], pb = a.pc[DEG];
+#pragma unroll
+        for (int i = DEG - 1; i >= 0; --i) {
+            pa = fma(pa, ta, a.pc[i]);
+            pb = fma(pb, tb, a.pc[i]);
+        }
+        const double wa = (va && ua < a.rc2x) ? ya - pa : 0.0;
+        const double wb_ = (vb && ub < a.rc2x) ? yb - pb : 0.0;
+        double *slota = &wb.acc[0][sa][lane], *slotb = &wb.acc[0][sb][lane];
+        *slota = fma(qs, wa, *slota);
+        *slotb = fma(qs, wb_, *slotb);
+        accs = fma(a23.y, wa, fma(b23.y, wb_, accs));
+    }
+    singular |= sing;
+    if (lane < m) atomicAdd(acc_s + lane, accs);
+    __syncwarp();
+}
+
 // One batch of <= 32 candidate sources [jb, jb+m) of a neighbour-cell run:
 //  1. fp32 prefilter of all 16 x m (target, source) pairs: lane l tests
 //     targets (l % 8, l % 8 + 8) against sources 8 (l / 8) .. + 7, two tests
@@ -459,7 +570,7 @@ __device__ __forceinline__ void dense_batch(WB &wb, int lane, int j, int m, doub
 //     sources of the target's own column count only if j > t;
 //  2. warp prefix scan of the hit counts and compaction of the hits;
 //  3. the list is evaluated 64 hits at a time (two per lane) on full warps.
-template <bool MI, bool COUNT, bool NEWTON, bool WIDE, bool FLD>
+template <bool MI, bool COUNT, bool NEWTON, bool WIDE, bool FLD, int DEG>
 __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int jb, int j1, double shx, double shy,
                                            double shz, const RealArgs &a, WarpBufT<FLD> &wb, int lane,
                                            const PreTargets &pt, const double3 org, int tbase, int hs,
@@ -538,7 +649,10 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     }
     const int c = __popc(hit);
     if (!COUNT && !FLD && NEWTON && __reduce_add_sync(0xffffffffu, (unsigned)c) >= (unsigned)a.dense_min) {
-        dense_batch<WIDE>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, hs, org, acc_src + jb, singular);
+        if (DEG > 0)
+            dense_batch_poly<DEG>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, hs, acc_src + jb, singular);
+        else
+            dense_batch<WIDE>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, hs, org, acc_src + jb, singular);
         return;
     }
     const int incl = warp_incl_scan(c, lane);
@@ -564,10 +678,15 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
             const unsigned en1 = wb.ent[e0 + lane];
             const unsigned en2 = v2 ? wb.ent[e0 + 32 + lane] : en1;
             Hit h1, h2;
-            const double x1 = hit_geometry<MI, NEWTON, FLD>(en1, true, a, wb, jb, tbase, singular, h1);
-            const double x2 = hit_geometry<MI, NEWTON, FLD>(en2, v2, a, wb, jb, tbase, singular, h2);
-            hit_value<WIDE, FLD>(x1, a, h1);
-            hit_value<WIDE, FLD>(x2, a, h2);
+            if (DEG > 0) {
+                hit_poly<(DEG > 0 ? DEG : 1)>(en1, true, a, wb, singular, h1);
+                hit_poly<(DEG > 0 ? DEG : 1)>(en2, v2, a, wb, singular, h2);
+            } else {
+                const double x1 = hit_geometry<MI, NEWTON, FLD>(en1, true, a, wb, jb, tbase, singular, h1);
+                const double x2 = hit_geometry<MI, NEWTON, FLD>(en2, v2, a, wb, jb, tbase, singular, h2);
+                hit_value<WIDE, FLD>(x1, a, h1);
+                hit_value<WIDE, FLD>(x2, a, h2);
+            }
             if (COUNT) {
                 cnt += (h1.ok ? (NEWTON ? 2 : 1) : 0) + (h2.ok ? (NEWTON ? 2 : 1) : 0);
             } else {
@@ -575,7 +694,11 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
                 apply_hit<NEWTON, FLD>(h2, wb, lane, acc_batch);
             }
         } else if (lane < rem) {
-            const Hit h = eval_hit<MI, NEWTON, WIDE, FLD>(wb.ent[e0 + lane], a, wb, jb, tbase, singular);
+            Hit h;
+            if (DEG > 0)
+                hit_poly<(DEG > 0 ? DEG : 1)>(wb.ent[e0 + lane], true, a, wb, singular, h);
+            else
+                h = eval_hit<MI, NEWTON, WIDE, FLD>(wb.ent[e0 + lane], a, wb, jb, tbase, singular);
             if (COUNT)
                 cnt += h.ok ? (NEWTON ? 2 : 1) : 0;
             else
@@ -605,11 +728,12 @@ __device__ __forceinline__ int zbound(const double4 *__restrict__ rec, int lo, i
 // partial sums of both sides go to acc_src (sorted order, zeroed before) and
 // a finishing kernel scatters them.  Otherwise the full column neighbourhood
 // and direct writes of phi (minimum-image mode for < 5 cells per axis).
-template <bool MI, bool COUNT, bool NEWTON, bool WIDE, bool FLD>
+template <bool MI, bool COUNT, bool NEWTON, bool WIDE, bool FLD, int DEG = 0>
 __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlocks) realspace_cell_kernel(
     const double4 *__restrict__ rec, const int *__restrict__ sidx, const int *__restrict__ starts,
     const int4 *__restrict__ units, const int *__restrict__ nunits, RealArgs a, double *__restrict__ phi,
     double *__restrict__ acc_src, int *__restrict__ flag, unsigned long long *__restrict__ npairs) {
+    static_assert(DEG == 0 || (NEWTON && !MI && !COUNT && !FLD && !WIDE), "polynomial pair term: Newton potential path");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpBufT<FLD> &wb = reinterpret_cast<WarpBufT<FLD> *>(smem_raw)[warp];
@@ -681,7 +805,7 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
 
     auto run = [&](int j0, int j1, double shx, double shy, double shz, int hs) {
         for (int jb = j0; jb < j1; jb += 32)
-            pair_batch<MI, COUNT, NEWTON, WIDE, FLD>(rec, jb, j1, shx, shy, shz, a, wb, lane, pt, org, un.y, hs, acc_src,
+            pair_batch<MI, COUNT, NEWTON, WIDE, FLD, DEG>(rec, jb, j1, shx, shy, shz, a, wb, lane, pt, org, un.y, hs, acc_src,
                                                 singular, cnt);
     };
     if (MI) {
@@ -874,6 +998,20 @@ __global__ void realspace_image_kernel(const double *__restrict__ pos, const dou
     phi[t] = v;
 }
 
+// The polynomial pair term (pair_poly) for this xi, rc: coefficients and
+// degree by pair_poly_fit (se_host.cpp, long double); 0 (erfc_fast) when no
+// degree <= 32 reaches the accuracy (xi rc > ~5) or SE_B200_PAIR_POLY=0.
+static int fit_pair_poly(RealArgs &a) {
+    a.rc2x = a.rc * a.rc;
+    a.pscale = 2.0 / a.rc2x;
+    static const bool off = [] {
+        const char *e = std::getenv("SE_B200_PAIR_POLY");
+        return e && std::atoi(e) == 0;
+    }();
+    a.pdeg = off ? 0 : pair_poly_fit(a.xi, a.rc, a.pc);
+    return a.pdeg;
+}
+
 // Prefilter hits (of kT x 32 slots) from which a batch is evaluated densely
 // (dense_batch).  SE_B200_DENSE_MIN overrides it (A/B runs; > 512 disables).
 static int dense_threshold() {
@@ -1019,7 +1157,18 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
     else if (full)
         args(wide ? realspace_cell_kernel<false, COUNT, false, true, FLD>
                   : realspace_cell_kernel<false, COUNT, false, false, FLD>);
-    else
+    else if constexpr (!COUNT && !FLD) {
+        // the polynomial pair term where it is fitted (pair_poly)
+        switch (wide ? 0 : a.pdeg) {
+            case 20: args(realspace_cell_kernel<false, false, true, false, false, 20>); break;
+            case 24: args(realspace_cell_kernel<false, false, true, false, false, 24>); break;
+            case 28: args(realspace_cell_kernel<false, false, true, false, false, 28>); break;
+            case 32: args(realspace_cell_kernel<false, false, true, false, false, 32>); break;
+            default:
+                args(wide ? realspace_cell_kernel<false, false, true, true, false>
+                          : realspace_cell_kernel<false, false, true, false, false>);
+        }
+    } else
         args(wide ? realspace_cell_kernel<false, COUNT, true, true, FLD>
                   : realspace_cell_kernel<false, COUNT, true, false, FLD>);
     SE_LAUNCH_CHECK();
@@ -1062,6 +1211,7 @@ static void realspace_impl(se_plan *pl, const double *pos, const double *q, int6
     a.rlo = N * rank / world;
     a.rhi = N * (rank + 1) / world;
     set_prefilter(a);
+    if (!FLD) fit_pair_poly(a);
     if (D >= 1 && rc > L / 2 + 1e-12) {
         int layers = (int)std::floor((rc + L / 2) / L) + 1;
         prof_begin(pl, SE_K_REALSPACE);
