@@ -60,7 +60,7 @@ std::vector<double> window_fourier(int window, int P, double h, double shape,
 double window_value(int window, double w, double shape, double x);
 double greens_zero_mode(int D, double R, double kappa);
 // polynomial pair term of the real-space kernel: coefficients, degree (0: none) -- se_host.cpp
-int pair_poly_fit(double xi, double rc, double *pc);
+int pair_poly_fit(double xi, double rc, int kind, double *pc);
 double bessel_i0(double x);
 
 // ---------------------------------------------------------- device buffers

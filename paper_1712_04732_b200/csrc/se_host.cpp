@@ -273,18 +273,25 @@ double greens_zero_mode(int D, double R, double kappa) {
 // coefficients to double then adds ~1 ulp of Q, |coefficients| < Q(0) --
 // comparable to the rounding of 1/r at the cutoff).  Monomial coefficients
 // in t go to pc[0..32]; returns the degree, 0 if none suffices (xi rc > ~5).
+// kind 1: the field's R = Q - (2 xi/sqrt pi) exp(-xi^2 u) instead of Q.
 static long double pair_P(long double s) {
     if (s <= 0.0L) return 2.0L / std::sqrt(3.14159265358979323846264338327950288L);
     const long double x = std::sqrt(s);
     return std::erf(x) / x;
 }
 
-int pair_poly_fit(double xi_, double rc_, double *pc) {
+int pair_poly_fit(double xi_, double rc_, int kind, double *pc) {
     static constexpr int kDegrees[] = {20, 24, 28, 32};
     const long double xi = xi_, S = (long double)xi_ * xi_ * rc_ * rc_;
     const long double pi = 3.14159265358979323846264338327950288L;
-    auto fq = [&](long double t) { return xi * pair_P(S * (t + 1.0L) / 2.0L); };
-    const long double qtol = std::ldexp(1.0L, -54) * fq(-1.0L);
+    // kind 1 (field): R = Q - (2 xi / sqrt pi) exp(-s), the factor of
+    // g = (erfc(x)/r + (2 xi/sqrt pi) exp(-x^2))/r^2 = (1/r^2)(1/r - R)
+    const long double c2 = 2.0L / std::sqrt(pi);
+    auto fq = [&](long double t) {
+        const long double s = S * (t + 1.0L) / 2.0L;
+        return xi * (pair_P(s) - (kind == 1 ? c2 * std::exp(-s) : 0.0L));
+    };
+    const long double qtol = std::ldexp(1.0L, -54) * xi * c2;  // a quarter ulp of Q(0) = 2 xi / sqrt(pi)
     for (int d : kDegrees) {
         const int n = d + 1;
         std::vector<long double> fv(n), c(n), mono(n, 0.0L), Tp(n, 0.0L), Tc(n, 0.0L);

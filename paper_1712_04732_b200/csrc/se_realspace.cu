@@ -265,6 +265,7 @@ struct __align__(16) WarpBufT {
     double2 sxy[32], szq[32];    // current source batch, likewise (16-B stride: a warp's
                                  // random reads cost the minimum 4 wavefronts per LDS.128)
     float4 sf[32];               // the same in fp32 for the prefilter
+    float4 tf[kT];               // unit targets relative to the unit origin, fp32 (w: 1 if inactive)
     double acc[FLD ? 3 : 1][kT][32];  // per-lane private accumulators acc[c][t][lane]: lane-owned banks
     unsigned short ent[kT * 32];  // compacted hits of a batch: (target slot << 5) | source
 };
@@ -299,6 +300,7 @@ struct Hit {
     double qt;  // target charge (source-side update with NEWTON)
     double qs;  // source charge (target-side update)
     double dx, dy, dz;  // x_t - x_s (field mode)
+    double u;           // r^2 as evaluated (field mode, polynomial pair term)
     int tt, k;
     bool ok;
 };
@@ -341,6 +343,7 @@ __device__ __forceinline__ double hit_geometry(unsigned en, bool valid, const Re
         h.dx = dx;
         h.dy = dy;
         h.dz = dz;
+        h.u = r2s;
     }
     return a.xi * rr;
 }
@@ -358,6 +361,19 @@ __device__ __forceinline__ void hit_value(double x, const RealArgs &a, Hit &h) {
     } else {
         h.f = erfc_fast<WIDE>(x, h.f);
     }
+}
+
+// Field mode with the polynomial pair term: g = (erfc(x)/r + c exp(-x^2))/r^2
+// = w^2 (w - R(r^2)), R(u) = Q(u) - c exp(-xi^2 u) -- one entire function,
+// fitted like Q (pair_poly_fit, kind 1); w = 1/r, or 0 outside the cutoff.
+template <int DEG>
+__device__ __forceinline__ void hit_value_field_poly(const RealArgs &a, Hit &h) {
+    const double t = fma(h.u, a.pscale, -1.0);
+    double p = a.pc[DEG];
+#pragma unroll
+    for (int i = DEG - 1; i >= 0; --i) p = fma(p, t, a.pc[i]);
+    const double w = h.f;
+    h.f = (w * w) * (w - p);
 }
 
 template <bool MI, bool NEWTON, bool WIDE, bool FLD, class WB>
@@ -413,7 +429,11 @@ __device__ __forceinline__ void apply_hit(const Hit &h, WarpBufT<FLD> &wb, int l
     }
     double *slot = &wb.acc[0][h.tt][lane];
     *slot = fma(h.qs, h.f, *slot);
+#ifdef SE_AB_NO_REDG  // timing experiment only (wrong results): no source-side reductions
+    if (NEWTON && h.ok && h.f == 123.0) atomicAdd(acc_batch + h.k, h.qt * h.f);
+#else
     if (NEWTON && h.ok) atomicAdd(acc_batch + h.k, h.qt * h.f);
+#endif
 }
 
 // Packed fp32x2 arithmetic (FFMA2 / FADD2, sm_100): two prefilter tests per
@@ -505,41 +525,40 @@ __device__ __forceinline__ void dense_batch(WB &wb, int lane, int j, int m, doub
 }
 
 // Dense batch, polynomial pair term (DEG > 0): lane l keeps source l in
-// registers; step t (unrolled, t = 0..kT-1) pairs it with unit target t,
-// the same for all lanes -- the target is a broadcast shared-memory read
-// (2 LDS.128 of one address), its accumulator row acc[tslot(t)][lane] and
-// the target's address are compile-time offsets, and the validity of the
-// (t, source) slot is bit t of one per-lane mask.  Pairs outside the
-// cutoff and invalid slots are computed and multiplied out by a select;
-// the source side leaves with one REDG per source and batch.
-template <int DEG, class WB>
+// registers; step t pairs it with unit target t, the same for all lanes --
+// the target is a broadcast shared-memory read (2 LDS.128 of one address)
+// and its accumulator row acc[tslot(t)][lane] a lane-private slot.  Two
+// targets per step, their polynomials as two interleaved Horner chains
+// (one chain per warp is latency bound); a rolled loop keeps the code in
+// the instruction cache.  Inactive target slots and sources past the run's
+// end sit far away (r > rc), so outside the own column (OWN = false) the
+// only test per slot is r^2 < rc^2 -- on the integer bits of r^2 (ALU, not
+// the fp64 pipe), as is the coincidence test 1/r > 1e14 (r < 1e-14).  In
+// the own column (OWN) only targets t < j count (the pair j <= t is visited
+// from j's side).  The source side leaves with one REDG per source and batch.
+__device__ __forceinline__ bool below_bits(double u, long long lim) { return __double_as_longlong(u) < lim; }
+
+template <int DEG, bool OWN, class WB>
 __device__ __forceinline__ void dense_batch_poly(WB &wb, int lane, int j, int m, double xs, double ys, double zs,
-                                                 double qs, const RealArgs &a, unsigned amask, int tbase, int hs,
+                                                 double qs, const RealArgs &a, unsigned amask, int tbase,
                                                  double *__restrict__ acc_s, int &singular) {
-    // valid (target, this source) pairs as a 16-bit mask over the targets:
-    // active targets, and in the own column only targets t < j
-    unsigned vt = amask & 0xffffu;
-    if (hs >= 0) {
+    unsigned vt = 0xffffu;
+    if (OWN) {
         const int c = min(max(j - tbase, 0), kT);
-        vt &= (1u << c) - 1u;
+        vt = amask & ((1u << c) - 1u);
     }
-    if (lane >= m) vt = 0u;
+    const long long lim = __double_as_longlong(a.rc2x);  // r^2 >= 0: bit order = value order
     double accs = 0.0;
-    int sing = 0;
-    // two targets per step, their polynomials as two interleaved Horner
-    // chains (the chain latency, not the fp64 pipe, bounds one chain per
-    // warp); a rolled loop keeps the code in the instruction cache
+    bool sing = false;
 #pragma unroll 2
     for (int t = 0; t < kT; t += 2) {
         const int sa = tslot(t), sb = tslot(t + 1);
         const double2 a01 = wb.txy[sa], a23 = wb.tzq[sa];
         const double2 b01 = wb.txy[sb], b23 = wb.tzq[sb];
-        const bool va = (vt >> t) & 1u, vb = (vt >> (t + 1)) & 1u;
         const double dxa = a01.x - xs, dya = a01.y - ys, dza = a23.x - zs;
         const double dxb = b01.x - xs, dyb = b01.y - ys, dzb = b23.x - zs;
         const double ua = fma(dza, dza, fma(dya, dya, dxa * dxa));
         const double ub = fma(dzb, dzb, fma(dyb, dyb, dxb * dxb));
-        sing |= ((va && ua < 1e-28) || (vb && ub < 1e-28)) ? 1 : 0;
         const double ya = rsqrt_nr(ua), yb = rsqrt_nr(ub);
         const double ta = fma(ua, a.pscale, -1.0), tb = fma(ub, a.pscale, -1.0);
         double pa = a.pc[DEG], pb = a.pc[DEG];
@@ -548,14 +567,21 @@ __device__ __forceinline__ void dense_batch_poly(WB &wb, int lane, int j, int m,
             pa = fma(pa, ta, a.pc[i]);
             pb = fma(pb, tb, a.pc[i]);
         }
-        const double wa = (va && ua < a.rc2x) ? ya - pa : 0.0;
-        const double wb_ = (vb && ub < a.rc2x) ? yb - pb : 0.0;
+        bool oka = below_bits(ua, lim), okb = below_bits(ub, lim);
+        if (OWN) {
+            oka = oka && ((vt >> t) & 1u);
+            okb = okb && ((vt >> (t + 1)) & 1u);
+        }
+        // 1/r > 1e14 (hi word): r < 1e-14, a coincidence (realspace.py:118-122)
+        sing = sing || (oka && __double2hiint(ya) > 0x42D6BCC4) || (okb && __double2hiint(yb) > 0x42D6BCC4);
+        const double wa = oka ? ya - pa : 0.0;
+        const double wb_ = okb ? yb - pb : 0.0;
         double *slota = &wb.acc[0][sa][lane], *slotb = &wb.acc[0][sb][lane];
         *slota = fma(qs, wa, *slota);
         *slotb = fma(qs, wb_, *slotb);
         accs = fma(a23.y, wa, fma(b23.y, wb_, accs));
     }
-    singular |= sing;
+    singular |= sing ? 1 : 0;
     if (lane < m) atomicAdd(acc_s + lane, accs);
     __syncwarp();
 }
@@ -570,15 +596,18 @@ __device__ __forceinline__ void dense_batch_poly(WB &wb, int lane, int j, int m,
 //     sources of the target's own column count only if j > t;
 //  2. warp prefix scan of the hit counts and compaction of the hits;
 //  3. the list is evaluated 64 hits at a time (two per lane) on full warps.
-template <bool MI, bool COUNT, bool NEWTON, bool WIDE, bool FLD, int DEG>
+template <bool MI, bool COUNT, bool NEWTON, bool WIDE, bool FLD, int DEGP>
 __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int jb, int j1, double shx, double shy,
                                            double shz, const RealArgs &a, WarpBufT<FLD> &wb, int lane,
                                            const PreTargets &pt, const double3 org, int tbase, int hs,
                                            double *__restrict__ acc_src, int &singular, long long &cnt) {
+    // polynomial pair term: DEG for the Newton potential, DEGF for the field
+    constexpr int DEG = FLD ? 0 : DEGP, DEGF = FLD ? DEGP : 0;
     const int j = jb + lane;
     // the lane's own source stays in registers for the dense path (zero
     // past the end of the run: finite, never evaluated)
-    double xs = 0.0, ys = 0.0, zs = 0.0, qs = 0.0;
+    const double far = -(8.0 * a.L + 4.0 * a.rc);  // past the end: r > rc from every target
+    double xs = far, ys = far, zs = far, qs = 0.0;
     if (j < j1) {
         const double4 r = rec[j];
         if (j + 32 < j1) prefetch_l1(rec + j + 32);  // the run's next batch
@@ -649,9 +678,13 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
     }
     const int c = __popc(hit);
     if (!COUNT && !FLD && NEWTON && __reduce_add_sync(0xffffffffu, (unsigned)c) >= (unsigned)a.dense_min) {
-        if (DEG > 0)
-            dense_batch_poly<DEG>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, hs, acc_src + jb, singular);
-        else
+        if (DEG > 0) {
+            if (hs >= 0)
+                dense_batch_poly<DEG, true>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, acc_src + jb, singular);
+            else
+                dense_batch_poly<DEG, false>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, acc_src + jb,
+                                             singular);
+        } else
             dense_batch<WIDE>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, hs, org, acc_src + jb, singular);
         return;
     }
@@ -684,8 +717,13 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
             } else {
                 const double x1 = hit_geometry<MI, NEWTON, FLD>(en1, true, a, wb, jb, tbase, singular, h1);
                 const double x2 = hit_geometry<MI, NEWTON, FLD>(en2, v2, a, wb, jb, tbase, singular, h2);
-                hit_value<WIDE, FLD>(x1, a, h1);
-                hit_value<WIDE, FLD>(x2, a, h2);
+                if (FLD && DEGF > 0) {
+                    hit_value_field_poly<(DEGF > 0 ? DEGF : 1)>(a, h1);
+                    hit_value_field_poly<(DEGF > 0 ? DEGF : 1)>(a, h2);
+                } else {
+                    hit_value<WIDE, FLD>(x1, a, h1);
+                    hit_value<WIDE, FLD>(x2, a, h2);
+                }
             }
             if (COUNT) {
                 cnt += (h1.ok ? (NEWTON ? 2 : 1) : 0) + (h2.ok ? (NEWTON ? 2 : 1) : 0);
@@ -695,10 +733,14 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
             }
         } else if (lane < rem) {
             Hit h;
-            if (DEG > 0)
+            if (DEG > 0) {
                 hit_poly<(DEG > 0 ? DEG : 1)>(wb.ent[e0 + lane], true, a, wb, singular, h);
-            else
+            } else if (FLD && DEGF > 0) {
+                hit_geometry<MI, NEWTON, FLD>(wb.ent[e0 + lane], true, a, wb, jb, tbase, singular, h);
+                hit_value_field_poly<(DEGF > 0 ? DEGF : 1)>(a, h);
+            } else {
                 h = eval_hit<MI, NEWTON, WIDE, FLD>(wb.ent[e0 + lane], a, wb, jb, tbase, singular);
+            }
             if (COUNT)
                 cnt += h.ok ? (NEWTON ? 2 : 1) : 0;
             else
@@ -733,7 +775,8 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
     const double4 *__restrict__ rec, const int *__restrict__ sidx, const int *__restrict__ starts,
     const int4 *__restrict__ units, const int *__restrict__ nunits, RealArgs a, double *__restrict__ phi,
     double *__restrict__ acc_src, int *__restrict__ flag, unsigned long long *__restrict__ npairs) {
-    static_assert(DEG == 0 || (NEWTON && !MI && !COUNT && !FLD && !WIDE), "polynomial pair term: Newton potential path");
+    static_assert(DEG == 0 || (!MI && !COUNT && !WIDE && (FLD ? !NEWTON : NEWTON)),
+                  "polynomial pair term: the Newton potential and the full-shell field paths");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpBufT<FLD> &wb = reinterpret_cast<WarpBufT<FLD> *>(smem_raw)[warp];
@@ -749,7 +792,9 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
     const int t = un.y + tl;
     const bool active = tl < un.z && t >= a.rlo && t < a.rhi;
     if (__ballot_sync(0xffffffffu, active) == 0) return;
-    const double4 tp = active ? rec[t] : make_double4(0, 0, 0, 0);
+    // inactive slots far away (r > rc from every source; dense_batch_poly)
+    const double farT = 8.0 * a.L + 4.0 * a.rc;
+    const double4 tp = active ? rec[t] : make_double4(farT, farT, farT, 0);
     if (lane < kT) {
         wb.txy[tslot(lane)] = make_double2(tp.x, tp.y);
         wb.tzq[tslot(lane)] = make_double2(tp.z, tp.w);
@@ -768,6 +813,9 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
     // to org = (column corner, zmin); the fp32 rounding margin of the expanded
     // form scales with the operand magnitudes: |t'| <= Rt, |s'| <= Rt + rc
     const double3 org = make_double3(cx * a.edge, cy * a.edge, zmin);
+    if (lane < kT)
+        wb.tf[lane] = make_float4((float)(tp.x - org.x), (float)(tp.y - org.y), (float)(tp.z - org.z), active ? 0.f : 1.f);
+    __syncwarp();
     PreTargets pt;
     {
         const double Rt = 1.4143 * a.edge + (zmax - zmin), Rs = Rt + 1.01 * a.rc;
@@ -858,14 +906,37 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
             } else {
                 ok = ok && yc >= 0 && yc < n;
             }
-            const double gx = max(abs(ox - cx) - 1, 0) * a.edge, gy = max(abs(oy - cy) - 1, 0) * a.edge;
-            const double h2 = a.rc2 - gx * gx - gy * gy;
-            ok = ok && h2 >= 0.0;
+            // the z-window: sources within rc of some target t satisfy
+            // |z_s - z_t| <= h_t, h_t^2 = rc^2 - (lateral distance from t to
+            // the source column's cell)^2 -- per target (the unit's targets
+            // spread over their own column's cross-section: ~10% fewer
+            // candidates than one window from the two cells' gap)
+            // (fp32 relative to the unit origin; h_t from h_t^2 + eps2, eps2 =
+            // 4e-6 rc^2 above the fp32 error of h_t^2, and 1e-5 rc more on
+            // each side: a superset of the exact window)
+            double wlo = 1e300, whi = -1e300;
+            if (ok) {
+                const float x0 = (float)((ox - cx) * a.edge), y0 = (float)((oy - cy) * a.edge), e = (float)a.edge;
+                const float rc2f = (float)a.rc2, eps2 = 4e-6f * rc2f;
+                float lo = 3e38f, hi = -3e38f;
+                for (int tt = 0; tt < kT; ++tt) {
+                    const float4 q = wb.tf[tt];
+                    const float gxt = fmaxf(0.f, fmaxf(x0 - q.x, q.x - (x0 + e)));
+                    const float gyt = fmaxf(0.f, fmaxf(y0 - q.y, q.y - (y0 + e)));
+                    const float h2t = rc2f - gxt * gxt - gyt * gyt;
+                    if (q.w == 0.f && h2t >= -eps2) {
+                        const float ht = sqrtf(h2t + eps2);
+                        lo = fminf(lo, q.z - ht);
+                        hi = fmaxf(hi, q.z + ht);
+                    }
+                }
+                ok = lo <= hi;
+                wlo = org.z + (double)lo - 1e-5 * a.rc;
+                whi = org.z + (double)hi + 1e-5 * a.rc;
+            }
             if (ok) {
                 cs = starts[xc * n + yc];
                 ce = starts[xc * n + yc + 1];
-                const double h = sqrt(h2);
-                const double wlo = zmin - h, whi = zmax + h;
                 const bool own = NEWTON && lane == 0;  // own column: sources above the unit only
                 j0 = own ? un.y + 1 : zbound(rec, cs, ce, zq(wlo, a.qinv) - 1, false, a.qinv);
                 j1 = zbound(rec, j0, ce, zq(whi, a.qinv) + 1, true, a.qinv);
@@ -1001,14 +1072,14 @@ __global__ void realspace_image_kernel(const double *__restrict__ pos, const dou
 // The polynomial pair term (pair_poly) for this xi, rc: coefficients and
 // degree by pair_poly_fit (se_host.cpp, long double); 0 (erfc_fast) when no
 // degree <= 32 reaches the accuracy (xi rc > ~5) or SE_B200_PAIR_POLY=0.
-static int fit_pair_poly(RealArgs &a) {
+static int fit_pair_poly(RealArgs &a, int kind) {
     a.rc2x = a.rc * a.rc;
     a.pscale = 2.0 / a.rc2x;
     static const bool off = [] {
         const char *e = std::getenv("SE_B200_PAIR_POLY");
         return e && std::atoi(e) == 0;
     }();
-    a.pdeg = off ? 0 : pair_poly_fit(a.xi, a.rc, a.pc);
+    a.pdeg = off ? 0 : pair_poly_fit(a.xi, a.rc, kind, a.pc);
     return a.pdeg;
 }
 
@@ -1154,9 +1225,22 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
     if (mi)
         args(wide ? realspace_cell_kernel<true, COUNT, false, true, FLD>
                   : realspace_cell_kernel<true, COUNT, false, false, FLD>);
-    else if (full)
-        args(wide ? realspace_cell_kernel<false, COUNT, false, true, FLD>
-                  : realspace_cell_kernel<false, COUNT, false, false, FLD>);
+    else if (full) {
+        if constexpr (FLD && !COUNT) {
+            switch (wide || pl->deterministic ? 0 : a.pdeg) {
+                case 20: args(realspace_cell_kernel<false, false, false, false, true, 20>); break;
+                case 24: args(realspace_cell_kernel<false, false, false, false, true, 24>); break;
+                case 28: args(realspace_cell_kernel<false, false, false, false, true, 28>); break;
+                case 32: args(realspace_cell_kernel<false, false, false, false, true, 32>); break;
+                default:
+                    args(wide ? realspace_cell_kernel<false, false, false, true, true>
+                              : realspace_cell_kernel<false, false, false, false, true>);
+            }
+        } else {
+            args(wide ? realspace_cell_kernel<false, COUNT, false, true, FLD>
+                      : realspace_cell_kernel<false, COUNT, false, false, FLD>);
+        }
+    }
     else if constexpr (!COUNT && !FLD) {
         // the polynomial pair term where it is fitted (pair_poly)
         switch (wide ? 0 : a.pdeg) {
@@ -1211,7 +1295,7 @@ static void realspace_impl(se_plan *pl, const double *pos, const double *q, int6
     a.rlo = N * rank / world;
     a.rhi = N * (rank + 1) / world;
     set_prefilter(a);
-    if (!FLD) fit_pair_poly(a);
+    fit_pair_poly(a, FLD ? 1 : 0);
     if (D >= 1 && rc > L / 2 + 1e-12) {
         int layers = (int)std::floor((rc + L / 2) / L) + 1;
         prof_begin(pl, SE_K_REALSPACE);
