@@ -336,7 +336,7 @@ def _source_hash(files):
 
 
 REALSPACE_SOURCES = ("paper_1712_04732_b200/csrc/se_realspace.cu", "paper_1712_04732_b200/csrc/se_erfc_coeffs.h",
-                     "paper_1712_04732_b200/csrc/se_common.h")
+                     "paper_1712_04732_b200/csrc/se_common.h", "paper_1712_04732_b200/csrc/se_host.cpp")
 
 
 def ncu_evidence():

@@ -538,10 +538,18 @@ __device__ __forceinline__ void dense_batch(WB &wb, int lane, int j, int m, doub
 // from j's side).  The source side leaves with one REDG per source and batch.
 __device__ __forceinline__ bool below_bits(double u, long long lim) { return __double_as_longlong(u) < lim; }
 
+#ifndef SE_DENSE_NT
+#define SE_DENSE_NT 2  // targets (interleaved Horner chains) per step
+#endif
+#ifndef SE_DENSE_UNROLL
+#define SE_DENSE_UNROLL 1  // measured: 1 beats 2 by 2-4% (cfg2, cfg5, cfg4)
+#endif
+constexpr int kDenseUnroll = SE_DENSE_UNROLL;
 template <int DEG, bool OWN, class WB>
 __device__ __forceinline__ void dense_batch_poly(WB &wb, int lane, int j, int m, double xs, double ys, double zs,
                                                  double qs, const RealArgs &a, unsigned amask, int tbase,
                                                  double *__restrict__ acc_s, int &singular) {
+    constexpr int NT = SE_DENSE_NT;
     unsigned vt = 0xffffu;
     if (OWN) {
         const int c = min(max(j - tbase, 0), kT);
@@ -550,36 +558,38 @@ __device__ __forceinline__ void dense_batch_poly(WB &wb, int lane, int j, int m,
     const long long lim = __double_as_longlong(a.rc2x);  // r^2 >= 0: bit order = value order
     double accs = 0.0;
     bool sing = false;
-#pragma unroll 2
-    for (int t = 0; t < kT; t += 2) {
-        const int sa = tslot(t), sb = tslot(t + 1);
-        const double2 a01 = wb.txy[sa], a23 = wb.tzq[sa];
-        const double2 b01 = wb.txy[sb], b23 = wb.tzq[sb];
-        const double dxa = a01.x - xs, dya = a01.y - ys, dza = a23.x - zs;
-        const double dxb = b01.x - xs, dyb = b01.y - ys, dzb = b23.x - zs;
-        const double ua = fma(dza, dza, fma(dya, dya, dxa * dxa));
-        const double ub = fma(dzb, dzb, fma(dyb, dyb, dxb * dxb));
-        const double ya = rsqrt_nr(ua), yb = rsqrt_nr(ub);
-        const double ta = fma(ua, a.pscale, -1.0), tb = fma(ub, a.pscale, -1.0);
-        double pa = a.pc[DEG], pb = a.pc[DEG];
+#pragma unroll kDenseUnroll
+    for (int t = 0; t < kT; t += NT) {
+        int sl[NT];
+        double2 p01[NT], p23[NT];
+        double u[NT], y[NT], tv[NT], p[NT];
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+            sl[k] = tslot(t + k);
+            p01[k] = wb.txy[sl[k]];
+            p23[k] = wb.tzq[sl[k]];
+            const double dx = p01[k].x - xs, dy = p01[k].y - ys, dz = p23[k].x - zs;
+            u[k] = fma(dz, dz, fma(dy, dy, dx * dx));
+            y[k] = rsqrt_nr(u[k]);
+            tv[k] = fma(u[k], a.pscale, -1.0);
+            p[k] = a.pc[DEG];
+        }
 #pragma unroll
         for (int i = DEG - 1; i >= 0; --i) {
-            pa = fma(pa, ta, a.pc[i]);
-            pb = fma(pb, tb, a.pc[i]);
+#pragma unroll
+            for (int k = 0; k < NT; ++k) p[k] = fma(p[k], tv[k], a.pc[i]);
         }
-        bool oka = below_bits(ua, lim), okb = below_bits(ub, lim);
-        if (OWN) {
-            oka = oka && ((vt >> t) & 1u);
-            okb = okb && ((vt >> (t + 1)) & 1u);
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+            bool ok = below_bits(u[k], lim);
+            if (OWN) ok = ok && ((vt >> (t + k)) & 1u);
+            // 1/r > 1e14 (hi word): r < 1e-14, a coincidence (realspace.py:118-122)
+            sing = sing || (ok && __double2hiint(y[k]) > 0x42D6BCC4);
+            const double w = ok ? y[k] - p[k] : 0.0;
+            double *slot = &wb.acc[0][sl[k]][lane];
+            *slot = fma(qs, w, *slot);
+            accs = fma(p23[k].y, w, accs);
         }
-        // 1/r > 1e14 (hi word): r < 1e-14, a coincidence (realspace.py:118-122)
-        sing = sing || (oka && __double2hiint(ya) > 0x42D6BCC4) || (okb && __double2hiint(yb) > 0x42D6BCC4);
-        const double wa = oka ? ya - pa : 0.0;
-        const double wb_ = okb ? yb - pb : 0.0;
-        double *slota = &wb.acc[0][sa][lane], *slotb = &wb.acc[0][sb][lane];
-        *slota = fma(qs, wa, *slota);
-        *slotb = fma(qs, wb_, *slotb);
-        accs = fma(a23.y, wa, fma(b23.y, wb_, accs));
     }
     singular |= sing ? 1 : 0;
     if (lane < m) atomicAdd(acc_s + lane, accs);

@@ -23,7 +23,7 @@ sys.path.insert(0, ROOT)
 
 SOURCES = {
     "realspace": ("paper_1712_04732_b200/csrc/se_realspace.cu", "paper_1712_04732_b200/csrc/se_erfc_coeffs.h",
-                  "paper_1712_04732_b200/csrc/se_common.h"),
+                  "paper_1712_04732_b200/csrc/se_common.h", "paper_1712_04732_b200/csrc/se_host.cpp"),
     "spread": ("paper_1712_04732_b200/csrc/se_spread.cu", "paper_1712_04732_b200/csrc/se_common.h"),
     "gather": ("paper_1712_04732_b200/csrc/se_spread.cu", "paper_1712_04732_b200/csrc/se_common.h"),
 }
