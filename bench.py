@@ -575,7 +575,7 @@ def run_ours(args):
                      "frac_of_hbm": frac(comp / t, pk["hbm_gbs"] * 1e9)}
         spread_gather = {"updates_per_launch": N * P3, **sg,
                          "peaks": {"smem_tbs": pk["smem_tbs"], "hbm_gbs": pk["hbm_gbs"], "source": pk["fp64_src"]}}
-    roofline = {"kernel": "realspace_cell_kernel (erfc pair sum)", "bound": "fp64",
+    roofline = {"kernel": "realspace_cell_kernel (erfc pair sum, polynomial pair term 1/r - Q(r^2))", "bound": "fp64",
                 "achieved": achieved, "peak": pk["fp64_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / pk["fp64_tflops"], "traffic": None,
                 "peak_source": pk["fp64_src"],

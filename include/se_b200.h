@@ -92,6 +92,14 @@ int se_grid_build(int D, double L, const se_params_t *p, se_grid_t *out);
 /* aft.padded_size (aft.py:76-84) and aft.next_even_smooth (aft.py:68-73). */
 int se_padded_size(double s, int32_t n, int32_t *out);
 int se_next_even_smooth(int32_t n, int32_t *out);
+/* The real-space kernel's polynomial pair term for (xi, rc): erfc(xi r)/r =
+ * 1/r - Q(r^2) (kind 0, potential) or (erfc(xi r)/r + 2 xi/sqrt(pi)
+ * exp(-xi^2 r^2))/r^2 = (1/r - R(r^2))/r^2 (kind 1, field), Q / R =
+ * sum_i coeffs[i] t^i, t = 2 r^2 / rc^2 - 1 (replaces the erfc of
+ * realspace.py:123-126 inside the kernel).  coeffs: 33 doubles; *degree =
+ * 20..32, or 0 when no degree <= 32 reaches the kernel's accuracy (xi rc >
+ * ~5: the kernel then evaluates erfc directly). */
+int se_pair_poly_coefficients(double xi, double rc, int kind, double *coeffs, int32_t *degree);
 /* precompute_truncated_greens geometry (sekspace.py:266-279): nconv, fine g0, R. */
 int se_d0_kernel_geometry(double L, int32_t M, int32_t P, double s0, double rc,
                           int32_t *nconv, int32_t *g0, double *R);

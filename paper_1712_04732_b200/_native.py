@@ -48,6 +48,7 @@ SIGNATURES = {
     "se_grid_build": [ctypes.c_int, ctypes.c_double, ctypes.POINTER(se_params_t), ctypes.POINTER(se_grid_t)],
     "se_padded_size": [ctypes.c_double, ctypes.c_int32, c_int32_p],
     "se_next_even_smooth": [ctypes.c_int32, c_int32_p],
+    "se_pair_poly_coefficients": [ctypes.c_double, ctypes.c_double, ctypes.c_int, _P, c_int32_p],
     "se_d0_kernel_geometry": [ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                               ctypes.c_double, c_int32_p, c_int32_p, c_double_p],
     "se_mode_partition_counts": [ctypes.c_int32, ctypes.c_int, ctypes.c_int32, c_int64_p, c_int64_p],

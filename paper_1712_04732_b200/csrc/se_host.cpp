@@ -383,6 +383,15 @@ int se_next_even_smooth(int32_t n, int32_t *out) {
     SE_API_END
 }
 
+int se_pair_poly_coefficients(double xi, double rc, int kind, double *coeffs, int32_t *degree) {
+    SE_API_BEGIN
+    if (!coeffs || !degree) fail(SE_EINVAL, "null argument");
+    if (!(xi > 0) || !(rc > 0)) fail(SE_EINVAL, "xi and rc must be positive");
+    if (kind != 0 && kind != 1) fail(SE_EINVAL, "kind must be 0 (potential) or 1 (field)");
+    *degree = pair_poly_fit(xi, rc, kind, coeffs);
+    SE_API_END
+}
+
 int se_d0_kernel_geometry(double L, int32_t M, int32_t P, double s0, double rc, int32_t *nconv,
                           int32_t *g0, double *R) {
     SE_API_BEGIN

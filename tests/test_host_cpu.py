@@ -186,3 +186,51 @@ def test_product_package_does_not_import_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "se_oracle" not in src and "oracle/" not in src, f
+
+
+def _pair_poly(xi, rc, kind):
+    c = np.zeros(33)
+    deg = ctypes.c_int32(0)
+    _native.call("se_pair_poly_coefficients", xi, rc, kind, c.ctypes.data_as(ctypes.c_void_p), ctypes.byref(deg))
+    return c, deg.value
+
+
+@pytest.mark.parametrize("xi,rc", [(4.2919, 1.0), (4.5501, 1.0), (8.0, 0.4), (14.31, 0.3), (3.0, 1.0), (10.0, 0.45)])
+def test_pair_poly_reproduces_the_erfc_pair_term(xi, rc):
+    # the real-space kernel's pair term 1/r - Q(r^2) (potential) and
+    # (1/r - R(r^2)) / r^2 (field) against 30-digit values of
+    # erfc(xi r)/r (realspace.py:123-126) and the field kernel, evaluated in
+    # fp64 exactly as the kernel does (Horner in t = 2 r^2/rc^2 - 1): the
+    # absolute error is of the order of the rounding of 1/r (err * r small)
+    import mpmath as mp
+    mp.mp.dps = 30
+    r = np.concatenate([np.linspace(1e-4, 1.0, 700) * rc, [rc * (1 - 1e-12)]])
+    u = r * r
+    t = u * (2.0 / (rc * rc)) - 1.0
+    y = 1.0 / np.sqrt(u)
+    for kind in (0, 1):
+        c, deg = _pair_poly(xi, rc, kind)
+        assert deg in (20, 24, 28, 32), deg
+        assert np.all(c[deg + 1:] == 0.0)
+        p = np.full_like(t, c[deg])
+        for i in range(deg - 1, -1, -1):
+            p = p * t + c[i]
+        if kind == 0:
+            got = y - p
+            want = np.array([float(mp.erfc(mp.mpf(xi) * mp.mpf(v)) / mp.mpf(v)) for v in r])
+            assert np.max(np.abs(got - want) * r) < 6e-16
+        else:
+            got = (y - p) * y * y
+            want = np.array([float((mp.erfc(mp.mpf(xi) * mp.mpf(v)) / mp.mpf(v)
+                                    + 2 * mp.mpf(xi) / mp.sqrt(mp.pi) * mp.exp(-(mp.mpf(xi) * mp.mpf(v)) ** 2))
+                                   / mp.mpf(v) ** 2) for v in r])
+            assert np.max(np.abs(got - want) * r ** 3) < 1e-15
+
+
+def test_pair_poly_declines_wide_cutoffs_and_checks_arguments():
+    c, deg = _pair_poly(6.0, 1.0, 0)  # xi rc = 6: erfc(6) ~ 2e-17, the kernel evaluates erfc directly
+    assert deg == 0
+    with pytest.raises(ValueError):
+        _pair_poly(-1.0, 1.0, 0)
+    with pytest.raises(ValueError):
+        _pair_poly(4.0, 1.0, 2)
