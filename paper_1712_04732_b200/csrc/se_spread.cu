@@ -133,15 +133,31 @@ __global__ void tile_keys_hist_kernel(const double *__restrict__ pos, int64_t N,
         if (hist[b]) atomicAdd(&counts[b], hist[b]);
 }
 
-// Stage the 3P window factors of a batch of particles.  wts layout:
-// [p][axis][t]; loc: [p][4] = the local start (x, y, z) within the padded
-// tile as bytes 0..2 of loc[p][0] (one broadcast LDS.32 for the consumers
-// instead of three; each axis task writes its own byte), loc[p][3] = the
-// sorted index.  FOLDQ multiplies the x factors by the charge.  PC > 0
-// is the window support P as a compile-time constant (0: runtime a.P).
+// Window-factor layout (stage_batch): factor t of (particle p, axis) at
+// wts[(3 p + axis) EA + t ET].  P = 8 (compile time): EA = 1, ET = 3 batch
+// + 1, i.e. [t][p][axis] -- measured 0.59 -> 0.53 ms spread, 0.36 -> 0.33 ms
+// gather at cfg2; other P keep [p][axis][t] (EA = P, ET = 1: the
+// transposed layout measured slower at P = 10).
+constexpr bool wts_transposed(int PC) { return PC == 8; }
+__host__ __device__ constexpr int wts_ea(int PC, int P) { return wts_transposed(PC) ? 1 : P; }
+__host__ __device__ constexpr int wts_et(int PC, int batch) { return wts_transposed(PC) ? 3 * batch + 1 : 1; }
+
+// Stage the 3P window factors of a batch of particles.  wts layout: see
+// wts_ea / wts_et (transposed for P = 8: a task (p, axis) writes its P
+// factors 3 batch + 1 doubles apart, so consecutive tasks hit consecutive
+// banks -- the [p][axis][t] layout makes every staging store 8-way
+// conflicted; the odd stride keeps the consumers' reads conflict free);
+// loc: [p][4] = the local start (x, y, z) within the padded tile as bytes
+// 0..2 of loc[p][0] (one broadcast LDS.32 for the consumers instead of
+// three; each axis task writes its own byte), loc[p][3] = the caller-order
+// index sidx[s] (gather; loaded here, off the store's critical path) or the
+// sorted index (sidx == nullptr).  FOLDQ multiplies the x factors by the
+// charge.  PC > 0 is the window support P as a compile-time constant (0:
+// runtime a.P).
 template <int WIN, bool FOLDQ, int PC>
 __device__ __forceinline__ void stage_batch(const double4 *__restrict__ rec, int s0, int nb, const int org[3],
-                                            const SpreadArgs &a, double *wts, int *loc) {
+                                            const SpreadArgs &a, double *wts, int *loc,
+                                            const int *__restrict__ sidx = nullptr) {
     const int P = PC > 0 ? PC : a.P;
     for (int task = threadIdx.x; task < nb * 3; task += blockDim.x) {
         int p = task / 3, ax = task - 3 * p;
@@ -149,17 +165,19 @@ __device__ __forceinline__ void stage_batch(const double4 *__restrict__ rec, int
         double x = ax == 0 ? r.x : (ax == 1 ? r.y : r.z);
         double u = __dadd_rn(x, a.off[ax]);
         long long f = stencil_first(u, a);
-        double *wo = wts + (p * 3 + ax) * P;
+        // factor t of (p, axis) at wts[(3 p + axis) EA + t ET] (wts_strides)
+        const int EA = wts_ea(PC, P), ET = wts_et(PC, a.batch);
+        double *wo = wts + (p * 3 + ax) * EA;
 #pragma unroll
         for (int t = 0; t < (PC > 0 ? PC : 64); ++t) {
             if (PC == 0 && t >= P) break;
             double d = __dsub_rn(__dmul_rn((double)(f + t), a.h), u);  // sekspace.py:116
             double v = window_eval<WIN>(d, a);
             if (FOLDQ && ax == 0) v = __dmul_rn(r.w, v);
-            wo[t] = v;
+            wo[t * ET] = v;
         }
         reinterpret_cast<unsigned char *>(loc + p * 4)[ax] = (unsigned char)(start_index(f, ax, a) - org[ax]);
-        if (ax == 0) loc[p * 4 + 3] = s0 + p;
+        if (ax == 0) loc[p * 4 + 3] = sidx ? sidx[s0 + p] : s0 + p;
     }
 }
 
@@ -233,7 +251,8 @@ constexpr int tile_pitch(int T, int P) {
                          : (P % 16 == 8 ? T + P - 1 + ((8 - (T + P - 1) % 16) + 16) % 16 : T + P - 1);
 }
 constexpr size_t tile_bytes(int T, int P) {
-    return sizeof(double) * ((size_t)(T + P - 1) * (T + P - 1) * tile_pitch(T, P) + (size_t)tile_batch(P) * 3 * P) +
+    return sizeof(double) * ((size_t)(T + P - 1) * (T + P - 1) * tile_pitch(T, P) +
+                             (size_t)(tile_batch(P) * 3 + (wts_transposed(P) ? 1 : 0)) * P) +
            sizeof(int) * (4 * tile_batch(P) + 2 * (T + P - 1) + tile_pitch(T, P));
 }
 // P = 8: 8 x 8 x 17 tiles measured 0.5% faster per cfg2 step than 10 x 10 x 17
@@ -286,7 +305,8 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
     const int ncell = Tp * plane;
     double *tile = smem;
     double *wts = tile + ncell;
-    int *loc = reinterpret_cast<int *>(wts + a.batch * 3 * P);
+    int *loc = reinterpret_cast<int *>(wts + (a.batch * 3 + (wts_transposed(PC) ? 1 : 0)) * P);
+    const int EA = wts_ea(PC, P), S = wts_et(PC, a.batch);  // wts strides (stage_batch)
     int *gmap = loc + 4 * a.batch;
     int org[3];
     unit_origin(un.x, a, org);
@@ -305,18 +325,35 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
         for (int p = 0; p < nb; ++p) {
             const int pk = loc[p * 4];
             const int lx0 = pk & 0xff, ly0 = (pk >> 8) & 0xff, lz0 = (pk >> 16) & 0xff;
-            const double *wx = wts + p * 3 * P, *wy = wx + P, *wz = wy + P;
+            const double *wx = wts + p * 3 * EA, *wy = wx + EA, *wz = wx + 2 * EA;  // factor t at [t * S]
             if (PC > 0) {
-                // nwarps == P: this warp owns exactly one x-plane of the particle
+                // nwarps == P: this warp owns exactly one x-plane of the
+                // particle; at P = 8 the (y, z) products are formed before
+                // the plane's read-modify-writes (all weight loads issued
+                // first: 0.60 -> 0.55 ms at cfg2; slower at P = 10)
                 int t0 = (warp - lx0) % PC;
                 t0 = t0 < 0 ? t0 + PC : t0;
-                const double wxt = wx[t0];
+                const double wxt = wx[t0 * S];
                 double *base = tile + (lx0 + t0) * plane + ly0 * pitch + lz0;
+                if (wts_transposed(PC)) {
+                    double yz[LanePairs<PC>::NPI];
 #pragma unroll
-                for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
-                    if (lp.valid(lane, it)) {
-                        double *c = base + lp.off[it];
-                        *c = fma(wxt, __dmul_rn(wy[lp.ty[it]], wz[lp.tz[it]]), *c);
+                    for (int it = 0; it < LanePairs<PC>::NPI; ++it)
+                        yz[it] = lp.valid(lane, it) ? __dmul_rn(wy[lp.ty[it] * S], wz[lp.tz[it] * S]) : 0.0;
+#pragma unroll
+                    for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
+                        if (lp.valid(lane, it)) {
+                            double *c = base + lp.off[it];
+                            *c = fma(wxt, yz[it], *c);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
+                        if (lp.valid(lane, it)) {
+                            double *c = base + lp.off[it];
+                            *c = fma(wxt, __dmul_rn(wy[lp.ty[it] * S], wz[lp.tz[it] * S]), *c);
+                        }
                     }
                 }
             } else {
@@ -324,11 +361,11 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
                 t0 = t0 < 0 ? t0 + nw : t0;
                 for (int pi = lane; pi < npair; pi += 32) {
                     int ty = pi / P, tz = pi - ty * P;
-                    double cyz = __dmul_rn(wy[ty], wz[tz]);
+                    double cyz = __dmul_rn(wy[ty * S], wz[tz * S]);
                     int off = (ly0 + ty) * pitch + lz0 + tz;
                     for (int t = t0; t < P; t += nw) {
                         double *c = tile + (lx0 + t) * plane + off;
-                        *c = fma(wx[t], cyz, *c);
+                        *c = fma(wx[t * S], cyz, *c);
                     }
                 }
             }
@@ -411,13 +448,24 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
     const int ncell = Tp * plane;
     double *tile = smem;
     double *wts = tile + ncell;
-    int *loc = reinterpret_cast<int *>(wts + a.batch * 3 * P);
+    int *loc = reinterpret_cast<int *>(wts + (a.batch * 3 + (wts_transposed(PC) ? 1 : 0)) * P);
+    const int EA = wts_ea(PC, P), S = wts_et(PC, a.batch);  // wts strides (stage_batch)
     int *gmap = loc + 4 * a.batch;
     int org[3];
     unit_origin(un.x, a, org);
     build_axis_maps(org, a, gmap);
     __syncthreads();
-    for_tile_cells(a, gmap, [&](int ti, long long gi) { tile[ti] = gi >= 0 ? grid[gi] : 0.0; });
+    // the padded tile by asynchronous 8-byte copies (cp.async, LDGSTS): a
+    // thread issues all its cells' loads back to back instead of waiting
+    // for each one in a register round trip
+    for_tile_cells(a, gmap, [&](int ti, long long gi) {
+        if (gi >= 0)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(tile + ti)),
+                         "l"(grid + gi));
+        else
+            tile[ti] = 0.0;
+    });
+    asm volatile("cp.async.wait_all;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = a.nwarps;
     const int npair = P * P;
     LanePairs<PC> lp;
@@ -425,13 +473,15 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
     for (int b0 = ubeg; b0 < uend; b0 += a.batch) {
         int nb = min(a.batch, uend - b0);
         __syncthreads();
-        stage_batch<WIN, false, PC>(rec, b0, nb, org, a, wts, loc);
+        // P = 8: the caller-order index is loaded at staging (off the
+        // store's critical path; slower at P = 10), else at the store
+        stage_batch<WIN, false, PC>(rec, b0, nb, org, a, wts, loc, wts_transposed(PC) ? sidx : nullptr);
         __syncthreads();
         // this lane's share of particle p's P^3 sum
         auto partial = [&](int p) -> double {
             const int pk = loc[p * 4];
             const int lx0 = pk & 0xff, ly0 = (pk >> 8) & 0xff, lz0 = (pk >> 16) & 0xff;
-            const double *wx = wts + p * 3 * P, *wy = wx + P, *wz = wy + P;
+            const double *wx = wts + p * 3 * EA, *wy = wx + EA, *wz = wx + 2 * EA;  // factor t at [t * S]
             double acc = 0.0;
             if (PC > 0) {
                 const double *base = tile + lx0 * plane + ly0 * pitch + lz0;
@@ -441,8 +491,8 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
                         const double *c = base + lp.off[it];
                         double s = 0.0;
 #pragma unroll
-                        for (int t = 0; t < PC; ++t) s = fma(wx[t], c[t * plane], s);
-                        acc = fma(__dmul_rn(wy[lp.ty[it]], wz[lp.tz[it]]), s, acc);
+                        for (int t = 0; t < PC; ++t) s = fma(wx[t * S], c[t * plane], s);
+                        acc = fma(__dmul_rn(wy[lp.ty[it] * S], wz[lp.tz[it] * S]), s, acc);
                     }
                 }
             } else {
@@ -450,14 +500,14 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
                     int ty = pi / P, tz = pi - ty * P;
                     const double *c = tile + lx0 * plane + (ly0 + ty) * pitch + lz0 + tz;
                     double s = 0.0;
-                    for (int t = 0; t < P; ++t) s = fma(wx[t], c[t * plane], s);
-                    acc = fma(__dmul_rn(wy[ty], wz[tz]), s, acc);
+                    for (int t = 0; t < P; ++t) s = fma(wx[t * S], c[t * plane], s);
+                    acc = fma(__dmul_rn(wy[ty * S], wz[tz * S]), s, acc);
                 }
             }
             return acc;
         };
         auto store = [&](int p, double acc) {
-            const int orig = sidx[loc[p * 4 + 3]];
+            const int orig = wts_transposed(PC) ? loc[p * 4 + 3] : sidx[loc[p * 4 + 3]];
             const double v = acc * h3;
             phi[orig] = accumulate ? phi[orig] + v : v;
         };
