@@ -28,4 +28,4 @@ for st in realspace spread gather; do
   timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off \
     -k regex:$K -c 1 -o $O/${st} -f python tools/gpu/profile_step.py cfg2 $st > $O/ncu_$st.log 2>&1; echo "ncu $st rc=$?"
 done
-tail -2 $O/pytest.log $O/ref_suite.log
+tail -n 2 $O/pytest.log $O/ref_suite.log
