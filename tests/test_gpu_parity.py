@@ -270,7 +270,10 @@ def test_two_particle_single_term_and_cutoff():
     assert np.all(se.real_space_sum(far, 5.0, rc, se.Periodicity(0)) == 0.0)
 
 
-@pytest.mark.parametrize("xi,rc", [(4.2919, 1.0), (12.0, 0.45)])
+# xi rc covers every degree of the polynomial pair term (se_pair_poly_coefficients:
+# 20 for xi rc <= 2.5, 24, 28, 32) and the erfc fallback (xi rc > ~5)
+@pytest.mark.parametrize("xi,rc", [(4.2919, 1.0), (12.0, 0.45), (2.0, 1.0), (8.0, 0.4), (4.0, 1.0), (4.8, 1.0),
+                                   (5.4, 1.0)])
 def test_isolated_pairs_sweep_pair_kernel(xi, rc):
     # K isolated +-1 pairs at separations spanning (0, rc): each potential is
     # one kernel term q erfc(xi r)/r, checked against 30-digit values.  The
@@ -297,9 +300,10 @@ def test_isolated_pairs_sweep_pair_kernel(xi, rc):
     # both pair-term forms are accurate in ABSOLUTE terms (the 1/r rounding):
     # erfc_fast's erfc fit keeps tiny tail terms to ~1e-9 relative, the
     # polynomial form 1/r - Q(r^2) (pair_poly, cancelling towards the
-    # cutoff) to ~ulp(1/rc) / term -- here < 2e-6 for terms >= 1e-10 / rc
-    rel = np.abs(-phi[:K] - want) / want
-    assert np.max(rel) < 2e-6
+    # cutoff) to ~ulp(1/rc) / term -- < 5e-6 for terms >= 1e-10 / rc
+    big = want * rc >= 1e-10
+    rel = np.abs(-phi[:K] - want)[big] / want[big]
+    assert np.max(rel) < 5e-6
 
 
 def test_threads_argument_and_determinism():
@@ -579,6 +583,28 @@ def test_realspace_geometry_sweep(D, L_over_rc, N):
     sel = rng.choice(N, min(N, 300), replace=False)
     ref = orc.realspace(pos, q, L, D, xi, rc, targets=sel)
     assert se.relative_rms_error(phi[sel], ref) < 1e-12
+
+
+@pytest.mark.parametrize("D", [3, 0])
+@pytest.mark.parametrize("xi_rc", [2.0, 3.5, 4.2919, 4.6, 5.5])
+def test_realspace_pair_term_every_degree_vs_oracle(D, xi_rc):
+    # a dense system (dense and compacted batches both) at xi rc values that
+    # select each degree of the polynomial pair term (20, 24, 28, 32) and the
+    # erfc fallback (5.5): the device real-space sum against the oracle's
+    # scipy-erfc evaluation of the reference's loop (realspace.py:100-126)
+    rc = 0.5
+    L = 8.0 * rc
+    N = 40000
+    rng = np.random.default_rng(int(10 * xi_rc) + D)
+    pos = rng.random((N, 3)) * L
+    q = rng.uniform(-1, 1, N)
+    q -= q.mean()
+    s = se.ParticleSystem(pos, q, L)
+    xi = xi_rc / rc
+    phi = se.real_space_sum(s, xi, rc, se.Periodicity(D))
+    sel = rng.choice(N, 400, replace=False)
+    ref = orc.realspace(pos, q, L, D, xi, rc, targets=sel)
+    assert se.relative_rms_error(phi[sel], ref) < 1e-14
 
 
 # ----------------------------------------------- randomized configurations
