@@ -157,9 +157,13 @@ __host__ __device__ constexpr int wts_et(int PC, int batch) { return wts_transpo
 template <int WIN, bool FOLDQ, int PC>
 __device__ __forceinline__ void stage_batch(const double4 *__restrict__ rec, int s0, int nb, const int org[3],
                                             const SpreadArgs &a, double *wts, int *loc,
-                                            const int *__restrict__ sidx = nullptr) {
+                                            const int *__restrict__ sidx = nullptr, int tid = -1, int nthr = 0) {
     const int P = PC > 0 ? PC : a.P;
-    for (int task = threadIdx.x; task < nb * 3; task += blockDim.x) {
+    if (tid < 0) {
+        tid = threadIdx.x;
+        nthr = blockDim.x;
+    }
+    for (int task = tid; task < nb * 3; task += nthr) {
         int p = task / 3, ax = task - 3 * p;
         double4 r = rec[s0 + p];
         double x = ax == 0 ? r.x : (ax == 1 ? r.y : r.z);
@@ -428,6 +432,97 @@ __global__ void spread_det_reduce_kernel(const double *__restrict__ dbuf, const 
                             }
         grid[gi] = v;
     }
+}
+
+// Warp-specialised spreading (P = 8): kSwsC plane-owner warps update the
+// tile with a staged batch while kSwsP producer warps stage the next batch
+// into the other of two factor / record buffers, handed over by named
+// barriers (FULL[b]: producers arrive, owners wait; EMPTY[b]: owners
+// arrive, producers wait) -- the CTA-wide barriers around each batch's
+// staging in spread_tile_kernel are gone.  SE_B200_SPREAD_WS=0: the
+// single-role kernel.
+constexpr int kSwsC = 8, kSwsP = 4;
+constexpr int kBarFull0 = 1, kBarEmpty0 = 3;  // ids 1, 2 and 3, 4 (0: __syncthreads)
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+constexpr size_t spread_ws_extra(int P) {  // the second factor + record buffer
+    return sizeof(double) * (size_t)(tile_batch(P) * 3 + 1) * P + sizeof(int) * 4 * tile_batch(P);
+}
+
+template <int WIN>
+__global__ void __launch_bounds__(32 * (kSwsC + kSwsP), 3) spread_ws_kernel(const double4 *__restrict__ rec,
+                                                                             const int4 *__restrict__ units,
+                                                                             const int *__restrict__ nunits,
+                                                                             SpreadArgs a, double *__restrict__ grid) {
+    constexpr int PC = 8, B = tile_batch(PC), NT = 32 * (kSwsC + kSwsP);
+    static_assert(wts_transposed(PC), "the warp-specialised spread uses the transposed factor layout");
+    if ((int)blockIdx.x >= *nunits) return;
+    const int4 un = units[blockIdx.x];
+    const int ubeg = (int)max((int64_t)un.y, a.rlo), uend = (int)min((int64_t)un.y + un.z, a.rhi);
+    if (ubeg >= uend) return;
+    extern __shared__ double smem[];
+    constexpr int Tp = TileC<PC>::Tp, pitch = TileC<PC>::pitch, plane = Tp * pitch, ncell = Tp * plane;
+    constexpr int WSZ = (B * 3 + 1) * PC, S = wts_et(PC, B);
+    double *tile = smem;
+    double *const wts0 = tile + ncell;                                 // buffer b: wts0 + b WSZ
+    int *const loc0 = reinterpret_cast<int *>(tile + ncell + 2 * WSZ);  // buffer b: loc0 + 4 b B
+    int *gmap = loc0 + 8 * B;
+    int org[3];
+    unit_origin(un.x, a, org);
+    for (int i = threadIdx.x; i < ncell; i += blockDim.x) tile[i] = 0.0;
+    build_axis_maps(org, a, gmap);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nbatch = (uend - ubeg + B - 1) / B;
+    if (warp >= kSwsC) {
+        // producers
+        const int tid = threadIdx.x - 32 * kSwsC;
+        for (int k = 0; k < nbatch; ++k) {
+            const int b = k & 1, b0 = ubeg + k * B, nb = min(B, uend - b0);
+            if (k >= 2) named_sync(kBarEmpty0 + b, NT);
+            stage_batch<WIN, true, PC>(rec, b0, nb, org, a, wts0 + b * WSZ, loc0 + 4 * b * B, nullptr, tid,
+                                       32 * kSwsP);
+            __threadfence_block();
+            named_arrive(kBarFull0 + b, NT);
+        }
+    } else {
+        // plane owners: warp w owns the padded tile's x planes lx == w (mod 8)
+        LanePairs<PC> lp;
+        lp.init(lane, pitch);
+        for (int k = 0; k < nbatch; ++k) {
+            const int b = k & 1, b0 = ubeg + k * B, nb = min(B, uend - b0);
+            named_sync(kBarFull0 + b, NT);
+            const double *wts = wts0 + b * WSZ;
+            const int *loc = loc0 + 4 * b * B;
+            for (int p = 0; p < nb; ++p) {
+                const int pk = loc[p * 4];
+                const int lx0 = pk & 0xff, ly0 = (pk >> 8) & 0xff, lz0 = (pk >> 16) & 0xff;
+                const double *wx = wts + p * 3, *wy = wx + 1, *wz = wx + 2;  // factor t at [t * S]
+                int t0 = (warp - lx0) % PC;
+                t0 = t0 < 0 ? t0 + PC : t0;
+                const double wxt = wx[t0 * S];
+                double *base = tile + (lx0 + t0) * plane + ly0 * pitch + lz0;
+                double yz[LanePairs<PC>::NPI];
+#pragma unroll
+                for (int it = 0; it < LanePairs<PC>::NPI; ++it)
+                    yz[it] = __dmul_rn(wy[lp.ty[it] * S], wz[lp.tz[it] * S]);
+#pragma unroll
+                for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
+                    double *c = base + lp.off[it];
+                    *c = fma(wxt, yz[it], *c);
+                }
+                __syncwarp();
+            }
+            if (k + 2 < nbatch) named_arrive(kBarEmpty0 + b, NT);
+        }
+    }
+    __syncthreads();
+    for_tile_cells(a, gmap, [&](int ti, long long gi) {
+        const double v = tile[ti];
+        if (gi >= 0 && v != 0.0) atomicAdd(grid + gi, v);
+    });
 }
 
 template <int WIN, int PC>
@@ -735,6 +830,15 @@ static void shard_range(int64_t N, int rank, int world, int64_t &lo, int64_t &hi
     hi = N * (rank + 1) / world;
 }
 
+// SE_B200_SPREAD_WS=0 selects the single-role spreading kernel (A/B runs)
+static bool spread_ws_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("SE_B200_SPREAD_WS");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 void spread_run(se_plan *pl, const double *pos, const double *q, int64_t N, double *grid, int rank, int world) {
     if (pl->p.P > pl->g.M) fail(SE_EINVAL, "window support P must not exceed M");
     const se_grid_t &g = pl->g;
@@ -757,6 +861,15 @@ void spread_run(se_plan *pl, const double *pos, const double *q, int64_t N, doub
             pl->sdet.ensure(sizeof(double) * (size_t)maxu * t.Tp * t.Tp * t.pitch);
             dbuf = pl->sdet.as<double>();
         }
+        if (PC == 8 && !det && spread_ws_enabled() && t.T == TileC<8>::T) {
+            const size_t smem = t.smem + spread_ws_extra(8);
+            dispatch_window(pl->p.window, [&](auto W) {
+                auto kern = spread_ws_kernel<decltype(W)::value>;
+                SE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                kern<<<(unsigned)maxu, 32 * (kSwsC + kSwsP), smem, pl->stream>>>(rec, pl->tbin.units.as<int4>(),
+                                                                                  pl->tbin.nunits.as<int>(), a, grid);
+            });
+        } else
         dispatch_window(pl->p.window, [&](auto W) {
             dispatch_p(PC, [&](auto PCv) {
                 auto kern = spread_tile_kernel<decltype(W)::value, decltype(PCv)::value>;
