@@ -24,7 +24,7 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/peaks tools/peaks.cu &&
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
   --log-file $O/launches.csv python tools/gpu/profile_step.py cfg2 > $O/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 for st in realspace spread gather; do
-  case $st in realspace) K=realspace_cell;; spread) K=spread_tile;; gather) K=gather_tile;; esac
+  case $st in realspace) K=realspace_cell;; spread) K="spread_(tile|ws)";; gather) K=gather_tile;; esac
   timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off \
     -k regex:$K -c 1 -o $O/${st} -f python tools/gpu/profile_step.py cfg2 $st > $O/ncu_$st.log 2>&1; echo "ncu $st rc=$?"
 done
