@@ -199,6 +199,14 @@ struct se_plan {
     // real-space sum without Newton's third law, spreading through per-unit
     // tiles reduced in a fixed order; from SE_B200_DETERMINISTIC at creation
     bool deterministic = false;
+    // the real-space kernel's polynomial pair term (pair_poly_fit, ~1 ms of
+    // host work): fitted once per (xi, rc, kind) and kept with the plan
+    struct PairPoly {
+        bool valid = false;
+        double xi = 0.0, rc = 0.0;
+        int deg = 0;
+        double pc[33] = {};
+    } pair_poly[2];  // kind 0: potential, 1: field
     cudaGraphExec_t gexec = nullptr;
     const void *gkey[3] = {};  // pos, q, phi
     int64_t gN = -1;

@@ -1082,14 +1082,26 @@ __global__ void realspace_image_kernel(const double *__restrict__ pos, const dou
 // The polynomial pair term (pair_poly) for this xi, rc: coefficients and
 // degree by pair_poly_fit (se_host.cpp, long double); 0 (erfc_fast) when no
 // degree <= 32 reaches the accuracy (xi rc > ~5) or SE_B200_PAIR_POLY=0.
-static int fit_pair_poly(RealArgs &a, int kind) {
+static int fit_pair_poly(se_plan *pl, RealArgs &a, int kind) {
     a.rc2x = a.rc * a.rc;
     a.pscale = 2.0 / a.rc2x;
     static const bool off = [] {
         const char *e = std::getenv("SE_B200_PAIR_POLY");
         return e && std::atoi(e) == 0;
     }();
-    a.pdeg = off ? 0 : pair_poly_fit(a.xi, a.rc, kind, a.pc);
+    if (off) {
+        a.pdeg = 0;
+        return 0;
+    }
+    se_plan::PairPoly &c = pl->pair_poly[kind];  // fitted once per plan (the fit is ~1 ms of host work)
+    if (!c.valid || c.xi != a.xi || c.rc != a.rc) {
+        c.deg = pair_poly_fit(a.xi, a.rc, kind, c.pc);
+        c.xi = a.xi;
+        c.rc = a.rc;
+        c.valid = true;
+    }
+    for (int i = 0; i < 33; ++i) a.pc[i] = c.pc[i];
+    a.pdeg = c.deg;
     return a.pdeg;
 }
 
@@ -1305,7 +1317,7 @@ static void realspace_impl(se_plan *pl, const double *pos, const double *q, int6
     a.rlo = N * rank / world;
     a.rhi = N * (rank + 1) / world;
     set_prefilter(a);
-    fit_pair_poly(a, FLD ? 1 : 0);
+    fit_pair_poly(pl, a, FLD ? 1 : 0);
     if (D >= 1 && rc > L / 2 + 1e-12) {
         int layers = (int)std::floor((rc + L / 2) / L) + 1;
         prof_begin(pl, SE_K_REALSPACE);
