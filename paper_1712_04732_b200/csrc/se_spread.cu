@@ -139,6 +139,7 @@ __global__ void tile_keys_hist_kernel(const double *__restrict__ pos, int64_t N,
 // gather at cfg2; other P keep [p][axis][t] (EA = P, ET = 1: the
 // transposed layout measured slower at P = 10).
 constexpr bool wts_transposed(int PC) { return PC == 8; }
+__host__ __device__ constexpr int tile_batch(int P) { return P >= 12 ? 32 : 64; }
 __host__ __device__ constexpr int wts_ea(int PC, int P) { return wts_transposed(PC) ? 1 : P; }
 __host__ __device__ constexpr int wts_et(int PC, int batch) { return wts_transposed(PC) ? 3 * batch + 1 : 1; }
 
@@ -170,7 +171,7 @@ __device__ __forceinline__ void stage_batch(const double4 *__restrict__ rec, int
         double u = __dadd_rn(x, a.off[ax]);
         long long f = stencil_first(u, a);
         // factor t of (p, axis) at wts[(3 p + axis) EA + t ET] (wts_strides)
-        const int EA = wts_ea(PC, P), ET = wts_et(PC, a.batch);
+        const int EA = wts_ea(PC, P), ET = wts_et(PC, PC > 0 ? tile_batch(PC) : a.batch);
         double *wo = wts + (p * 3 + ax) * EA;
 #pragma unroll
         for (int t = 0; t < (PC > 0 ? PC : 64); ++t) {
@@ -196,6 +197,11 @@ __device__ __forceinline__ void unit_origin(int bin, const SpreadArgs &a, int or
 
 // Per-axis grid index of every padded-tile coordinate (-1 off the grid),
 // wrapped on periodic axes: gmap[ax * Tp + l] (x, y: Tp entries; z: pitch).
+#ifndef TILE_FLAT
+#define TILE_FLAT 1
+#endif
+template <int PC>
+struct TileC;
 __device__ __forceinline__ void build_axis_maps(const int org[3], const SpreadArgs &a, int *gmap) {
     for (int i = threadIdx.x; i < 2 * a.Tp + a.pitch; i += blockDim.x) {
         const int ax = min(i / a.Tp, 2), l = i - ax * a.Tp;
@@ -210,8 +216,22 @@ __device__ __forceinline__ void build_axis_maps(const int org[3], const SpreadAr
 
 // Visit every padded-tile cell with its grid index: one warp per (lx, ly)
 // row, lanes along z (coalesced in the grid's z-fastest layout).
-template <class F>
+template <int PC = 0, class F>
 __device__ __forceinline__ void for_tile_cells(const SpreadArgs &a, const int *gmap, F f) {
+    if constexpr (PC > 0 && TILE_FLAT && TileC<PC>::T > 0) {
+        // compile-time tile geometry: the cells as one flat range over all
+        // threads (every lane busy; the row / column split is a multiply by a
+        // constant instead of a runtime division)
+        constexpr int Tp = TileC<PC>::Tp, pitch = TileC<PC>::pitch, ncell = Tp * Tp * pitch;
+        const long long s1 = a.shape[1], s2 = a.shape[2];
+        for (int i = threadIdx.x; i < ncell; i += blockDim.x) {
+            const int row = i / pitch, lz = i - row * pitch;
+            const int lx = row / Tp, ly = row - lx * Tp;
+            const int gx = gmap[lx], gy = gmap[Tp + ly], gz = gmap[2 * Tp + lz];
+            f(i, (gx | gy | gz) >= 0 ? ((long long)gx * s1 + gy) * s2 + gz : -1LL);
+        }
+        return;
+    }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
     const int Tp = a.Tp;
     for (int row = warp; row < Tp * Tp; row += nwarp) {
@@ -247,7 +267,6 @@ __device__ __forceinline__ void for_tile_cells(const SpreadArgs &a, const int *g
 // at P = 8, 3 CTAs per SM beat both 2 (larger tiles) and 4 (smaller tiles).
 constexpr size_t kSmemSM = 228 * 1024, kSmemReserved = 1024;
 constexpr size_t kSmemFirst = kSmemSM / 3 - kSmemReserved;
-constexpr int tile_batch(int P) { return P >= 12 ? 32 : 64; }
 constexpr bool tile_aniso(int P) { return P % 16 != 0 && P <= 12; }
 constexpr int tile_Tz(int T, int P) { return tile_aniso(P) ? 17 : T; }
 constexpr int tile_pitch(int T, int P) {
@@ -309,9 +328,10 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
     const int ncell = Tp * plane;
     double *tile = smem;
     double *wts = tile + ncell;
-    int *loc = reinterpret_cast<int *>(wts + (a.batch * 3 + (wts_transposed(PC) ? 1 : 0)) * P);
-    const int EA = wts_ea(PC, P), S = wts_et(PC, a.batch);  // wts strides (stage_batch)
-    int *gmap = loc + 4 * a.batch;
+    const int BATCH = PC > 0 ? tile_batch(PC) : a.batch;  // a.batch == tile_batch(P) (tile_setup)
+    int *loc = reinterpret_cast<int *>(wts + (BATCH * 3 + (wts_transposed(PC) ? 1 : 0)) * P);
+    const int EA = wts_ea(PC, P), S = wts_et(PC, BATCH);  // wts strides (stage_batch)
+    int *gmap = loc + 4 * BATCH;
     int org[3];
     unit_origin(un.x, a, org);
     for (int i = threadIdx.x; i < ncell; i += blockDim.x) tile[i] = 0.0;
@@ -321,8 +341,8 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
     const int npair = P * P;
     LanePairs<PC> lp;
     lp.init(lane, pitch);
-    for (int b0 = ubeg; b0 < uend; b0 += a.batch) {
-        int nb = min(a.batch, uend - b0);
+    for (int b0 = ubeg; b0 < uend; b0 += BATCH) {
+        int nb = min(BATCH, uend - b0);
         __syncthreads();  // tile zeroed / previous batch consumed
         stage_batch<WIN, true, PC>(rec, b0, nb, org, a, wts, loc);
         __syncthreads();
@@ -384,7 +404,7 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
         for (int i = threadIdx.x; i < ncell; i += blockDim.x) o[i] = tile[i];
         return;
     }
-    for_tile_cells(a, gmap, [&](int ti, long long gi) {
+    for_tile_cells<PC>(a, gmap, [&](int ti, long long gi) {
         const double v = tile[ti];
         if (gi >= 0 && v != 0.0) atomicAdd(grid + gi, v);
     });
@@ -519,7 +539,7 @@ __global__ void __launch_bounds__(32 * (kSwsC + kSwsP), 3) spread_ws_kernel(cons
         }
     }
     __syncthreads();
-    for_tile_cells(a, gmap, [&](int ti, long long gi) {
+    for_tile_cells<PC>(a, gmap, [&](int ti, long long gi) {
         const double v = tile[ti];
         if (gi >= 0 && v != 0.0) atomicAdd(grid + gi, v);
     });
@@ -543,9 +563,10 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
     const int ncell = Tp * plane;
     double *tile = smem;
     double *wts = tile + ncell;
-    int *loc = reinterpret_cast<int *>(wts + (a.batch * 3 + (wts_transposed(PC) ? 1 : 0)) * P);
-    const int EA = wts_ea(PC, P), S = wts_et(PC, a.batch);  // wts strides (stage_batch)
-    int *gmap = loc + 4 * a.batch;
+    const int BATCH = PC > 0 ? tile_batch(PC) : a.batch;  // a.batch == tile_batch(P) (tile_setup)
+    int *loc = reinterpret_cast<int *>(wts + (BATCH * 3 + (wts_transposed(PC) ? 1 : 0)) * P);
+    const int EA = wts_ea(PC, P), S = wts_et(PC, BATCH);  // wts strides (stage_batch)
+    int *gmap = loc + 4 * BATCH;
     int org[3];
     unit_origin(un.x, a, org);
     build_axis_maps(org, a, gmap);
@@ -553,7 +574,7 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
     // the padded tile by asynchronous 8-byte copies (cp.async, LDGSTS): a
     // thread issues all its cells' loads back to back instead of waiting
     // for each one in a register round trip
-    for_tile_cells(a, gmap, [&](int ti, long long gi) {
+    for_tile_cells<PC>(a, gmap, [&](int ti, long long gi) {
         if (gi >= 0)
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(tile + ti)),
                          "l"(grid + gi));
@@ -565,8 +586,8 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
     const int npair = P * P;
     LanePairs<PC> lp;
     lp.init(lane, pitch);
-    for (int b0 = ubeg; b0 < uend; b0 += a.batch) {
-        int nb = min(a.batch, uend - b0);
+    for (int b0 = ubeg; b0 < uend; b0 += BATCH) {
+        int nb = min(BATCH, uend - b0);
         __syncthreads();
         // P = 8: the caller-order index is loaded at staging (off the
         // store's critical path; slower at P = 10), else at the store
