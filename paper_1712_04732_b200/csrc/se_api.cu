@@ -80,19 +80,18 @@ __global__ void check_kernel(const double *__restrict__ pos, const double *__res
 
 // core.py:65-77 (box) and core.py:180-191 (neutrality): ValueError for D > 0,
 // a warning flag for D = 0.
-void check_system(se_plan *pl, const double *pos, const double *q, int64_t N, bool neutrality) {
-    pl->warnings = 0;
-    if (N <= 0) return;
-    pl->check.ensure(sizeof(double) * 4);
+// the check kernel alone (no host synchronisation; capturable)
+void check_launch(se_plan *pl, const double *pos, const double *q, int64_t N) {
     SE_CUDA(cudaMemsetAsync(pl->check.ptr, 0, sizeof(double) * 4, pl->stream));
     int64_t blocks = (N + 255) / 256;
     if (blocks > 1184) blocks = 1184;
     check_kernel<<<(unsigned)blocks, 256, 0, pl->stream>>>(pos, q, N, pl->L, pl->check.as<double>());
     SE_LAUNCH_CHECK();
     pl->launches += 1;
-    double h[4];
-    SE_CUDA(cudaMemcpyAsync(h, pl->check.ptr, sizeof(double) * 4, cudaMemcpyDeviceToHost, pl->stream));
-    SE_CUDA(cudaStreamSynchronize(pl->stream));
+}
+
+// the verdict on the check kernel's sums h = [sum q, sum |q|, #outside]
+void check_verdict(se_plan *pl, const double *h, bool neutrality) {
     if (h[2] > 0) fail(SE_EINVAL, "all coordinates must lie in [0, L)");
     if (!neutrality) return;
     double qabs = h[1] > 1.0 ? h[1] : 1.0;
@@ -103,12 +102,55 @@ void check_system(se_plan *pl, const double *pos, const double *q, int64_t N, bo
         fail(SE_EINVAL, "periodic Ewald summation requires a charge-neutral system");
 }
 
+void check_system(se_plan *pl, const double *pos, const double *q, int64_t N, bool neutrality) {
+    pl->warnings = 0;
+    if (N <= 0) return;
+    pl->check.ensure(sizeof(double) * 4);
+    check_launch(pl, pos, q, N);
+    double h[4];
+    SE_CUDA(cudaMemcpyAsync(h, pl->check.ptr, sizeof(double) * 4, cudaMemcpyDeviceToHost, pl->stream));
+    SE_CUDA(cudaStreamSynchronize(pl->stream));
+    check_verdict(pl, h, neutrality);
+}
+
+void flag_verdict(int h) {
+    if (h == 1) fail(SE_ESINGULAR, "coincident distinct particles");
+    if (h == 2) fail(SE_ESINGULAR, "particle coincides with an image");
+}
+
 void check_flag(se_plan *pl) {
     int h = 0;
     SE_CUDA(cudaMemcpyAsync(&h, pl->flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, pl->stream));
     SE_CUDA(cudaStreamSynchronize(pl->stream));
-    if (h == 1) fail(SE_ESINGULAR, "coincident distinct particles");
-    if (h == 2) fail(SE_ESINGULAR, "particle coincides with an image");
+    flag_verdict(h);
+}
+
+// The fused total potential checks its input WITHOUT a host round trip
+// before the device work: the check kernel is the first node of the body
+// (inside the CUDA graph), the binning kernels read coordinates through
+// sane_coord (se_common.h) so invalid input cannot index out of range, and
+// the sums come back together with the singularity flag (and, for the
+// _host entry, the potentials) under ONE synchronisation at the end.  The
+// caller sees the reference's errors in the reference's order (box,
+// neutrality, coincidence); only their timing moved (the timeline of
+// profiles/timeline_cfg2_r02.txt: 0.1 ms of idle GPU per call at cfg2).
+void total_verdict(se_plan *pl, int64_t N, const void *extra_dev, void *extra_host, size_t extra_bytes) {
+    if (!pl->verdict_host) SE_CUDA(cudaMallocHost((void **)&pl->verdict_host, sizeof(double) * 5));
+    double *h = pl->verdict_host;
+    int *f = reinterpret_cast<int *>(h + 4);
+    *f = 0;
+    const bool checked_run = N > 0 && pl->check.ptr && pl->flag.ptr;
+    if (checked_run) {
+        SE_CUDA(cudaMemcpyAsync(h, pl->check.ptr, sizeof(double) * 4, cudaMemcpyDeviceToHost, pl->stream));
+        SE_CUDA(cudaMemcpyAsync(f, pl->flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, pl->stream));
+    }
+    if (extra_bytes)
+        SE_CUDA(cudaMemcpyAsync(extra_host, extra_dev, extra_bytes, cudaMemcpyDeviceToHost, pl->stream));
+    SE_CUDA(cudaStreamSynchronize(pl->stream));
+    if (checked_run) {
+        check_verdict(pl, h, true);
+        flag_verdict(*f);
+    }
 }
 
 struct Events {
@@ -191,6 +233,7 @@ void total_body(se_plan *pl, const double *pos, const double *q, int64_t N, doub
     }
     pl->phik.ensure(sizeof(double) * (N ? N : 1));
     cudaStream_t main_st = pl->stream;
+    check_launch(pl, pos, q, N);  // read back by total_verdict
     SE_CUDA(cudaEventRecord(pl->fork_ev, main_st));
     SE_CUDA(cudaStreamWaitEvent(pl->side, pl->fork_ev, 0));
     pl->stream = pl->side;
@@ -300,25 +343,6 @@ void total_body_graphed(se_plan *pl, const double *pos, const double *q, int64_t
     }
 }
 
-void total_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, double *timings) {
-    check_system(pl, pos, q, N, true);
-    if (!timings && N > 0) {
-        if (pl->graphs)
-            total_body_graphed(pl, pos, q, N, phi);
-        else
-            total_body(pl, pos, q, N, phi, false);
-    } else {
-        Events ev(timings != nullptr, pl->stream);
-        ev.mark();
-        realspace_run(pl, pos, q, N, phi, 1, 0, 1);
-        ev.mark();
-        kspace_pipeline(pl, pos, q, N, phi, 1, timings, 1, 0, 1);
-        if (timings) timings[SE_T_REALSPACE] = ev.secs(0, 1);
-    }
-    check_flag(pl);
-    prof_collect(pl);
-}
-
 template <class T>
 T *stage_in(se_plan *pl, DevBuf &b, const T *host, size_t n) {
     b.ensure(sizeof(T) * (n ? n : 1));
@@ -329,6 +353,30 @@ T *stage_in(se_plan *pl, DevBuf &b, const T *host, size_t n) {
 void stage_out(se_plan *pl, void *host, const void *dev, size_t bytes) {
     if (bytes) SE_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, pl->stream));
     SE_CUDA(cudaStreamSynchronize(pl->stream));
+}
+
+void total_pipeline(se_plan *pl, const double *pos, const double *q, int64_t N, double *phi, double *timings,
+                    void *out_host = nullptr) {
+    if (!timings && N > 0) {
+        pl->warnings = 0;
+        pl->check.ensure(sizeof(double) * 4);
+        if (pl->graphs)
+            total_body_graphed(pl, pos, q, N, phi);
+        else
+            total_body(pl, pos, q, N, phi, false);
+        total_verdict(pl, N, phi, out_host, out_host ? sizeof(double) * N : 0);
+    } else {
+        check_system(pl, pos, q, N, true);
+        Events ev(timings != nullptr, pl->stream);
+        ev.mark();
+        realspace_run(pl, pos, q, N, phi, 1, 0, 1);
+        ev.mark();
+        kspace_pipeline(pl, pos, q, N, phi, 1, timings, 1, 0, 1);
+        if (timings) timings[SE_T_REALSPACE] = ev.secs(0, 1);
+        check_flag(pl);
+        if (out_host) stage_out(pl, out_host, phi, sizeof(double) * N);
+    }
+    prof_collect(pl);
 }
 
 // realspace.py:183-185: -2 xi q / sqrt(pi)
@@ -373,6 +421,8 @@ void plan_release_device(se_plan *pl) {
                       &pl->ghat, &pl->grid_dev, &pl->io_pos, &pl->io_q, &pl->io_phi, &pl->io_grid, &pl->check, &pl->pairs, &pl->racc, &pl->sdet,
                       &pl->zs_rowsI, &pl->zs_Hk, &pl->zs_Z, &pl->zs_B})
         d->release();
+    if (pl->verdict_host) cudaFreeHost(pl->verdict_host);
+    pl->verdict_host = nullptr;
     if (pl->own_stream) cudaStreamDestroy(pl->own_stream);
 }
 }  // namespace se
@@ -809,8 +859,7 @@ int se_total_potential_host(se_plan_t plan, const double *pos, const double *q, 
     const double *dp = stage_in(pl, pl->io_pos, pos, 3 * (size_t)N);
     const double *dq = stage_in(pl, pl->io_q, q, (size_t)N);
     pl->io_phi.ensure(sizeof(double) * (N ? N : 1));
-    total_pipeline(pl, dp, dq, N, pl->io_phi.as<double>(), timings);
-    stage_out(pl, phi, pl->io_phi.ptr, sizeof(double) * N);
+    total_pipeline(pl, dp, dq, N, pl->io_phi.as<double>(), timings, phi);
     SE_API_END
 }
 

@@ -228,6 +228,7 @@ struct se_plan {
     // deferred checks: the shard entry points return without synchronising
     // (device error flags, profiling events); se_plan_finish does both
     bool defer = false;
+    double *verdict_host = nullptr;  // pinned: check sums [0..3], singularity flag [4] (total_verdict)
     cufftHandle slab_f2 = 0, slab_i2 = 0, slab_x = 0;
     // row-distributed AFT (D = 1, 2), for one (world, rank)
     int zs_world = -1, zs_rank = -1, zs_nI = 0;
@@ -299,6 +300,20 @@ void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, i
 int64_t binning_max_units(const Binning &b, int64_t N, int nbins, int chunk);
 
 // shared device helpers ---------------------------------------------------
+// A coordinate as the binning kernels use it.  Valid input (x in [0, L)) is
+// returned unchanged.  The fused total-potential call reports a coordinate
+// outside the box (core.py:65-77) only AFTER its device work, without a host
+// round trip up front; until then such a coordinate (NaN included) is replaced
+// by a pseudo-random point of the box derived from its index, identically in
+// the key and the record kernels, so every later kernel indexes in range and
+// no bin piles up.  The results of such a call are discarded by the error.
+#ifdef __CUDACC__
+__device__ __forceinline__ double sane_coord(double x, double L, long long i, int ax) {
+    if (x >= 0.0 && x < L) return x;
+    const unsigned h = (unsigned)(3 * i + ax) * 2654435761u;
+    return L * ((double)(h >> 8) * (1.0 / 16777216.0));
+}
+#endif
 struct WinParams {
     int window;
     int P;

@@ -83,14 +83,14 @@ __device__ __forceinline__ unsigned column_key(const double *__restrict__ pos, i
     for (int ax = 0; ax < 2; ++ax) {
         // clamped on both sides: the C ABI rejects coordinates outside
         // [0, L), this only keeps an unchecked caller's keys in range
-        int ci = (int)floor(pos[3 * i + ax] / a.edge);
+        int ci = (int)floor(sane_coord(pos[3 * i + ax], a.L, i, ax) / a.edge);
         ci = ci < 0 ? 0 : ci;
         c[ax] = ci < a.n - 1 ? ci : a.n - 1;
     }
     colid = (unsigned)(c[0] * a.n + c[1]);
     // within a column, order by the quantized z: Q(z) = floor(z qinv) is then
     // non-decreasing along every column (z in [0, L))
-    int sub = zq(pos[3 * i + 2], a.qinv);
+    int sub = zq(sane_coord(pos[3 * i + 2], a.L, i, 2), a.qinv);
     sub = sub < 0 ? 0 : (sub >= (1 << a.kb) ? (1 << a.kb) - 1 : sub);
     return (colid << a.kb) | (unsigned)sub;
 }
@@ -398,8 +398,11 @@ __device__ __forceinline__ void hit_poly(unsigned en, bool valid, const RealArgs
     const double2 s01 = wb.sxy[h.k], s23 = wb.szq[h.k];
     const double dx = t01.x - s01.x, dy = t01.y - s01.y, dz = t23.x - s23.x;
     const double u = fma(dz, dz, fma(dy, dy, dx * dx));
-    singular |= u < 1e-28 ? 1 : 0;
-    h.ok = valid && u < a.rc2x;
+    // u >= 0: the order of its bit pattern is the order of its value, so both
+    // tests run on the integer pipe (a DSETP occupies the fp64 pipe)
+    const long long ub = __double_as_longlong(u);
+    singular |= ub < 0x3A1FB0F6BE506019LL ? 1 : 0;  // u < 1e-28
+    h.ok = valid && ub < __double_as_longlong(a.rc2x);
     const double f = pair_poly<DEG>(u, a);
     h.f = h.ok ? f : 0.0;
     h.qt = t23.y;

@@ -169,11 +169,13 @@ __global__ void __launch_bounds__(1024) bin_order_large_kernel(const int *__rest
 }
 
 __global__ void gather_records_kernel(const double *__restrict__ pos, const double *__restrict__ q,
-                                      const int *__restrict__ idx, double4 *__restrict__ rec, int64_t n) {
+                                      const int *__restrict__ idx, double4 *__restrict__ rec, int64_t n,
+                                      double L) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    int j = idx[i];
-    rec[i] = make_double4(pos[3 * (int64_t)j], pos[3 * (int64_t)j + 1], pos[3 * (int64_t)j + 2], q ? q[j] : 0.0);
+    const long long j = idx[i];
+    rec[i] = make_double4(sane_coord(pos[3 * j], L, j, 0), sane_coord(pos[3 * j + 1], L, j, 1),
+                          sane_coord(pos[3 * j + 2], L, j, 2), q ? q[j] : 0.0);
 }
 
 // One CTA: exclusive scans of bin counts and of per-bin unit counts, then the
@@ -308,7 +310,7 @@ void binning_sort(se_plan *pl, Binning &b, const double *pos, const double *q, i
                                              b.nlarge.as<int>(), cap);
         bin_order_large_kernel<<<148, 1024, 0, st>>>(b.fstart.as<int>(), nfine, N, b.idx_sorted.as<int>(),
                                                      b.large.as<int>(), b.nlarge.as<int>(), cap);
-        gather_records_kernel<<<nb, 256, 0, st>>>(pos, q, b.idx_sorted.as<int>(), b.rec.as<double4>(), N);
+        gather_records_kernel<<<nb, 256, 0, st>>>(pos, q, b.idx_sorted.as<int>(), b.rec.as<double4>(), N, pl->L);
         SE_LAUNCH_CHECK();
         pl->launches += 8;
     }

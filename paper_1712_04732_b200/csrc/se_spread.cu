@@ -40,6 +40,7 @@ struct SpreadArgs {
     double w, shapep, peak, mm, ww2, i0b;
     double invw, gcoef;  // 1/w and -m^2/(2 w^2)
     int64_t rlo, rhi;  // sorted-particle range of this shard
+    double L;          // box edge (sane_coord)
 };
 
 // ---------------------------------------------------------------- windows
@@ -99,7 +100,7 @@ __device__ __forceinline__ unsigned tile_key(const double *__restrict__ pos, int
     int tc[3];
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-        double u = __dadd_rn(pos[3 * i + ax], a.off[ax]);
+        double u = __dadd_rn(sane_coord(pos[3 * i + ax], a.L, i, ax), a.off[ax]);
         tc[ax] = tile_coord(start_index(stencil_first(u, a), ax, a), ax, a);
     }
     return (unsigned)((tc[0] * a.nt[1] + tc[1]) * a.nt[2] + tc[2]);
@@ -721,6 +722,7 @@ static SpreadArgs make_args(se_plan *pl) {
         a.off[i] = g.offsets[i];
     }
     a.h = g.h;
+    a.L = pl->L;
     a.halfP = 0.5 * p.P;
     a.window = p.window;
     a.w = 0.5 * p.P * g.h;

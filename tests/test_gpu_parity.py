@@ -258,6 +258,43 @@ def test_error_conventions():
         se.real_space_sum(s, -1.0, 0.4, se.Periodicity(3))
 
 
+@pytest.mark.parametrize("D", [3, 0])
+def test_invalid_coordinates_are_reported_after_the_device_work(D):
+    """core.py:65-77: coordinates outside [0, L) are a ValueError.  The fused
+    device call reports them after its device work (no host round trip up
+    front); the binning kernels read coordinates through sane_coord, so a
+    NaN, a negative value, x >= L or a whole batch of unwrapped coordinates
+    neither faults nor piles up -- and the next valid call is untouched."""
+    dev = torch.device("cuda", 0)
+    L, N = 2.0, 20000
+    p = se.SEParams(xi=6.0, rc=0.5, M=32, P=8, window="bm", shape=20.0, eps=1e-8,
+                    **({"s0": 3.0, "R": 3.5} if D == 0 else {}))
+    peri = se.Periodicity(D)
+    s = rand_system(N, L, 11)
+    pos = torch.from_numpy(s.positions).to(dev)
+    q = torch.from_numpy(s.charges).to(dev)
+    good = sedev.total_potential(pos, q, L, p, peri).cpu().numpy()
+    ref = se.total_potential(s, p, peri)
+    assert np.linalg.norm(good - ref) <= 1e-12 * np.linalg.norm(ref)
+    for kind in ("nan", "negative", "at_L", "far", "half_unwrapped"):
+        bad = pos.clone()
+        if kind == "nan":
+            bad[7, 1] = float("nan")
+        elif kind == "negative":
+            bad[3, 0] = -1e-9
+        elif kind == "at_L":
+            bad[N - 1, 2] = L
+        elif kind == "far":
+            bad[5] = torch.tensor([1e300, -1e300, float("inf")], dtype=torch.float64)
+        else:
+            bad[: N // 2] += L  # unwrapped MD coordinates
+        for _ in range(3):  # eager, graph capture, graph replay
+            with pytest.raises(ValueError, match=r"\[0, L\)"):
+                sedev.total_potential(bad, q, L, p, peri)
+    again = sedev.total_potential(pos, q, L, p, peri).cpu().numpy()
+    assert np.max(np.abs(again - good)) <= 1e-13 * np.max(np.abs(good))
+
+
 def test_two_particle_single_term_and_cutoff():
     from scipy.special import erfc
     r = 0.2
