@@ -212,7 +212,12 @@ int se_kspace_potential_dev(se_plan_t plan, const double *pos, const double *q, 
  * particles (realspace.py:121-122,157,161). */
 int se_realspace_dev(se_plan_t plan, const double *pos, const double *q, int64_t N,
                      double *phi, int add_self);
-/* core.total_potential (core.py:194-216): phi = phi_R + phi_F + phi_self. */
+/* core.total_potential (core.py:194-216): phi = phi_R + phi_F + phi_self.
+ * Input errors (coordinates outside [0, L), core.py:65-77; a non-neutral
+ * periodic system, core.py:180-191; coincident particles) are returned as
+ * SE_EINVAL / SE_ESINGULAR like everywhere else, but are detected by a check
+ * kernel INSIDE the device work and read back with one synchronisation at
+ * the end of the call -- phi is undefined when the status is not SE_OK. */
 int se_total_potential_dev(se_plan_t plan, const double *pos, const double *q, int64_t N,
                            double *phi, double *timings);
 
