@@ -104,34 +104,64 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.
+
+    One nvidia-smi process per measurement, started BEFORE the warm-up (its
+    start-up takes longer than a short timed region) and read by a thread
+    that stamps every sample on arrival; `mark()` opens the timed window,
+    leaving the `with` block closes it, and only samples that arrived inside
+    the window are summarised."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, period_ms=50):
         self.index = index
+        self.period_ms = period_ms
         self.proc = None
+        self.samples = []  # (arrival time, line)
+        self.t0 = None
+        self.t1 = None
+
+    def _read(self):
+        try:
+            for l in self.proc.stdout:
+                if l.strip():
+                    self.samples.append((time.perf_counter(), l))
+        except Exception:
+            pass
 
     def __enter__(self):
+        import threading
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
         except Exception:
             self.proc = None
         return self
 
+    def mark(self):
+        """The timed region starts now."""
+        self.t0 = time.perf_counter()
+
     def __exit__(self, *exc):
-        self.lines = []
+        self.t1 = time.perf_counter()
         if self.proc is not None:
+            # one more period, so that a sample taken inside a region shorter
+            # than the period still arrives (it is stamped on arrival)
+            time.sleep(1e-3 * self.period_ms)
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except Exception:
-                out = ""
-            self.lines = [l for l in out.splitlines() if l.strip()]
+                pass
+            self.thread.join(timeout=2)
+        t0 = self.t0 if self.t0 is not None else -1.0
+        self.lines = [l for (t, l) in self.samples if t0 <= t <= self.t1 + 1e-3 * self.period_ms]
 
     def summary(self):
         sm, smax, reasons = [], [], set()
@@ -243,6 +273,21 @@ def cpu_sample(pos, q, threads=1, n_cells=2, n_kspace=20000, seed=0):
             "seconds": seconds}
 
 
+def config_dict(args, world):
+    """The `config` object of the JSON line -- the same for both arms."""
+    single = world == 1 and "RANK" not in os.environ
+    return {"workload": DESCR[CFG["workload"]], "N": CFG["N"], "seed": CFG["seed"],
+            "parallelism": ("single GPU (fused pipeline, CUDA graph)" if single else
+                            (f"domain decomposition x{world}: particles partitioned (contiguous "
+                             "chunks of the random input order), migrated to x-slabs of "
+                             "real-space columns, +x halo with Newton sums returned, touched "
+                             "grid planes to the k-space slab owners, slab FFT with two "
+                             "all-to-all transposes (D = 3)" if args.mode == "domain" else
+                             f"particle-shard x{world} with replicated inputs, {args.kspace} "
+                             "k-space")),
+            "l2": "flushed (256 MB write) between timed steps, outside the step events"}
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path (its port) on the host
     cores.  Each step is one bounded sample of the workload (cpu_sample);
@@ -272,7 +317,7 @@ def run_reference(args):
             "ms_per_step": 1e3 * statistics.mean(secs), "wall_s_timed_region": t_wall,
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.md 3.1)",
-            "config": {"workload": DESCR[CFG["workload"]], "N": CFG["N"], "seed": CFG["seed"]},
+            "config": config_dict(args, int(os.environ.get("WORLD_SIZE", "1"))),
             "cpu_baseline": {"value": value, "unit": "particles/s", "cores": threads, "kind": "port",
                              "sample": last["sample"]},
             "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -403,6 +448,8 @@ def measure(name, args, dev, world, rank, sharded, steps, warmup, extras=True):
         def step():
             return sedev.total_potential(pos_d, q_d, L, prm, peri, out=phi_d)
 
+    clk = ClockSampler(local)
+    clk.__enter__()  # running before the warm-up; the timed window opens at clk.mark()
     plan.set_profiling(True)
     for _ in range(max(3, warmup)):
         step()
@@ -423,7 +470,8 @@ def measure(name, args, dev, world, rank, sharded, steps, warmup, extras=True):
     if sharded:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
+    try:
+        clk.mark()
         t_wall0 = time.perf_counter()
         for i in range(steps):
             flush.zero_()
@@ -434,6 +482,8 @@ def measure(name, args, dev, world, rank, sharded, steps, warmup, extras=True):
         if sharded:
             dist.barrier()
         t_wall = time.perf_counter() - t_wall0
+    finally:
+        clk.__exit__(None, None, None)
     launches = plan.launches() - launches0
     ktimes = plan.kernel_times()
     plan.set_profiling(False)
@@ -604,17 +654,7 @@ def run_ours(args):
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.md 3.1; no public dataset exists for this path)",
-            "config": {"workload": DESCR[CFG["workload"]], "N": N, "seed": CFG["seed"],
-                       "parallelism": ("single GPU (fused pipeline, CUDA graph)" if world == 1 and not
-                                       ("RANK" in os.environ) else
-                                       (f"domain decomposition x{world}: particles partitioned (contiguous "
-                                        "chunks of the random input order), migrated to x-slabs of "
-                                        "real-space columns, +x halo with Newton sums returned, touched "
-                                        "grid planes to the k-space slab owners, slab FFT with two "
-                                        "all-to-all transposes (D = 3)" if args.mode == "domain" else
-                                        f"particle-shard x{world} with replicated inputs, {args.kspace} "
-                                        "k-space")),
-                       "l2": "flushed (256 MB write) between timed steps, outside the step events"},
+            "config": config_dict(args, world),
             "e2e": m["e2e"], "roofline": roofline, "kernels": kern,
             "spread_gather": spread_gather,
             "kernels_note": ("event spans per stage on the stream it runs on; the k-space pipeline "
