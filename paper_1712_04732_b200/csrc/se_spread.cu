@@ -298,20 +298,43 @@ struct TileC {
     static constexpr int plane = Tp * pitch;
 };
 
-template <int PC>
+// Lanes per row of pairs: pi = lane + LW it.  With LW a multiple of P a
+// lane's z offset tz = pi mod P is the same in every iteration, so its z
+// factor is loaded ONCE per particle (one shared-memory wavefront per
+// iteration less): P = 8, 16 have LW = 32 anyway; P = 10 uses 30 lanes (4
+// iterations of 30, 30, 30, 10 pairs instead of 32, 32, 32, 4: the same
+// number of tile wavefronts, 5 factor loads instead of 8).  For lanes < LW
+// the bank pattern is the one described above (offset == pi mod 16).
+#ifndef SE_LANEPAIR_TZ
+#define SE_LANEPAIR_TZ 1
+#endif
+// The (y, z) products before the plane's read-modify-writes (all factor
+// loads issued first): P = 8 (round 2, first session), and with the single
+// z-factor load also P = 10, 12 (-3% / -2.5% spread; P = 16: +5%, not used).
+#ifndef SE_YZ_FIRST_MAXP
+#define SE_YZ_FIRST_MAXP 12
+#endif
+constexpr bool yz_first(int PC) { return wts_transposed(PC) || (PC > 0 && PC <= SE_YZ_FIRST_MAXP); }
+constexpr int lanepair_width(int PC, bool narrow) { return (SE_LANEPAIR_TZ && narrow && PC == 10) ? 30 : 32; }
+// NARROW: the spreading kernels (measured at P = 10: spread -9%, the gather
+// +12..20% -- it keeps 32 lanes).
+template <int PC, bool NARROW = true>
 struct LanePairs {
-    static constexpr int NPI = PC > 0 ? (PC * PC + 31) / 32 : 1;
+    static constexpr int LW = lanepair_width(PC, NARROW);
+    static constexpr int NPI = PC > 0 ? (PC * PC + LW - 1) / LW : 1;
+    // every iteration of a lane has the same tz
+    static constexpr bool TZC = SE_LANEPAIR_TZ && PC > 0 && LW % (PC > 0 ? PC : 1) == 0;
     int ty[NPI], tz[NPI], off[NPI];
     __device__ __forceinline__ void init(int lane, int pitch) {
 #pragma unroll
         for (int it = 0; it < NPI; ++it) {
-            const int pi = lane + 32 * it;
+            const int pi = lane + LW * it;
             ty[it] = pi / (PC > 0 ? PC : 1);
             tz[it] = pi - ty[it] * (PC > 0 ? PC : 1);
             off[it] = ty[it] * pitch + tz[it];
         }
     }
-    __device__ __forceinline__ bool valid(int lane, int it) const { return lane + 32 * it < PC * PC; }
+    __device__ __forceinline__ bool valid(int lane, int it) const { return lane < LW && lane + LW * it < PC * PC; }
 };
 
 template <int WIN, int PC>
@@ -360,11 +383,15 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
                 t0 = t0 < 0 ? t0 + PC : t0;
                 const double wxt = wx[t0 * S];
                 double *base = tile + (lx0 + t0) * plane + ly0 * pitch + lz0;
-                if (wts_transposed(PC)) {
+                // z factor: one load per particle when tz does not depend on it
+                const double wzc = LanePairs<PC>::TZC ? wz[lp.tz[0] * S] : 0.0;
+                if (yz_first(PC)) {
                     double yz[LanePairs<PC>::NPI];
 #pragma unroll
                     for (int it = 0; it < LanePairs<PC>::NPI; ++it)
-                        yz[it] = lp.valid(lane, it) ? __dmul_rn(wy[lp.ty[it] * S], wz[lp.tz[it] * S]) : 0.0;
+                        yz[it] = lp.valid(lane, it)
+                                     ? __dmul_rn(wy[lp.ty[it] * S], LanePairs<PC>::TZC ? wzc : wz[lp.tz[it] * S])
+                                     : 0.0;
 #pragma unroll
                     for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
                         if (lp.valid(lane, it)) {
@@ -377,7 +404,8 @@ __global__ void __launch_bounds__(512) spread_tile_kernel(const double4 *__restr
                     for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
                         if (lp.valid(lane, it)) {
                             double *c = base + lp.off[it];
-                            *c = fma(wxt, __dmul_rn(wy[lp.ty[it] * S], wz[lp.tz[it] * S]), *c);
+                            *c = fma(wxt, __dmul_rn(wy[lp.ty[it] * S], LanePairs<PC>::TZC ? wzc : wz[lp.tz[it] * S]),
+                                     *c);
                         }
                     }
                 }
@@ -526,9 +554,10 @@ __global__ void __launch_bounds__(32 * (kSwsC + kSwsP), 3) spread_ws_kernel(cons
                 const double wxt = wx[t0 * S];
                 double *base = tile + (lx0 + t0) * plane + ly0 * pitch + lz0;
                 double yz[LanePairs<PC>::NPI];
+                const double wzc = LanePairs<PC>::TZC ? wz[lp.tz[0] * S] : 0.0;  // tz is the same in both iterations
 #pragma unroll
                 for (int it = 0; it < LanePairs<PC>::NPI; ++it)
-                    yz[it] = __dmul_rn(wy[lp.ty[it] * S], wz[lp.tz[it] * S]);
+                    yz[it] = __dmul_rn(wy[lp.ty[it] * S], LanePairs<PC>::TZC ? wzc : wz[lp.tz[it] * S]);
 #pragma unroll
                 for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
                     double *c = base + lp.off[it];
@@ -585,7 +614,7 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
     asm volatile("cp.async.wait_all;" ::: "memory");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = a.nwarps;
     const int npair = P * P;
-    LanePairs<PC> lp;
+    LanePairs<PC, false> lp;
     lp.init(lane, pitch);
     for (int b0 = ubeg; b0 < uend; b0 += BATCH) {
         int nb = min(BATCH, uend - b0);
@@ -602,14 +631,15 @@ __global__ void __launch_bounds__(512, (PC >= 10 ? 2 : 0)) gather_tile_kernel(co
             double acc = 0.0;
             if (PC > 0) {
                 const double *base = tile + lx0 * plane + ly0 * pitch + lz0;
+                const double wzc = LanePairs<PC, false>::TZC ? wz[lp.tz[0] * S] : 0.0;
 #pragma unroll
-                for (int it = 0; it < LanePairs<PC>::NPI; ++it) {
+                for (int it = 0; it < LanePairs<PC, false>::NPI; ++it) {
                     if (lp.valid(lane, it)) {
                         const double *c = base + lp.off[it];
                         double s = 0.0;
 #pragma unroll
                         for (int t = 0; t < PC; ++t) s = fma(wx[t * S], c[t * plane], s);
-                        acc = fma(__dmul_rn(wy[lp.ty[it] * S], wz[lp.tz[it] * S]), s, acc);
+                        acc = fma(__dmul_rn(wy[lp.ty[it] * S], LanePairs<PC, false>::TZC ? wzc : wz[lp.tz[it] * S]), s, acc);
                     }
                 }
             } else {
