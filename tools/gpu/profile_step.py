@@ -4,7 +4,7 @@
 
 Warm-up evaluations (tables, cuFFT plans, CUDA graph) run outside the
 profiler range; exactly one device-resident evaluation of the workload --
-or, with stage = spread | gather | realspace, one call of that stage --
+or, with stage = spread | gather | kspace | realspace, one call of that stage --
 runs between cudaProfilerStart / cudaProfilerStop, so the ncu launch list
 and --set full captures are of the same build and inputs the bench times.
 """
@@ -48,6 +48,8 @@ def main():
             _native.call("se_spread_dev", pl.handle, _native.ptr(pos), _native.ptr(q), N, _native.ptr(grid))
         elif stage == "gather":
             _native.call("se_gather_dev", pl.handle, _native.ptr(grid), _native.ptr(pos), N, _native.ptr(phi), 0)
+        elif stage == "kspace":
+            _native.call("se_kspace_apply_dev", pl.handle, _native.ptr(grid), 1, None)
         elif stage == "realspace":
             _native.call("se_realspace_dev", pl.handle, _native.ptr(pos), _native.ptr(q), N, _native.ptr(phi), 1)
         else:

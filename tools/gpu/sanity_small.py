@@ -8,7 +8,8 @@ import warnings
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, ROOT)
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tools")]
+import workloads  # noqa: E402
 import paper_1712_04732_b200 as se  # noqa: E402
 
 rng = np.random.default_rng(0)
@@ -28,4 +29,14 @@ for D in (0, 1, 2, 3):
 s = se.ParticleSystem(rng.random((50, 3)), np.r_[np.ones(25), -np.ones(25)], 1.0)
 p = se.SEParams(xi=12.0, rc=0.4, M=64, P=34, window="kb", shape=85.0, eps=1e-12)
 se.se_kspace(s, p, se.Periodicity(3))
+# the compile-time-P tile kernels (spread: 30-lane pair rows at P = 10, the
+# warp-specialised kernel at P = 8), ES and Gaussian windows, D = 3 and D = 1
+s = se.ParticleSystem(rng.random((3000, 3)) * 2.0, np.r_[np.ones(1500), -np.ones(1500)], 2.0)
+for P in (4, 6, 8, 10, 12, 16):
+    for window, shape in (("bm", 2.5 * P), ("gaussian", float(np.sqrt(P * np.pi)))):
+        for D in (3, 1):
+            p = se.SEParams(xi=6.0, rc=0.5, M=32, P=P, window=window, shape=shape, eps=1e-8,
+                            **({} if D == 3 else dict(s0=2.5, s=3.0, nI=6, R=workloads._R(1, 2.0, 32, P, 2.5))))
+            phi = se.se_kspace(s, p, se.Periodicity(D))
+            assert np.all(np.isfinite(phi))
 print("sanity ok")
