@@ -599,6 +599,72 @@ __device__ __forceinline__ void dense_batch_poly(WB &wb, int lane, int j, int m,
     __syncwarp();
 }
 
+// Dense batch of the Newton field (DEG > 0: the polynomial pair factor
+// g = w^2 (w - R(r^2)), hit_value_field_poly): the structure of
+// dense_batch_poly with three components -- the target side E_t += q_s g d
+// (d = x_t - x_s) into the lane-owned rows acc[c][slot][lane], the source
+// side E_s -= q_t g d in registers, leaving with three REDG per source and
+// batch instead of three per pair.
+template <int DEG, bool OWN, class WB>
+__device__ __forceinline__ void dense_batch_field_poly(WB &wb, int lane, int j, int m, double xs, double ys, double zs,
+                                                       double qs, const RealArgs &a, unsigned amask, int tbase,
+                                                       double *__restrict__ acc_s, int &singular) {
+    constexpr int NT = SE_DENSE_NT;
+    unsigned vt = 0xffffu;
+    if (OWN) {
+        const int c = min(max(j - tbase, 0), kT);
+        vt = amask & ((1u << c) - 1u);
+    }
+    const long long lim = __double_as_longlong(a.rc2x);
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    bool sing = false;
+#pragma unroll 1
+    for (int t = 0; t < kT; t += NT) {
+        int sl[NT];
+        double dx[NT], dy[NT], dz[NT], qt[NT], u[NT], y[NT], tv[NT], p[NT];
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+            sl[k] = tslot(t + k);
+            const double2 p01 = wb.txy[sl[k]], p23 = wb.tzq[sl[k]];
+            dx[k] = p01.x - xs;
+            dy[k] = p01.y - ys;
+            dz[k] = p23.x - zs;
+            qt[k] = p23.y;
+            u[k] = fma(dz[k], dz[k], fma(dy[k], dy[k], dx[k] * dx[k]));
+            y[k] = rsqrt_nr(u[k]);
+            tv[k] = fma(u[k], a.pscale, -1.0);
+            p[k] = a.pc[DEG];
+        }
+#pragma unroll
+        for (int i = DEG - 1; i >= 0; --i) {
+#pragma unroll
+            for (int k = 0; k < NT; ++k) p[k] = fma(p[k], tv[k], a.pc[i]);
+        }
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+            bool ok = below_bits(u[k], lim);
+            if (OWN) ok = ok && ((vt >> (t + k)) & 1u);
+            sing = sing || (ok && __double2hiint(y[k]) > 0x42D6BCC4);  // r < 1e-14
+            const double g = ok ? (y[k] * y[k]) * (y[k] - p[k]) : 0.0;
+            const double gs = qs * g, gt = qt[k] * g;
+            double *s0 = &wb.acc[0][sl[k]][lane], *s1 = &wb.acc[1][sl[k]][lane], *s2 = &wb.acc[2][sl[k]][lane];
+            *s0 = fma(gs, dx[k], *s0);
+            *s1 = fma(gs, dy[k], *s1);
+            *s2 = fma(gs, dz[k], *s2);
+            ax = fma(-gt, dx[k], ax);
+            ay = fma(-gt, dy[k], ay);
+            az = fma(-gt, dz[k], az);
+        }
+    }
+    singular |= sing ? 1 : 0;
+    if (lane < m) {
+        atomicAdd(acc_s + 3 * lane, ax);
+        atomicAdd(acc_s + 3 * lane + 1, ay);
+        atomicAdd(acc_s + 3 * lane + 2, az);
+    }
+    __syncwarp();
+}
+
 // One batch of <= 32 candidate sources [jb, jb+m) of a neighbour-cell run:
 //  1. fp32 prefilter of all 16 x m (target, source) pairs: lane l tests
 //     targets (l % 8, l % 8 + 8) against sources 8 (l / 8) .. + 7, two tests
@@ -690,8 +756,17 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
         hit &= ~(spread(excl(tbase + pt.ta)) | (spread(excl(tbase + pt.tb)) << 1));
     }
     const int c = __popc(hit);
-    if (!COUNT && !FLD && NEWTON && __reduce_add_sync(0xffffffffu, (unsigned)c) >= (unsigned)a.dense_min) {
-        if (DEG > 0) {
+    if (!COUNT && NEWTON && (!FLD || DEGF > 0) &&
+        __reduce_add_sync(0xffffffffu, (unsigned)c) >= (unsigned)a.dense_min) {
+        if constexpr (FLD) {
+            constexpr int DF = DEGF > 0 ? DEGF : 1;
+            if (hs >= 0)
+                dense_batch_field_poly<DF, true>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, acc_src + 3 * jb,
+                                                 singular);
+            else
+                dense_batch_field_poly<DF, false>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, acc_src + 3 * jb,
+                                                  singular);
+        } else if (DEG > 0) {
             if (hs >= 0)
                 dense_batch_poly<DEG, true>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, acc_src + jb, singular);
             else
@@ -788,8 +863,8 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
     const double4 *__restrict__ rec, const int *__restrict__ sidx, const int *__restrict__ starts,
     const int4 *__restrict__ units, const int *__restrict__ nunits, RealArgs a, double *__restrict__ phi,
     double *__restrict__ acc_src, int *__restrict__ flag, unsigned long long *__restrict__ npairs) {
-    static_assert(DEG == 0 || (!MI && !COUNT && !WIDE && (FLD ? !NEWTON : NEWTON)),
-                  "polynomial pair term: the Newton potential and the full-shell field paths");
+    static_assert(DEG == 0 || (!MI && !COUNT && !WIDE && (FLD || NEWTON)),
+                  "polynomial pair term: the Newton potential and the field (Newton or full shell) paths");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpBufT<FLD> &wb = reinterpret_cast<WarpBufT<FLD> *>(smem_raw)[warp];
@@ -1205,14 +1280,25 @@ static void cell_bin(se_plan *pl, const double *pos, const double *q, int64_t N,
     prof_end(pl, SE_K_SORT);
 }
 
-// The full shell without Newton's third law: in the deterministic mode
-// (no source-side atomics) and for the field, where the three source-side
-// fp64 atomics per pair cost more than evaluating every pair twice
-// (cfg2: 30.5 ms full shell against 33.9 ms with Newton, B200)
+// The full shell without Newton's third law: in the deterministic mode (no
+// source-side atomics), and for the field when its polynomial pair factor is
+// not available -- all of the erfc-path field's pairs go through the
+// compacted path with three source-side fp64 atomics each, which costs more
+// than evaluating every pair twice (cfg2: 30.5 ms full shell against 33.9 ms
+// with Newton).  With the polynomial factor the field runs the half shell
+// with Newton like the potential: its dense batches keep the source side in
+// registers (three REDG per source and batch, dense_batch_field_poly).
 // (the domain decomposition relies on the +x half shell: Newton there)
+static bool narrow_erfc(const RealArgs &a) { return !(a.xi * a.rc * (1.0 + 1e-4) > SE_ERFC_XMAX); }
 template <bool FLD>
-static bool full_shell(const se_plan *pl) {
-    return pl->dom.ncols == 0 && (FLD || pl->deterministic);
+static bool full_shell(const se_plan *pl, const RealArgs &a) {
+    if (pl->dom.ncols != 0) return false;
+    if (pl->deterministic) return true;
+    static const bool newton_field = [] {
+        const char *e = std::getenv("SE_B200_FIELD_NEWTON");  // A/B: 0 = the full-shell field
+        return !(e && std::atoi(e) == 0);
+    }();
+    return FLD && !(newton_field && a.pdeg > 0 && narrow_erfc(a));
 }
 
 template <bool COUNT, bool FLD = false>
@@ -1227,7 +1313,7 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
     const bool mi = c.mode[0] == 2 || c.mode[1] == 2 || c.mode[2] == 2;
     // deterministic mode: no Newton (no source-side atomics), each target
     // sums its own partners in a fixed order
-    const bool full = mi || full_shell<FLD>(pl);
+    const bool full = mi || full_shell<FLD>(pl, a);
     unsigned blocks = (unsigned)((maxu + kWarps - 1) / kWarps);
     cudaStream_t st = pl->stream;
     const size_t smem = sizeof(WarpBufT<FLD>) * kWarps;
@@ -1276,6 +1362,17 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
             default:
                 args(wide ? realspace_cell_kernel<false, false, true, true, false>
                           : realspace_cell_kernel<false, false, true, false, false>);
+        }
+    } else if constexpr (!COUNT && FLD) {
+        // the Newton field: only with the polynomial pair factor (full_shell)
+        switch (wide ? 0 : a.pdeg) {
+            case 20: args(realspace_cell_kernel<false, false, true, false, true, 20>); break;
+            case 24: args(realspace_cell_kernel<false, false, true, false, true, 24>); break;
+            case 28: args(realspace_cell_kernel<false, false, true, false, true, 28>); break;
+            case 32: args(realspace_cell_kernel<false, false, true, false, true, 32>); break;
+            default:
+                args(wide ? realspace_cell_kernel<false, false, true, true, true>
+                          : realspace_cell_kernel<false, false, true, false, true>);
         }
     } else
         args(wide ? realspace_cell_kernel<false, COUNT, true, true, FLD>
@@ -1330,7 +1427,7 @@ static void realspace_impl(se_plan *pl, const double *pos, const double *q, int6
         prof_end(pl, SE_K_REALSPACE);
         pl->launches += 1;
     } else {
-        cell_bin(pl, pos, q, N, a, full_shell<FLD>(pl));
+        cell_bin(pl, pos, q, N, a, full_shell<FLD>(pl, a));
         launch_cell<false, FLD>(pl, N, a, phi, nullptr);
     }
 }
@@ -1392,7 +1489,7 @@ void realspace_pair_count(se_plan *pl, const double *pos, const double *q, int64
     SE_CUDA(cudaMemsetAsync(pl->flag.ptr, 0, sizeof(int) * 4, pl->stream));
     pl->pairs.ensure(sizeof(unsigned long long));
     SE_CUDA(cudaMemsetAsync(pl->pairs.ptr, 0, sizeof(unsigned long long), pl->stream));
-    cell_bin(pl, pos, q, N, a, full_shell<false>(pl));
+    cell_bin(pl, pos, q, N, a, full_shell<false>(pl, a));
     launch_cell<true>(pl, N, a, nullptr, pl->pairs.as<unsigned long long>());
     unsigned long long h = 0;
     SE_CUDA(cudaMemcpyAsync(&h, pl->pairs.ptr, sizeof(h), cudaMemcpyDeviceToHost, pl->stream));

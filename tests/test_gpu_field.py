@@ -223,3 +223,29 @@ def test_field_dlt3_rejects_es_window():
     p = se.SEParams(xi=7.0, rc=0.45, M=20, P=8, window="bm", shape=20.0, s0=3.0, s=2.0, nI=4, R=2.0)
     with pytest.raises(ValueError):
         se.total_field(se.ParticleSystem(pos, q, 1.0), p, se.Periodicity(2))
+
+
+@pytest.mark.parametrize("D", [0, 1, 2, 3])
+def test_field_newton_dense_batches_match_full_shell(D):
+    # a dense system (~2000 partners per particle: most batches take the
+    # dense Newton path, dense_batch_field_poly) against the deterministic
+    # mode's full-shell field, which sums every target's partners itself
+    N, L = 30000, 1.0
+    pos, q = _system(N, L, 77 + D)
+    xi, rc = 14.0, 0.25
+    from paper_1712_04732_b200.realspace import real_space_field
+
+    system = se.ParticleSystem(pos, q, L)
+    e_newton = real_space_field(system, xi, rc, se.Periodicity(D))
+    se.set_deterministic(True)
+    try:
+        e_full = real_space_field(system, xi, rc, se.Periodicity(D))
+    finally:
+        se.set_deterministic(False)
+    assert _rel(e_newton, e_full) < 1e-13
+    # Newton's third law pairwise: the real-space forces sum to zero
+    F = q[:, None] * e_newton
+    assert np.abs(F.sum(0)).max() < 1e-11 * np.abs(F).sum(0).max()
+    sel = np.random.default_rng(5).choice(N, 40, replace=False)
+    ref = orc.realspace_field(pos, q, L, D, xi, rc, targets=sel)
+    assert _rel(e_newton[sel], ref) < 1e-12
