@@ -389,9 +389,11 @@ __device__ __forceinline__ Hit eval_hit(unsigned en, const RealArgs &a, const WB
 // compacted hit (slot tt, source k) -> h.f = erfc(xi r)/r, 0 outside the
 // cutoff or for an invalid (duplicate) slot.  Any zero distance among the
 // hits is a coincidence (the self pair is never compacted with NEWTON).
-template <int DEG, class WB>
+// Without NEWTON (the deterministic mode's full shell) the prefilter also
+// passes the self pair (source jb + k == target tbase + t): dropped, not flagged.
+template <int DEG, bool NEWTON = true, class WB>
 __device__ __forceinline__ void hit_poly(unsigned en, bool valid, const RealArgs &a, const WB &wb, int &singular,
-                                         Hit &h) {
+                                         Hit &h, int jb = 0, int tbase = 0) {
     h.tt = (int)(en >> 5);
     h.k = (int)(en & 31u);
     const double2 t01 = wb.txy[h.tt], t23 = wb.tzq[h.tt];
@@ -401,8 +403,14 @@ __device__ __forceinline__ void hit_poly(unsigned en, bool valid, const RealArgs
     // u >= 0: the order of its bit pattern is the order of its value, so both
     // tests run on the integer pipe (a DSETP occupies the fp64 pipe)
     const long long ub = __double_as_longlong(u);
-    singular |= ub < 0x3A1FB0F6BE506019LL ? 1 : 0;  // u < 1e-28
-    h.ok = valid && ub < __double_as_longlong(a.rc2x);
+    const bool zero = ub < 0x3A1FB0F6BE506019LL;  // u < 1e-28
+    if (NEWTON) {
+        singular |= zero ? 1 : 0;
+        h.ok = valid && ub < __double_as_longlong(a.rc2x);
+    } else {
+        singular |= (valid && zero && jb + h.k != tbase + tslot(h.tt)) ? 1 : 0;
+        h.ok = valid && !zero && ub < __double_as_longlong(a.rc2x);
+    }
     const double f = pair_poly<DEG>(u, a);
     h.f = h.ok ? f : 0.0;
     h.qt = t23.y;
@@ -548,15 +556,23 @@ __device__ __forceinline__ bool below_bits(double u, long long lim) { return __d
 #define SE_DENSE_UNROLL 1  // measured: 1 beats 2 by 2-4% (cfg2, cfg5, cfg4)
 #endif
 constexpr int kDenseUnroll = SE_DENSE_UNROLL;
-template <int DEG, bool OWN, class WB>
+// Without NEWTON (the full shell of the deterministic mode: every target sums
+// all its partners, no source side) the own column (OWN) drops only the self
+// pair t == j, and nothing leaves through atomics.
+template <int DEG, bool OWN, bool NEWTON = true, class WB>
 __device__ __forceinline__ void dense_batch_poly(WB &wb, int lane, int j, int m, double xs, double ys, double zs,
                                                  double qs, const RealArgs &a, unsigned amask, int tbase,
                                                  double *__restrict__ acc_s, int &singular) {
     constexpr int NT = SE_DENSE_NT;
     unsigned vt = 0xffffu;
     if (OWN) {
-        const int c = min(max(j - tbase, 0), kT);
-        vt = amask & ((1u << c) - 1u);
+        if (NEWTON) {
+            const int c = min(max(j - tbase, 0), kT);
+            vt = amask & ((1u << c) - 1u);
+        } else {
+            const int c = j - tbase;
+            vt = amask & ~((c >= 0 && c < kT) ? (1u << c) : 0u);
+        }
     }
     const long long lim = __double_as_longlong(a.rc2x);  // r^2 >= 0: bit order = value order
     double accs = 0.0;
@@ -591,11 +607,11 @@ __device__ __forceinline__ void dense_batch_poly(WB &wb, int lane, int j, int m,
             const double w = ok ? y[k] - p[k] : 0.0;
             double *slot = &wb.acc[0][sl[k]][lane];
             *slot = fma(qs, w, *slot);
-            accs = fma(p23[k].y, w, accs);
+            if (NEWTON) accs = fma(p23[k].y, w, accs);
         }
     }
     singular |= sing ? 1 : 0;
-    if (lane < m) atomicAdd(acc_s + lane, accs);
+    if (NEWTON && lane < m) atomicAdd(acc_s + lane, accs);
     __syncwarp();
 }
 
@@ -756,9 +772,14 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
         hit &= ~(spread(excl(tbase + pt.ta)) | (spread(excl(tbase + pt.tb)) << 1));
     }
     const int c = __popc(hit);
-    if (!COUNT && NEWTON && (!FLD || DEGF > 0) &&
+    if (!COUNT && (FLD ? (NEWTON && DEGF > 0) : (NEWTON || DEG > 0)) &&
         __reduce_add_sync(0xffffffffu, (unsigned)c) >= (unsigned)a.dense_min) {
-        if constexpr (FLD) {
+        if constexpr (!NEWTON && !FLD) {
+            // full shell (deterministic mode): every batch may hold the unit's own
+            // targets as sources; the self pair is dropped by its index
+            dense_batch_poly<(DEG > 0 ? DEG : 1), true, false>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase,
+                                                               nullptr, singular);
+        } else if constexpr (FLD) {
             constexpr int DF = DEGF > 0 ? DEGF : 1;
             if (hs >= 0)
                 dense_batch_field_poly<DF, true>(wb, lane, j, m, xs, ys, zs, qs, a, pt.amask, tbase, acc_src + 3 * jb,
@@ -800,8 +821,8 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
             const unsigned en2 = v2 ? wb.ent[e0 + 32 + lane] : en1;
             Hit h1, h2;
             if (DEG > 0) {
-                hit_poly<(DEG > 0 ? DEG : 1)>(en1, true, a, wb, singular, h1);
-                hit_poly<(DEG > 0 ? DEG : 1)>(en2, v2, a, wb, singular, h2);
+                hit_poly<(DEG > 0 ? DEG : 1), NEWTON>(en1, true, a, wb, singular, h1, jb, tbase);
+                hit_poly<(DEG > 0 ? DEG : 1), NEWTON>(en2, v2, a, wb, singular, h2, jb, tbase);
             } else {
                 const double x1 = hit_geometry<MI, NEWTON, FLD>(en1, true, a, wb, jb, tbase, singular, h1);
                 const double x2 = hit_geometry<MI, NEWTON, FLD>(en2, v2, a, wb, jb, tbase, singular, h2);
@@ -822,7 +843,7 @@ __device__ __forceinline__ void pair_batch(const double4 *__restrict__ rec, int 
         } else if (lane < rem) {
             Hit h;
             if (DEG > 0) {
-                hit_poly<(DEG > 0 ? DEG : 1)>(wb.ent[e0 + lane], true, a, wb, singular, h);
+                hit_poly<(DEG > 0 ? DEG : 1), NEWTON>(wb.ent[e0 + lane], true, a, wb, singular, h, jb, tbase);
             } else if (FLD && DEGF > 0) {
                 hit_geometry<MI, NEWTON, FLD>(wb.ent[e0 + lane], true, a, wb, jb, tbase, singular, h);
                 hit_value_field_poly<(DEGF > 0 ? DEGF : 1)>(a, h);
@@ -863,8 +884,7 @@ __global__ void __launch_bounds__(32 * kWarps, FLD ? kMinBlocksField : kMinBlock
     const double4 *__restrict__ rec, const int *__restrict__ sidx, const int *__restrict__ starts,
     const int4 *__restrict__ units, const int *__restrict__ nunits, RealArgs a, double *__restrict__ phi,
     double *__restrict__ acc_src, int *__restrict__ flag, unsigned long long *__restrict__ npairs) {
-    static_assert(DEG == 0 || (!MI && !COUNT && !WIDE && (FLD || NEWTON)),
-                  "polynomial pair term: the Newton potential and the field (Newton or full shell) paths");
+    static_assert(DEG == 0 || (!MI && !COUNT && !WIDE), "polynomial pair term: cell path, narrow erfc range");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpBufT<FLD> &wb = reinterpret_cast<WarpBufT<FLD> *>(smem_raw)[warp];
@@ -1346,6 +1366,17 @@ static void launch_cell(se_plan *pl, int64_t N, const RealArgs &a, double *phi, 
                 default:
                     args(wide ? realspace_cell_kernel<false, false, false, true, true>
                               : realspace_cell_kernel<false, false, false, false, true>);
+            }
+        } else if constexpr (!FLD && !COUNT) {
+            // the deterministic potential: polynomial pair term and dense batches too
+            switch (wide ? 0 : a.pdeg) {
+                case 20: args(realspace_cell_kernel<false, false, false, false, false, 20>); break;
+                case 24: args(realspace_cell_kernel<false, false, false, false, false, 24>); break;
+                case 28: args(realspace_cell_kernel<false, false, false, false, false, 28>); break;
+                case 32: args(realspace_cell_kernel<false, false, false, false, false, 32>); break;
+                default:
+                    args(wide ? realspace_cell_kernel<false, false, false, true, false>
+                              : realspace_cell_kernel<false, false, false, false, false>);
             }
         } else {
             args(wide ? realspace_cell_kernel<false, COUNT, false, true, FLD>

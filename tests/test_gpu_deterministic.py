@@ -86,3 +86,29 @@ def test_coincident_z_layer(det):
     se.set_deterministic(False)
     c = se.real_space_sum(s, 6.0, 0.5, se.Periodicity(2))
     assert se.relative_rms_error(c, ref) < 1e-13
+
+
+@pytest.mark.parametrize("D", [3, 1, 0])
+def test_dense_full_shell_matches_newton_and_oracle(det, D):
+    # ~2000 partners per particle: most batches of the deterministic mode's
+    # full shell take the dense path (dense_batch_poly without Newton: the
+    # self pair dropped by its index, no source side), the rest the
+    # compacted path with the polynomial pair term
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import se_oracle as orc
+
+    s = _system(30000, 1.0, 90 + D)
+    xi, rc = 14.0, 0.25
+    peri = se.Periodicity(D)
+    a = se.real_space_sum(s, xi, rc, peri)
+    b = se.real_space_sum(s, xi, rc, peri)
+    assert np.array_equal(a, b)
+    se.set_deterministic(False)
+    ref = se.real_space_sum(s, xi, rc, peri)
+    assert se.relative_rms_error(a, ref) < 1e-14
+    sel = np.random.default_rng(6).choice(s.N, 40, replace=False)
+    want = orc.realspace(s.positions, s.charges, s.L, D, xi, rc, targets=sel)
+    assert se.relative_rms_error(a[sel], want) < 1e-13
