@@ -1,5 +1,8 @@
+"""cfg2 real-space stage time (binning + kernel, CUDA events) in the default
+(Newton) and the deterministic (full shell) mode.   python tools/gpu/det_time.py"""
 import sys, os, numpy as np, torch
-sys.path[:0]=['/root/repo','/root/repo/tools']
+ROOT=os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path[:0]=[ROOT,os.path.join(ROOT,'tools')]
 import workloads, paper_1712_04732_b200 as se
 from paper_1712_04732_b200 import _native, device as sedev
 w=workloads.ALL['cfg2'](); dev=torch.device('cuda',0)
