@@ -39,4 +39,21 @@ for P in (4, 6, 8, 10, 12, 16):
                             **({} if D == 3 else dict(s0=2.5, s=3.0, nI=6, R=workloads._R(1, 2.0, 32, P, 2.5))))
             phi = se.se_kspace(s, p, se.Periodicity(D))
             assert np.all(np.isfinite(phi))
+# fields (every D; Gaussian window for D < 3), default and deterministic mode,
+# and a dense system whose real-space batches take the dense (Newton and
+# full-shell) paths as well as the compacted ones
+from paper_1712_04732_b200.realspace import real_space_field, real_space_sum  # noqa: E402
+
+dense = se.ParticleSystem(rng.random((6000, 3)), np.r_[np.ones(3000), -np.ones(3000)], 1.0)
+for det in (False, True):
+    se.set_deterministic(det)
+    for D in (0, 1, 2, 3):
+        s = se.ParticleSystem(rng.random((700, 3)) * 2.0, np.r_[np.ones(350), -np.ones(350)], 2.0)
+        p, _ = se.auto_params(s, se.Periodicity(D), 5.0, 1e-8, window="gaussian")
+        E = se.total_field(s, p, se.Periodicity(D))
+        phi = se.total_potential(s, p, se.Periodicity(D))
+        assert np.all(np.isfinite(E)) and np.all(np.isfinite(phi))
+        assert np.all(np.isfinite(real_space_sum(dense, 14.0, 0.25, se.Periodicity(D))))
+        assert np.all(np.isfinite(real_space_field(dense, 14.0, 0.25, se.Periodicity(D))))
+se.set_deterministic(False)
 print("sanity ok")
