@@ -676,7 +676,9 @@ def run_ours(args):
         load_workload(args.workload)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         pos_h, q_h = make_inputs()
-        line["cpu_baseline"] = cpu_sample(pos_h, q_h, threads=1)
+        big = args.workload.startswith("cfg2")  # ~12 s of CPU work at cfg2; clustered cfg5 cells stay at 2
+        line["cpu_baseline"] = cpu_sample(pos_h, q_h, threads=1, n_cells=6 if big else 2,
+                                          n_kspace=60000 if big else 20000)
     if rank == 0:
         emit(line)
     if sharded:
